@@ -1,0 +1,20 @@
+"""Seeded synthetic inputs shared by the oracle tests, the GPU tests and bench.py.
+
+This package draws random systems and points and converts high-precision
+reals into DD/QD limbs.  It holds none of the method's arithmetic: no
+monomial, derivative, Speelpenning or DD/QD arithmetic lives here.
+"""
+from .systems import (  # noqa: F401
+    CONFIGS,
+    SystemArrays,
+    config_system,
+    random_system,
+    unit_circle_limbs,
+    split_limbs,
+    limbs_from_values,
+    special_linear_system,
+    special_gaussian_system,
+    special_univariate_system,
+    homogeneous_system,
+    system_from_terms,
+)

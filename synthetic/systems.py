@@ -1,0 +1,278 @@
+"""Seeded generators for sparse polynomial systems and evaluation points.
+
+Recipe (SURVEY.md §8(d) "Synthetic inputs", readings C7 and C11 in DESIGN.md):
+
+* ``rng = numpy.random.Generator(numpy.random.PCG64(seed))``.
+* For each polynomial i = 0..n-1 and term t = 0..m-1 (independent supports per
+  polynomial, reading C7): ``vars = sorted(rng.choice(n, k, replace=False))``,
+  ``exps = rng.integers(1, D+1, k)``, ``theta_c = rng.uniform(0, 2*pi)``.
+* Then point angles ``rng.uniform(0, 2*pi, size=(P, n))``.
+* Each real cos/sin of an angle (the double theta, taken exactly) is evaluated
+  in mpmath at 64*L+64 bits and split greedily into L round-to-nearest doubles,
+  giving normalised DD (L=2) or QD (L=4) limbs.
+
+Array layout is the one ``include/phc.h`` declares: ``coeff`` and points are
+``[..][2][L]`` float64 with the real limbs first, then the imaginary limbs.
+
+This module holds none of the evaluation method's arithmetic; the limb split
+below is input preparation (round a high-precision real to a limb vector).
+"""
+from __future__ import annotations
+
+import math
+import os
+from dataclasses import dataclass
+from multiprocessing import get_context
+
+import numpy as np
+from mpmath.libmp import from_float, from_int, from_rational, mpf_cos_sin, mpf_sub, round_nearest, to_float
+
+# BASELINE.json configs[0..4] (n, m, k, D, limbs, points)
+CONFIGS = {
+    "tiny": dict(n=8, m=8, k=4, D=3, limbs=2, points=1),
+    "c2": dict(n=20, m=20, k=10, D=4, limbs=2, points=1),
+    "c3": dict(n=40, m=40, k=20, D=5, limbs=4, points=1),
+    "batch": dict(n=32, m=32, k=16, D=4, limbs=2, points=65536),
+    "large": dict(n=256, m=256, k=32, D=8, limbs=4, points=1),
+    "large_batch": dict(n=256, m=256, k=32, D=8, limbs=4, points=4096),
+}
+
+
+@dataclass
+class SystemArrays:
+    """A sparse polynomial system in the C-ABI's CSR layout (include/phc.h)."""
+
+    n_eq: int
+    n_var: int
+    limbs: int
+    poly_ptr: np.ndarray  # int64 [n_eq+1]
+    term_ptr: np.ndarray  # int64 [n_terms+1]
+    var_idx: np.ndarray  # int32 [n_factors], 0-based, strictly increasing per term
+    exponent: np.ndarray  # int32 [n_factors], >= 1
+    coeff: np.ndarray  # float64 [n_terms][2][limbs]
+
+    @property
+    def n_terms(self) -> int:
+        return int(self.term_ptr.shape[0] - 1)
+
+    def terms(self, i):
+        """Yield (t, [(var, exp), ...]) for the terms of polynomial i (host helper)."""
+        for t in range(int(self.poly_ptr[i]), int(self.poly_ptr[i + 1])):
+            a, b = int(self.term_ptr[t]), int(self.term_ptr[t + 1])
+            yield t, list(zip(self.var_idx[a:b].tolist(), self.exponent[a:b].tolist()))
+
+
+def split_limbs(v, limbs: int, prec: int) -> list[float]:
+    """Greedy round-to-nearest split of an mpmath mpf tuple into ``limbs`` doubles."""
+    out = []
+    r = v
+    for _ in range(limbs):
+        h = to_float(r, False, round_nearest)  # round to nearest (mpmath's default truncates)
+        out.append(h)
+        r = mpf_sub(r, from_float(h), prec)
+    return out
+
+
+def _cos_sin_limbs(args):
+    thetas, limbs = args
+    prec = 64 * limbs + 64
+    out = np.empty((len(thetas), 2, limbs), dtype=np.float64)
+    for j, th in enumerate(thetas):
+        c, s = mpf_cos_sin(from_float(float(th)), prec)
+        out[j, 0, :] = split_limbs(c, limbs, prec)
+        out[j, 1, :] = split_limbs(s, limbs, prec)
+    return out
+
+
+def _procs() -> int:
+    try:
+        return max(1, len(os.sched_getaffinity(0)))
+    except AttributeError:  # pragma: no cover
+        return os.cpu_count() or 1
+
+
+def unit_circle_limbs(thetas: np.ndarray, limbs: int, workers: int | None = None) -> np.ndarray:
+    """e^{i theta} for every double theta, as [..., 2, limbs] float64 limbs."""
+    flat = np.ascontiguousarray(thetas, dtype=np.float64).reshape(-1)
+    if flat.size == 0:
+        return np.empty(thetas.shape + (2, limbs))
+    workers = workers or _procs()
+    if flat.size < 4096 or workers == 1:
+        res = _cos_sin_limbs((flat, limbs))
+    else:
+        chunks = np.array_split(flat, workers * 4)
+        with get_context("fork").Pool(workers) as pool:
+            res = np.concatenate(pool.map(_cos_sin_limbs, [(c, limbs) for c in chunks]))
+    return res.reshape(thetas.shape + (2, limbs))
+
+
+def system_from_terms(n_eq, n_var, limbs, polys, coeff_limbs) -> SystemArrays:
+    """Build CSR arrays from ``polys[i] = [[(var, exp), ...] per term]`` and coefficient limbs [T][2][L]."""
+    poly_ptr = [0]
+    term_ptr = [0]
+    vi, ex = [], []
+    for terms in polys:
+        for term in terms:
+            for v, a in term:
+                vi.append(v)
+                ex.append(a)
+            term_ptr.append(len(vi))
+        poly_ptr.append(len(term_ptr) - 1)
+    coeff = np.asarray(coeff_limbs, dtype=np.float64).reshape(len(term_ptr) - 1, 2, limbs)
+    return SystemArrays(
+        n_eq=n_eq,
+        n_var=n_var,
+        limbs=limbs,
+        poly_ptr=np.asarray(poly_ptr, dtype=np.int64),
+        term_ptr=np.asarray(term_ptr, dtype=np.int64),
+        var_idx=np.asarray(vi, dtype=np.int32),
+        exponent=np.asarray(ex, dtype=np.int32),
+        coeff=np.ascontiguousarray(coeff),
+    )
+
+
+def random_system(n, m, k, D, limbs, seed, points=1, workers=None):
+    """The BASELINE.json system family: n polynomials, m terms each, k distinct variables
+    per term, exponents iid uniform in 1..D, unit-circle coefficients and points.
+
+    Returns (SystemArrays, X) with X float64 [points][n][2][limbs].
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    polys = []
+    thetas_c = np.empty(n * m)
+    for i in range(n):
+        terms = []
+        for t in range(m):
+            vars_ = sorted(rng.choice(n, k, replace=False).tolist())
+            exps = rng.integers(1, D + 1, k).tolist()
+            thetas_c[i * m + t] = rng.uniform(0.0, 2.0 * math.pi)
+            terms.append(list(zip(vars_, exps)))
+        polys.append(terms)
+    thetas_x = rng.uniform(0.0, 2.0 * math.pi, size=(points, n))
+    coeff = unit_circle_limbs(thetas_c, limbs, workers)
+    X = unit_circle_limbs(thetas_x, limbs, workers)
+    return system_from_terms(n, n, limbs, polys, coeff), X
+
+
+def config_system(name: str, seed: int = 1, points: int | None = None, workers=None):
+    """System + points for a BASELINE.json config name (see CONFIGS)."""
+    c = CONFIGS[name]
+    P = c["points"] if points is None else points
+    return random_system(c["n"], c["m"], c["k"], c["D"], c["limbs"], seed, P, workers)
+
+
+def limbs_from_values(values, limbs: int) -> np.ndarray:
+    """Exact small complex values (Python complex / int / Fraction pairs) → [..][2][limbs] limbs.
+
+    Each real part is split greedily; for values that are doubles the tail limbs are 0.
+    """
+    arr = []
+    prec = 64 * limbs + 64
+    for z in values:
+        if isinstance(z, tuple):
+            re, im = z
+        else:
+            re, im = complex(z).real, complex(z).imag
+        row = []
+        for part in (re, im):
+            if hasattr(part, "numerator") and not isinstance(part, (int, float)):
+                mp = from_rational(part.numerator, part.denominator, prec)
+            elif isinstance(part, int):
+                mp = from_int(part)
+            else:
+                mp = from_float(float(part))
+            row.append(split_limbs(mp, limbs, prec))
+        arr.append(row)
+    return np.asarray(arr, dtype=np.float64).reshape(len(values), 2, limbs)
+
+
+# ---------------------------------------------------------------------------
+# Special systems whose results are known without the oracle
+# ---------------------------------------------------------------------------
+
+def special_linear_system(n, limbs, seed):
+    """k = 1, a = 1, each (i, v) once: F = C x and J = C exactly (P4).
+
+    Coefficients are small Gaussian integers, points small Gaussian integers, so
+    every intermediate result is an exact double.  Returns (system, X, C) with C
+    an int64 [n][n][2] array of Gaussian-integer coefficients.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    C = rng.integers(-9, 10, size=(n, n, 2))
+    polys = [[[(v, 1)] for v in range(n)] for _ in range(n)]
+    coeff = np.zeros((n * n, 2, limbs))
+    coeff[:, 0, 0] = C[:, :, 0].reshape(-1)
+    coeff[:, 1, 0] = C[:, :, 1].reshape(-1)
+    x = rng.integers(-9, 10, size=(n, 2))
+    X = np.zeros((1, n, 2, limbs))
+    X[0, :, 0, 0] = x[:, 0]
+    X[0, :, 1, 0] = x[:, 1]
+    return system_from_terms(n, n, limbs, polys, coeff), X, C, x
+
+
+def special_gaussian_system(n, m, k, D, limbs, seed):
+    """Random sparse system with coefficients in Z[i] (|re|,|im| <= 3) and a point in {±1, ±i}^n.
+
+    Every monomial value is a unit in Z[i] and every partial is a small Gaussian
+    integer, so all intermediates are exact doubles (P5): the GPU output must
+    equal the exact result bitwise.
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    polys = []
+    cl = []
+    for i in range(n):
+        terms = []
+        for t in range(m):
+            kk = min(k, n)
+            vars_ = sorted(rng.choice(n, kk, replace=False).tolist())
+            exps = rng.integers(1, D + 1, kk).tolist()
+            terms.append(list(zip(vars_, exps)))
+            cl.append(rng.integers(-3, 4, size=2))
+        polys.append(terms)
+    coeff = np.zeros((len(cl), 2, limbs))
+    coeff[:, :, 0] = np.asarray(cl)
+    units = np.array([[1, 0], [-1, 0], [0, 1], [0, -1]])
+    X = np.zeros((1, n, 2, limbs))
+    X[0, :, :, 0] = units[rng.integers(0, 4, size=n)]
+    return system_from_terms(n, n, limbs, polys, coeff), X
+
+
+def special_univariate_system(degree, limbs, seed):
+    """n = 1, f(x) = sum_{d=0}^{degree} c_d x^d (P4: reduces to Horner / mpmath.polyval).
+
+    The constant term c_0 is a k = 0 term.  Returns (system, X, thetas_c, theta_x).
+    """
+    rng = np.random.Generator(np.random.PCG64(seed))
+    polys = [[[]] + [[(0, d)] for d in range(1, degree + 1)]]
+    thetas_c = rng.uniform(0.0, 2.0 * math.pi, size=degree + 1)
+    theta_x = rng.uniform(0.0, 2.0 * math.pi, size=(1, 1))
+    coeff = unit_circle_limbs(thetas_c, limbs, 1)
+    X = unit_circle_limbs(theta_x, limbs, 1)
+    return system_from_terms(1, 1, limbs, polys, coeff), X
+
+
+def homogeneous_system(n, m, k, d, limbs, seed, points=1):
+    """Every term of f_i has total degree d_i = d + (i % 3) (P8 Euler identity:
+    sum_v x_v J_{i,v} = d_i f_i).  Exponent vectors are compositions of d_i into k
+    positive parts.  Returns (system, X, degrees)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    polys = []
+    degs = []
+    thetas_c = np.empty(n * m)
+    for i in range(n):
+        di = d + (i % 3)
+        degs.append(di)
+        kk = min(k, n, di)
+        terms = []
+        for t in range(m):
+            vars_ = sorted(rng.choice(n, kk, replace=False).tolist())
+            cuts = sorted(rng.choice(np.arange(1, di), kk - 1, replace=False).tolist()) if kk > 1 else []
+            bounds = [0] + cuts + [di]
+            exps = [bounds[j + 1] - bounds[j] for j in range(kk)]
+            thetas_c[i * m + t] = rng.uniform(0.0, 2.0 * math.pi)
+            terms.append(list(zip(vars_, exps)))
+        polys.append(terms)
+    thetas_x = rng.uniform(0.0, 2.0 * math.pi, size=(points, n))
+    coeff = unit_circle_limbs(thetas_c, limbs, 1)
+    X = unit_circle_limbs(thetas_x, limbs, 1)
+    return system_from_terms(n, n, limbs, polys, coeff), X, degs
