@@ -1,0 +1,124 @@
+/* phc.h — C ABI of the B200 evaluator of a sparse polynomial system and its Jacobian
+ * in complex double-double (DD) or quad-double (QD) arithmetic.
+ *
+ * What is computed (PAPER.md = Verschelde & Yoffe 2011, arXiv 1109.0545):
+ *   Y = "the evaluated polynomials ... along with all partial derivatives as needed
+ *   in the Jacobian matrix" (Alg. 2 discussion), i.e. for a point x in C^n
+ *     F[i]    = f_i(x)        = sum_{t in T_i} c_t prod_j x_{i_{t,j}}^{a_{t,j}}
+ *     J[i][v] = df_i/dx_v(x),
+ *   by the paper's algorithmic-differentiation scheme for normalised monomials
+ *   x_{i_1}^{a_1} ... x_{i_k}^{a_k}, i_1 < ... < i_k, a_j >= 1 (§6):
+ *   Speelpenning prefix/suffix products (indices as DESIGN.md reading C1)
+ *   over a shared per-point table of variable powers, then the coefficient product
+ *   and the sums per polynomial / per Jacobian entry (Alg. 2 "Monomial_Evaluation",
+ *   "Coefficient_Product").
+ *
+ * Number layout.  A complex number is 2*L doubles: L real limbs then L imaginary
+ * limbs, limbs non-overlapping and decreasing in magnitude (L = 2: DD, L = 4: QD).
+ *   x   : [n_var][2][L]
+ *   F   : [n_eq][2][L]
+ *   J   : [n_eq][n_var][2][L], row-major, J[i][v] = df_i/dx_v; structural zeros are exact 0.
+ *   Batched arrays have a leading [n_points] dimension.
+ * Device pointers must be 32-byte aligned (256-bit vector accesses).
+ *
+ * Errors.  Every int-returning function returns PHC_OK (0) or a negative code and
+ * sets a thread-local message readable with phc_last_error().  Non-finite inputs x
+ * are not checked on the hot path: NaN/Inf propagate into F and J.
+ *
+ * Ordering.  Device-pointer calls are asynchronous on the caller's stream
+ * (cudaStream_t passed as void*; NULL = legacy default stream): they return once
+ * the work is enqueued.  Kernel faults surface at the caller's next synchronisation.
+ * A handle owns per-stream-agnostic scratch: do not run two eval calls of the same
+ * handle concurrently on different streams (calls on one stream are fine).
+ *
+ * Determinism.  For a given system and point the results are bitwise reproducible:
+ * every sum is taken in a fixed order, independent of the launch configuration,
+ * of n_points and of the device list of a batch call.
+ */
+#ifndef PHC_H
+#define PHC_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  PHC_OK = 0,
+  PHC_EINVAL = -1,       /* invalid argument or malformed system */
+  PHC_ENOMEM = -2,       /* device or host allocation failed */
+  PHC_ECUDA = -3,        /* a CUDA runtime call or kernel launch failed */
+  PHC_EUNSUPPORTED = -4  /* valid but beyond the compiled limits (see below) */
+};
+
+/* Compiled limits: limbs in {2, 4}; factors per term k <= PHC_MAX_K; exponents <= PHC_MAX_EXP;
+ * n_var <= PHC_MAX_VARS. */
+#define PHC_MAX_K 64
+#define PHC_MAX_EXP 255
+#define PHC_MAX_VARS 65534
+
+typedef struct phc_system phc_system; /* opaque; owned by the library */
+
+/* Create a system handle on CUDA device `device` (the "home" device).
+ *   n_eq, n_var >= 1;  limbs = 2 (complex DD) or 4 (complex QD).
+ *   poly_ptr [n_eq+1]     CSR over terms: polynomial i owns terms poly_ptr[i] .. poly_ptr[i+1]-1;
+ *                         poly_ptr[0] = 0, non-decreasing, poly_ptr[n_eq] = n_terms.
+ *   term_ptr [n_terms+1]  CSR over factors: term t owns factors term_ptr[t] .. term_ptr[t+1]-1;
+ *                         term_ptr[0] = 0, non-decreasing. k = 0 is a constant term.
+ *   var_idx  [n_factors]  0-based variable of each factor, strictly increasing within a term
+ *                         (normalised monomial).
+ *   exponent [n_factors]  a_j >= 1.
+ *   coeff    [n_terms][2][limbs]  c_t, finite limbs.
+ * All array pointers are HOST pointers; they are deep-copied (the caller keeps ownership).
+ * Duplicate terms within a polynomial are allowed and summed.
+ * Returns PHC_EINVAL on malformed input, PHC_EUNSUPPORTED beyond the compiled limits. */
+int phc_system_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_terms,
+                      const int64_t* poly_ptr, const int64_t* term_ptr, const int32_t* var_idx,
+                      const int32_t* exponent, const double* coeff, int32_t device);
+
+/* Release the handle and every device buffer it owns (all devices). NULL is a no-op. */
+void phc_system_destroy(phc_system* s);
+
+/* One point on the home device.  x, f, jac: device pointers on the home device
+ * (layouts above); f and jac are written in full and must not alias x. */
+int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* jac, void* stream);
+
+/* n_points points.  x [n_points][n_var][2][L], f [n_points][n_eq][2][L],
+ * jac [n_points][n_eq][n_var][2][L]: device pointers on the home device.
+ * devices[0..n_devices-1]: CUDA devices to shard the points over (contiguous, equal
+ * ranges; repeats allowed, e.g. {0,0,0,0}, for testing the shard bookkeeping on one GPU);
+ * devices = NULL or n_devices = 0 means {home}.  Inputs are scattered and outputs
+ * gathered over NVLink peer copies; every device's work is ordered after the work
+ * already enqueued on `stream`, and `stream` waits for the gather.  Results are
+ * bitwise identical for every device list. */
+int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double* x, double* f, double* jac,
+                            const int32_t* devices, int32_t n_devices, void* stream);
+
+/* End-to-end convenience: x, f, jac are HOST pointers (pinned or pageable); copies in,
+ * evaluates n_points points on the home device (or sharded as above) and copies out.
+ * Synchronous: returns after f and jac are written. */
+int phc_eval_jacobian_batch_host(const phc_system* s, int64_t n_points, const double* x_host, double* f_host,
+                                 double* jac_host, const int32_t* devices, int32_t n_devices);
+
+/* Static facts about the system, as built: counts used by the benchmark's model.
+ * out[0] = n_terms, out[1] = n_factors, out[2] = max k, out[3] = max exponent D,
+ * out[4] = nnz(J) (structurally nonzero entries), out[5] = complex multiplies per point
+ * performed by the kernels, out[6] = complex additions per point performed by the kernels,
+ * out[7] = kernel launches per eval call (single point). */
+int phc_system_stats(const phc_system* s, int64_t out[8]);
+
+/* FP64 pipe peak of `device` in TFLOP/s (2 flops per DFMA), measured with independent
+ * DFMA chains over `ms_target` milliseconds; the SURVEY.md §8(d) denominator. */
+int phc_fp64_peak(int32_t device, double ms_target, double* tflops);
+
+/* Thread-local message describing the last failure in this thread ("" if none). */
+const char* phc_last_error(void);
+
+/* Library version string. */
+const char* phc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PHC_H */

@@ -1,0 +1,23 @@
+"""phc-b200: evaluate a sparse polynomial system and its Jacobian on a B200 in complex
+double-double / quad-double arithmetic (Verschelde & Yoffe 2011, arXiv 1109.0545, §6).
+
+The C ABI (include/phc.h) is the boundary; this package only marshals arguments.
+"""
+from ._lib import (  # noqa: F401
+    PHC_EINVAL,
+    PHC_ECUDA,
+    PHC_ENOMEM,
+    PHC_EUNSUPPORTED,
+    PHC_OK,
+    PhcError,
+    phc_eval_jacobian,
+    phc_eval_jacobian_batch,
+    phc_eval_jacobian_batch_host,
+    phc_fp64_peak,
+    phc_last_error,
+    phc_system_create,
+    phc_system_destroy,
+    phc_system_stats,
+    phc_version,
+)
+from .system import System  # noqa: F401

@@ -1,0 +1,122 @@
+"""ctypes binding of the C ABI declared in include/phc.h (argument marshalling only).
+
+Every function here has the C name; every step of the evaluation runs in the CUDA
+kernels of libphc.so.  There is no fallback: if the shared library is missing the
+import fails loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libphc.so")
+
+PHC_OK = 0
+PHC_EINVAL = -1
+PHC_ENOMEM = -2
+PHC_ECUDA = -3
+PHC_EUNSUPPORTED = -4
+PHC_MAX_K = 64
+PHC_MAX_EXP = 255
+
+EXPORTED = (
+    "phc_system_create",
+    "phc_system_destroy",
+    "phc_eval_jacobian",
+    "phc_eval_jacobian_batch",
+    "phc_eval_jacobian_batch_host",
+    "phc_system_stats",
+    "phc_fp64_peak",
+    "phc_last_error",
+    "phc_version",
+)
+
+
+class PhcError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"phc error {code}: {msg}")
+        self.code = code
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} not found: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(the CUDA extension is required; there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    P = ctypes.c_void_p
+    i32, i64 = ctypes.c_int32, ctypes.c_int64
+    lib.phc_system_create.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, P, i32]
+    lib.phc_system_create.restype = ctypes.c_int
+    lib.phc_system_destroy.argtypes = [P]
+    lib.phc_system_destroy.restype = None
+    lib.phc_eval_jacobian.argtypes = [P, P, P, P, P]
+    lib.phc_eval_jacobian.restype = ctypes.c_int
+    lib.phc_eval_jacobian_batch.argtypes = [P, i64, P, P, P, P, i32, P]
+    lib.phc_eval_jacobian_batch.restype = ctypes.c_int
+    lib.phc_eval_jacobian_batch_host.argtypes = [P, i64, P, P, P, P, i32]
+    lib.phc_eval_jacobian_batch_host.restype = ctypes.c_int
+    lib.phc_system_stats.argtypes = [P, P]
+    lib.phc_system_stats.restype = ctypes.c_int
+    lib.phc_fp64_peak.argtypes = [i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
+    lib.phc_fp64_peak.restype = ctypes.c_int
+    lib.phc_last_error.argtypes = []
+    lib.phc_last_error.restype = ctypes.c_char_p
+    lib.phc_version.argtypes = []
+    lib.phc_version.restype = ctypes.c_char_p
+    return lib
+
+
+lib = _load()
+
+
+def check(rc):
+    if rc != PHC_OK:
+        raise PhcError(rc, lib.phc_last_error().decode())
+    return rc
+
+
+# --- thin same-name wrappers (raw pointers / ints) -------------------------------------------
+
+def phc_system_create(n_eq, n_var, limbs, n_terms, poly_ptr, term_ptr, var_idx, exponent, coeff, device):
+    h = ctypes.c_void_p()
+    check(lib.phc_system_create(ctypes.byref(h), n_eq, n_var, limbs, n_terms, poly_ptr, term_ptr, var_idx,
+                                exponent, coeff, device))
+    return h
+
+
+def phc_system_destroy(h):
+    lib.phc_system_destroy(h)
+
+
+def phc_eval_jacobian(h, x, f, jac, stream):
+    return check(lib.phc_eval_jacobian(h, x, f, jac, stream))
+
+
+def phc_eval_jacobian_batch(h, n_points, x, f, jac, devices, n_devices, stream):
+    return check(lib.phc_eval_jacobian_batch(h, n_points, x, f, jac, devices, n_devices, stream))
+
+
+def phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices):
+    return check(lib.phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices))
+
+
+def phc_system_stats(h):
+    out = (ctypes.c_int64 * 8)()
+    check(lib.phc_system_stats(h, out))
+    return list(out)
+
+
+def phc_fp64_peak(device=0, ms_target=200.0):
+    v = ctypes.c_double()
+    check(lib.phc_fp64_peak(device, ms_target, ctypes.byref(v)))
+    return v.value
+
+
+def phc_last_error():
+    return lib.phc_last_error().decode()
+
+
+def phc_version():
+    return lib.phc_version().decode()

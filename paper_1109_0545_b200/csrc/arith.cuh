@@ -1,0 +1,288 @@
+// Device double-double (DD) and quad-double (QD) complex arithmetic core.
+//
+// The paper computes in complex double-double and complex quad-double arithmetic
+// from QD-2.3.9 ("complex quad double"
+// P:606).  This file restates the published error-free-transformation
+// algorithms (Dekker / Knuth two_sum, FMA two_prod; the Hida-Li-Bailey DD and QD
+// algorithms) for sm_100a.  Every floating-point step uses the __dadd_rn /
+// __dmul_rn / __fma_rn intrinsics so that nvcc can neither contract nor reassociate
+// an error-free transformation.
+//
+// Variants (reading C8): additions are the "sloppy" (normwise-accurate)
+// forms, multiplications the standard FMA forms; the complex DD product is fused
+// (one renormalisation per real part).  All are branch-free, so negation commutes
+// with every operation (conjugation metamorphic test, P9) and warps never diverge.
+#pragma once
+#include <cstdint>
+
+namespace phc {
+
+#define PHC_DEV __device__ __forceinline__
+
+PHC_DEV double add_(double a, double b) { return __dadd_rn(a, b); }
+PHC_DEV double sub_(double a, double b) { return __dadd_rn(a, -b); }
+PHC_DEV double mul_(double a, double b) { return __dmul_rn(a, b); }
+PHC_DEV double fma_(double a, double b, double c) { return __fma_rn(a, b, c); }
+
+// s + e == a + b exactly (6 DADD).
+PHC_DEV void two_sum(double a, double b, double& s, double& e) {
+  s = add_(a, b);
+  double bb = sub_(s, a);
+  e = add_(sub_(a, sub_(s, bb)), sub_(b, bb));
+}
+// s + e == a + b exactly when |a| >= |b| (3 DADD).
+PHC_DEV void quick_two_sum(double a, double b, double& s, double& e) {
+  s = add_(a, b);
+  e = sub_(b, sub_(s, a));
+}
+// p + e == a * b exactly (DMUL + DFMA).
+PHC_DEV void two_prod(double a, double b, double& p, double& e) {
+  p = mul_(a, b);
+  e = fma_(a, b, -p);
+}
+
+// ---------------------------------------------------------------------------
+// double-double
+// ---------------------------------------------------------------------------
+struct dd {
+  double x[2];
+};
+
+PHC_DEV dd dd_make(double h, double l) { dd r; r.x[0] = h; r.x[1] = l; return r; }
+PHC_DEV dd dd_neg(const dd& a) { return dd_make(-a.x[0], -a.x[1]); }
+
+// sloppy add: error <= ~2u^2 (|a| + |b|)  (normwise accurate)
+PHC_DEV dd dd_add(const dd& a, const dd& b) {
+  double s, e;
+  two_sum(a.x[0], b.x[0], s, e);
+  e = add_(e, add_(a.x[1], b.x[1]));
+  dd r;
+  quick_two_sum(s, e, r.x[0], r.x[1]);
+  return r;
+}
+PHC_DEV dd dd_mul(const dd& a, const dd& b) {
+  double p, e;
+  two_prod(a.x[0], b.x[0], p, e);
+  e = fma_(a.x[0], b.x[1], e);
+  e = fma_(a.x[1], b.x[0], e);
+  dd r;
+  quick_two_sum(p, e, r.x[0], r.x[1]);
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// quad-double (Hida, Li, Bailey: sloppy add, sloppy mul, branch-free renormalisation)
+// ---------------------------------------------------------------------------
+struct qd {
+  double x[4];
+};
+
+PHC_DEV qd qd_neg(const qd& a) { qd r; for (int i = 0; i < 4; ++i) r.x[i] = -a.x[i]; return r; }
+
+// (a, b, c) <- three_sum(a, b, c): a + b + c exactly, a the leading term
+PHC_DEV void three_sum(double& a, double& b, double& c) {
+  double t1, t2, t3;
+  two_sum(a, b, t1, t2);
+  two_sum(c, t1, a, t3);
+  two_sum(t2, t3, b, c);
+}
+// (a, b) <- leading two of a + b + c
+PHC_DEV void three_sum2(double& a, double& b, double c) {
+  double t1, t2, t3;
+  two_sum(a, b, t1, t2);
+  two_sum(c, t1, a, t3);
+  b = add_(t2, t3);
+}
+// branch-free renormalisation of a 5-term expansion into 4 limbs
+PHC_DEV qd renorm5(double c0, double c1, double c2, double c3, double c4) {
+  double s, t0, t1, t2, t3;
+  quick_two_sum(c3, c4, s, t3);
+  quick_two_sum(c2, s, s, t2);
+  quick_two_sum(c1, s, s, t1);
+  qd r;
+  quick_two_sum(c0, s, r.x[0], t0);
+  quick_two_sum(t2, t3, s, t2);
+  quick_two_sum(t1, s, s, t1);
+  quick_two_sum(t0, s, r.x[1], t0);
+  quick_two_sum(t1, t2, s, t1);
+  quick_two_sum(t0, s, r.x[2], t0);
+  r.x[3] = add_(t0, t1);
+  return r;
+}
+
+PHC_DEV qd qd_add(const qd& a, const qd& b) {
+  double s0, s1, s2, s3, t0, t1, t2, t3;
+  two_sum(a.x[0], b.x[0], s0, t0);
+  two_sum(a.x[1], b.x[1], s1, t1);
+  two_sum(a.x[2], b.x[2], s2, t2);
+  two_sum(a.x[3], b.x[3], s3, t3);
+  two_sum(s1, t0, s1, t0);
+  three_sum(s2, t0, t1);
+  three_sum2(s3, t0, t2);
+  t0 = add_(add_(t0, t1), t3);
+  return renorm5(s0, s1, s2, s3, t0);
+}
+
+PHC_DEV qd qd_mul(const qd& a, const qd& b) {
+  double p0, p1, p2, p3, p4, p5, q0, q1, q2, q3, q4, q5;
+  two_prod(a.x[0], b.x[0], p0, q0);
+  two_prod(a.x[0], b.x[1], p1, q1);
+  two_prod(a.x[1], b.x[0], p2, q2);
+  two_prod(a.x[0], b.x[2], p3, q3);
+  two_prod(a.x[1], b.x[1], p4, q4);
+  two_prod(a.x[2], b.x[0], p5, q5);
+  // O(eps) terms
+  three_sum(p1, p2, q0);
+  // O(eps^2) terms: (p2, q1, q2) + (p3, p4, p5)
+  three_sum(p2, q1, q2);
+  three_sum(p3, p4, p5);
+  double s0, s1, s2, t0, t1;
+  two_sum(p2, p3, s0, t0);
+  two_sum(q1, p4, s1, t1);
+  s2 = add_(q2, p5);
+  two_sum(s1, t0, s1, t0);
+  s2 = add_(s2, add_(t0, t1));
+  // O(eps^3) terms
+  double o3 = mul_(a.x[0], b.x[3]);
+  o3 = fma_(a.x[1], b.x[2], o3);
+  o3 = fma_(a.x[2], b.x[1], o3);
+  o3 = fma_(a.x[3], b.x[0], o3);
+  o3 = add_(o3, add_(add_(q0, q3), add_(q4, q5)));
+  s1 = add_(s1, o3);
+  return renorm5(p0, p1, s0, s1, s2);
+}
+
+// ---------------------------------------------------------------------------
+// complex values, templated on the real type; Prec<L> traits below
+// ---------------------------------------------------------------------------
+template <class R>
+struct cplx {
+  R re, im;
+};
+
+using cdd = cplx<dd>;
+using cqd = cplx<qd>;
+
+template <int L> struct Prec;
+
+template <> struct Prec<2> {
+  using real = dd;
+  using C = cdd;
+  static constexpr int L = 2;
+  PHC_DEV static C zero() { C z; z.re = dd_make(0, 0); z.im = dd_make(0, 0); return z; }
+  PHC_DEV static C one() { C z; z.re = dd_make(1, 0); z.im = dd_make(0, 0); return z; }
+  PHC_DEV static C add(const C& a, const C& b) { C r; r.re = dd_add(a.re, b.re); r.im = dd_add(a.im, b.im); return r; }
+  // fused complex DD product: each real part is a 2-term dot product accumulated
+  // in one error term, with one renormalisation (normwise error ~ u^2 |a||b|).
+  PHC_DEV static C mul(const C& a, const C& b) {
+    C r;
+    {
+      double p1, e1, p2, e2, s, t;
+      two_prod(a.re.x[0], b.re.x[0], p1, e1);
+      two_prod(a.im.x[0], b.im.x[0], p2, e2);
+      two_sum(p1, -p2, s, t);
+      t = add_(t, sub_(e1, e2));
+      t = fma_(a.re.x[0], b.re.x[1], t);
+      t = fma_(a.re.x[1], b.re.x[0], t);
+      t = fma_(-a.im.x[0], b.im.x[1], t);
+      t = fma_(-a.im.x[1], b.im.x[0], t);
+      quick_two_sum(s, t, r.re.x[0], r.re.x[1]);
+    }
+    {
+      double p1, e1, p2, e2, s, t;
+      two_prod(a.re.x[0], b.im.x[0], p1, e1);
+      two_prod(a.im.x[0], b.re.x[0], p2, e2);
+      two_sum(p1, p2, s, t);
+      t = add_(t, add_(e1, e2));
+      t = fma_(a.re.x[0], b.im.x[1], t);
+      t = fma_(a.re.x[1], b.im.x[0], t);
+      t = fma_(a.im.x[0], b.re.x[1], t);
+      t = fma_(a.im.x[1], b.re.x[0], t);
+      quick_two_sum(s, t, r.im.x[0], r.im.x[1]);
+    }
+    return r;
+  }
+  // multiply by a small positive integer s (exact in binary64): product exact via two_prod
+  PHC_DEV static real mul_int_real(const real& a, double s) {
+    double p, e;
+    two_prod(a.x[0], s, p, e);
+    e = fma_(a.x[1], s, e);
+    real r;
+    quick_two_sum(p, e, r.x[0], r.x[1]);
+    return r;
+  }
+  PHC_DEV static C mul_int(const C& a, double s) { C r; r.re = mul_int_real(a.re, s); r.im = mul_int_real(a.im, s); return r; }
+};
+
+template <> struct Prec<4> {
+  using real = qd;
+  using C = cqd;
+  static constexpr int L = 4;
+  PHC_DEV static C zero() { C z; for (int i = 0; i < 4; ++i) { z.re.x[i] = 0; z.im.x[i] = 0; } return z; }
+  PHC_DEV static C one() { C z = zero(); z.re.x[0] = 1; return z; }
+  PHC_DEV static C add(const C& a, const C& b) { C r; r.re = qd_add(a.re, b.re); r.im = qd_add(a.im, b.im); return r; }
+  PHC_DEV static C mul(const C& a, const C& b) {
+    C r;
+    r.re = qd_add(qd_mul(a.re, b.re), qd_neg(qd_mul(a.im, b.im)));
+    r.im = qd_add(qd_mul(a.re, b.im), qd_mul(a.im, b.re));
+    return r;
+  }
+  PHC_DEV static real mul_int_real(const real& a, double s) {
+    // a_j * s = p_j + e_j exactly; collect by order of magnitude
+    double p0, p1, p2, p3, e0, e1, e2;
+    two_prod(a.x[0], s, p0, e0);
+    two_prod(a.x[1], s, p1, e1);
+    two_prod(a.x[2], s, p2, e2);
+    p3 = mul_(a.x[3], s);
+    double s1, t1;
+    two_sum(p1, e0, s1, t1);      // O(eps)
+    three_sum(p2, e1, t1);        // O(eps^2) -> p2, (e1, t1) O(eps^3)
+    double s3 = add_(add_(p3, e2), add_(e1, t1));
+    return renorm5(p0, s1, p2, s3, 0.0);
+  }
+  PHC_DEV static C mul_int(const C& a, double s) { C r; r.re = mul_int_real(a.re, s); r.im = mul_int_real(a.im, s); return r; }
+};
+
+// ---------------------------------------------------------------------------
+// global-memory complex load/store in the [2][L] f64 layout (re limbs, im limbs).
+// 256-bit vector accesses (LDG.E.ENL2.256 / STG.E.ENL2.256 on sm_100a).
+// ---------------------------------------------------------------------------
+PHC_DEV void ld4(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.nc.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+PHC_DEV void ld4_rw(const double* p, double& a, double& b, double& c, double& d) {
+  asm volatile("ld.global.v4.f64 {%0, %1, %2, %3}, [%4];" : "=d"(a), "=d"(b), "=d"(c), "=d"(d) : "l"(p));
+}
+PHC_DEV void st4(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c), "d"(d) : "memory");
+}
+
+template <int L> PHC_DEV typename Prec<L>::C cload(const double* p);
+template <int L> PHC_DEV void cstore(double* p, const typename Prec<L>::C& v);
+template <int L> PHC_DEV typename Prec<L>::C cload_rw(const double* p);
+
+template <> PHC_DEV cdd cload<2>(const double* p) {
+  cdd v; ld4(p, v.re.x[0], v.re.x[1], v.im.x[0], v.im.x[1]); return v;
+}
+template <> PHC_DEV cdd cload_rw<2>(const double* p) {
+  cdd v; ld4_rw(p, v.re.x[0], v.re.x[1], v.im.x[0], v.im.x[1]); return v;
+}
+template <> PHC_DEV void cstore<2>(double* p, const cdd& v) { st4(p, v.re.x[0], v.re.x[1], v.im.x[0], v.im.x[1]); }
+template <> PHC_DEV cqd cload<4>(const double* p) {
+  cqd v;
+  ld4(p, v.re.x[0], v.re.x[1], v.re.x[2], v.re.x[3]);
+  ld4(p + 4, v.im.x[0], v.im.x[1], v.im.x[2], v.im.x[3]);
+  return v;
+}
+template <> PHC_DEV cqd cload_rw<4>(const double* p) {
+  cqd v;
+  ld4_rw(p, v.re.x[0], v.re.x[1], v.re.x[2], v.re.x[3]);
+  ld4_rw(p + 4, v.im.x[0], v.im.x[1], v.im.x[2], v.im.x[3]);
+  return v;
+}
+template <> PHC_DEV void cstore<4>(double* p, const cqd& v) {
+  st4(p, v.re.x[0], v.re.x[1], v.re.x[2], v.re.x[3]);
+  st4(p + 4, v.im.x[0], v.im.x[1], v.im.x[2], v.im.x[3]);
+}
+
+}  // namespace phc

@@ -1,0 +1,551 @@
+// Host runtime and C ABI (include/phc.h): validate and pack the system, own the
+// per-device table replicas and scratch, select and launch the kernels, shard
+// batches over devices and gather the results.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/phc.h"
+#include "kernels_generic.cuh"
+#include "kernels_block.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CUDA_TRY(expr)                                                                         \
+  do {                                                                                         \
+    cudaError_t e_ = (expr);                                                                   \
+    if (e_ != cudaSuccess) return fail(PHC_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+template <class T>
+int dalloc(T** p, size_t n) {
+  if (n == 0) n = 1;
+  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    *p = nullptr;
+    cudaGetLastError();
+    return fail(PHC_ENOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
+  }
+  return PHC_OK;
+}
+
+// Per-device replica of the packed tables plus scratch (tables
+// replicated once per device at first use).
+struct DeviceState {
+  int dev = -1;
+  cudaStream_t stream = nullptr;  // internal stream for non-home shards
+  cudaEvent_t done = nullptr;
+  // generic path tables
+  int64_t* term_ptr = nullptr;
+  uint32_t* fac = nullptr;
+  double* coeff = nullptr;
+  int64_t* poly_ptr = nullptr;
+  int64_t* jptr = nullptr;
+  int64_t* jidx = nullptr;
+  // block path tables
+  phc::BlockTables bt{};
+  bool have_block = false;
+  // scratch
+  double* PT = nullptr;
+  double* Y = nullptr;
+  double* G = nullptr;
+  int64_t chunk_cap = 0;
+  // staging buffers for remote shards
+  double* xs = nullptr;
+  double* fs = nullptr;
+  double* js = nullptr;
+  int64_t stage_cap = 0;
+  ~DeviceState() {
+    DeviceGuard g(dev);
+    for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
+                    (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)bt.fac, (void*)bt.coeff,
+                    (void*)bt.blk})
+      if (p) cudaFree(p);
+    if (stream) cudaStreamDestroy(stream);
+    if (done) cudaEventDestroy(done);
+  }
+};
+
+}  // namespace
+
+struct phc_system {
+  int32_t n_eq = 0, n_var = 0, L = 0, home = 0;
+  int64_t n_terms = 0, n_factors = 0;
+  int kmax = 0, E = 1;
+  int64_t nnz = 0;
+  int64_t cm_per_point = 0, ca_per_point = 0;
+  // host copies
+  std::vector<int64_t> poly_ptr, term_ptr;
+  std::vector<uint32_t> fac;
+  std::vector<double> coeff;
+  std::vector<int64_t> jptr, jidx;
+  phc::HostBlockPlan plan;  // warp-per-block layout (kernels_block.cuh)
+  std::mutex mu;
+  std::map<int, std::unique_ptr<DeviceState>> devs;
+  // host-API staging on the home device
+  double *hx = nullptr, *hf = nullptr, *hj = nullptr;
+  int64_t h_cap = 0;
+  cudaStream_t hstream = nullptr;
+};
+
+namespace {
+
+size_t cbytes(const phc_system* s) { return (size_t)2 * s->L * sizeof(double); }
+
+int upload(void* dst, const void* src, size_t bytes) {
+  if (bytes == 0) return PHC_OK;
+  CUDA_TRY(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice));
+  return PHC_OK;
+}
+
+int get_device_state(phc_system* s, int dev, DeviceState** out) {
+  std::lock_guard<std::mutex> lk(s->mu);
+  auto it = s->devs.find(dev);
+  if (it != s->devs.end()) {
+    *out = it->second.get();
+    return PHC_OK;
+  }
+  DeviceGuard g(dev);
+  std::unique_ptr<DeviceState> d(new DeviceState());
+  d->dev = dev;
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaEventCreateWithFlags(&d->done, cudaEventDisableTiming));
+  int rc;
+  if ((rc = dalloc(&d->term_ptr, s->term_ptr.size()))) return rc;
+  if ((rc = dalloc(&d->fac, s->fac.size()))) return rc;
+  if ((rc = dalloc(&d->coeff, s->coeff.size()))) return rc;
+  if ((rc = dalloc(&d->poly_ptr, s->poly_ptr.size()))) return rc;
+  if ((rc = dalloc(&d->jptr, s->jptr.size()))) return rc;
+  if ((rc = dalloc(&d->jidx, s->jidx.size()))) return rc;
+  if ((rc = upload(d->term_ptr, s->term_ptr.data(), s->term_ptr.size() * 8))) return rc;
+  if ((rc = upload(d->fac, s->fac.data(), s->fac.size() * 4))) return rc;
+  if ((rc = upload(d->coeff, s->coeff.data(), s->coeff.size() * 8))) return rc;
+  if ((rc = upload(d->poly_ptr, s->poly_ptr.data(), s->poly_ptr.size() * 8))) return rc;
+  if ((rc = upload(d->jptr, s->jptr.data(), s->jptr.size() * 8))) return rc;
+  if ((rc = upload(d->jidx, s->jidx.data(), s->jidx.size() * 8))) return rc;
+  if (s->plan.usable) {
+    if ((rc = phc::upload_block_tables(s->plan, &d->bt))) return fail(rc, "block table upload failed");
+    d->have_block = true;
+  }
+  *out = d.get();
+  s->devs[dev] = std::move(d);
+  return PHC_OK;
+}
+
+int ensure_scratch(const phc_system* s, DeviceState* d, int64_t want_points) {
+  const int64_t pt_pp = (int64_t)(s->n_var + 1) * 2 * s->E;  // complex entries per point
+  const int64_t per_point = (pt_pp + s->n_terms + s->n_factors) * (int64_t)cbytes(s);
+  const int64_t budget = (int64_t)1 << 30;  // 1 GiB of scratch per device
+  int64_t cap = std::max<int64_t>(1, std::min<int64_t>(want_points, budget / std::max<int64_t>(per_point, 1)));
+  if (cap <= d->chunk_cap) return PHC_OK;
+  DeviceGuard g(d->dev);
+  cudaDeviceSynchronize();
+  if (d->PT) cudaFree(d->PT);
+  if (d->Y) cudaFree(d->Y);
+  if (d->G) cudaFree(d->G);
+  d->PT = d->Y = d->G = nullptr;
+  d->chunk_cap = 0;
+  int rc;
+  const int64_t cd = 2 * s->L;
+  if ((rc = dalloc(&d->PT, (size_t)(cap * pt_pp * cd)))) return rc;
+  if ((rc = dalloc(&d->Y, (size_t)(cap * s->n_terms * cd)))) return rc;
+  if ((rc = dalloc(&d->G, (size_t)(cap * s->n_factors * cd)))) return rc;
+  d->chunk_cap = cap;
+  return PHC_OK;
+}
+
+template <int L, int MAXK>
+void launch_term(const phc_system* s, DeviceState* d, int64_t np, cudaStream_t st) {
+  dim3 grid((unsigned)((s->n_terms + 127) / 128), (unsigned)np);
+  phc::term_kernel<L, MAXK><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, d->PT, s->n_var, s->E, s->n_terms,
+                                                  s->n_factors, np, d->Y, d->G);
+}
+
+template <int L>
+int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
+                cudaStream_t st) {
+  int rc = ensure_scratch(s, d, n_points);
+  if (rc) return rc;
+  const int64_t cd = 2 * L;
+  for (int64_t p0 = 0; p0 < n_points; p0 += d->chunk_cap) {
+    const int64_t np = std::min(d->chunk_cap, n_points - p0);
+    const int64_t nth = np * (s->n_var + 1);
+    phc::power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * s->n_var * cd, s->n_var, s->E,
+                                                                              np, d->PT);
+    if (s->kmax <= 8)
+      launch_term<L, 8>(s, d, np, st);
+    else if (s->kmax <= 16)
+      launch_term<L, 16>(s, d, np, st);
+    else if (s->kmax <= 32)
+      launch_term<L, 32>(s, d, np, st);
+    else
+      launch_term<L, PHC_MAX_K>(s, d, np, st);
+    const int64_t ne = (int64_t)s->n_eq * s->n_var + s->n_eq;
+    dim3 grid((unsigned)((ne + 127) / 128), (unsigned)np);
+    phc::reduce_kernel<L><<<grid, 128, 0, st>>>(d->jptr, d->jidx, d->poly_ptr, d->Y, d->G, s->n_eq, s->n_var,
+                                                 s->n_terms, s->n_factors, np, f + p0 * s->n_eq * cd,
+                                                 jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return PHC_OK;
+}
+
+// Evaluate n_points points resident on device d, on stream st.
+int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
+                  cudaStream_t st) {
+  if (n_points <= 0) return PHC_OK;
+  if (d->have_block) {
+    int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, f, jac, st)
+                       : phc::run_block<4>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, f, jac, st);
+    if (rc) return fail(PHC_ECUDA, "block kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
+    return PHC_OK;
+  }
+  return s->L == 2 ? run_generic<2>(s, d, n_points, x, f, jac, st) : run_generic<4>(s, d, n_points, x, f, jac, st);
+}
+
+int ensure_stage(const phc_system* s, DeviceState* d, int64_t np) {
+  if (np <= d->stage_cap) return PHC_OK;
+  DeviceGuard g(d->dev);
+  cudaDeviceSynchronize();
+  if (d->xs) cudaFree(d->xs);
+  if (d->fs) cudaFree(d->fs);
+  if (d->js) cudaFree(d->js);
+  d->xs = d->fs = d->js = nullptr;
+  d->stage_cap = 0;
+  const int64_t cd = 2 * s->L;
+  int rc;
+  if ((rc = dalloc(&d->xs, (size_t)(np * s->n_var * cd)))) return rc;
+  if ((rc = dalloc(&d->fs, (size_t)(np * s->n_eq * cd)))) return rc;
+  if ((rc = dalloc(&d->js, (size_t)(np * (int64_t)s->n_eq * s->n_var * cd)))) return rc;
+  d->stage_cap = np;
+  return PHC_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* phc_last_error(void) { return g_err.c_str(); }
+const char* phc_version(void) { return "phc-b200 0.1 (sm_100a)"; }
+
+int phc_system_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_terms,
+                      const int64_t* poly_ptr, const int64_t* term_ptr, const int32_t* var_idx,
+                      const int32_t* exponent, const double* coeff, int32_t device) {
+  g_err.clear();
+  if (!out) return fail(PHC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_eq < 1 || n_var < 1) return fail(PHC_EINVAL, "n_eq and n_var must be >= 1 (got %d, %d)", n_eq, n_var);
+  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 (DD) or 4 (QD), got %d", limbs);
+  if (n_var > PHC_MAX_VARS) return fail(PHC_EUNSUPPORTED, "n_var %d exceeds %d", n_var, PHC_MAX_VARS);
+  if (n_terms < 0) return fail(PHC_EINVAL, "n_terms < 0");
+  if (!poly_ptr || !term_ptr || (n_terms > 0 && !coeff)) return fail(PHC_EINVAL, "NULL array");
+  if (poly_ptr[0] != 0 || poly_ptr[n_eq] != n_terms) return fail(PHC_EINVAL, "poly_ptr must start at 0 and end at n_terms");
+  for (int i = 0; i < n_eq; ++i)
+    if (poly_ptr[i + 1] < poly_ptr[i]) return fail(PHC_EINVAL, "poly_ptr not monotone at %d", i);
+  if (term_ptr[0] != 0) return fail(PHC_EINVAL, "term_ptr[0] must be 0");
+  for (int64_t t = 0; t < n_terms; ++t)
+    if (term_ptr[t + 1] < term_ptr[t]) return fail(PHC_EINVAL, "term_ptr not monotone at %lld", (long long)t);
+  const int64_t n_factors = term_ptr[n_terms];
+  if (n_factors > 0 && (!var_idx || !exponent)) return fail(PHC_EINVAL, "NULL var_idx/exponent");
+  int kmax = 0, emax = 1;
+  for (int64_t t = 0; t < n_terms; ++t) {
+    const int64_t a = term_ptr[t], b = term_ptr[t + 1];
+    if (b - a > PHC_MAX_K) return fail(PHC_EUNSUPPORTED, "term %lld has k = %lld > %d", (long long)t, (long long)(b - a), PHC_MAX_K);
+    kmax = std::max<int>(kmax, (int)(b - a));
+    for (int64_t q = a; q < b; ++q) {
+      if (var_idx[q] < 0 || var_idx[q] >= n_var)
+        return fail(PHC_EINVAL, "term %lld: variable index %d out of range [0, %d)", (long long)t, var_idx[q], n_var);
+      if (q > a && var_idx[q] <= var_idx[q - 1])
+        return fail(PHC_EINVAL, "term %lld: variable indices must be strictly increasing", (long long)t);
+      if (exponent[q] < 1) return fail(PHC_EINVAL, "term %lld: exponent %d < 1", (long long)t, exponent[q]);
+      if (exponent[q] > PHC_MAX_EXP) return fail(PHC_EUNSUPPORTED, "exponent %d > %d", exponent[q], PHC_MAX_EXP);
+      emax = std::max(emax, exponent[q]);
+    }
+  }
+  for (int64_t q = 0; q < n_terms * 2 * limbs; ++q)
+    if (!std::isfinite(coeff[q])) return fail(PHC_EINVAL, "coefficient limb %lld is not finite", (long long)q);
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    return fail(PHC_ECUDA, "no CUDA device available");
+  }
+  if (device < 0 || device >= ndev) return fail(PHC_EINVAL, "device %d out of range (have %d)", device, ndev);
+
+  std::unique_ptr<phc_system> s(new phc_system());
+  s->n_eq = n_eq;
+  s->n_var = n_var;
+  s->L = limbs;
+  s->home = device;
+  s->n_terms = n_terms;
+  s->n_factors = n_factors;
+  s->kmax = kmax;
+  s->E = emax;
+  s->poly_ptr.assign(poly_ptr, poly_ptr + n_eq + 1);
+  s->term_ptr.assign(term_ptr, term_ptr + n_terms + 1);
+  s->fac.resize(n_factors);
+  for (int64_t q = 0; q < n_factors; ++q) s->fac[q] = (uint32_t)var_idx[q] | ((uint32_t)exponent[q] << 16);
+  s->coeff.assign(coeff, coeff + n_terms * 2 * limbs);
+  // Jacobian CSR: for (i, v) the factor slots of terms of f_i on x_v, in factor order.
+  std::vector<int64_t> cnt((size_t)n_eq * n_var + 1, 0);
+  for (int i = 0; i < n_eq; ++i)
+    for (int64_t t = poly_ptr[i]; t < poly_ptr[i + 1]; ++t)
+      for (int64_t q = term_ptr[t]; q < term_ptr[t + 1]; ++q) cnt[(size_t)i * n_var + var_idx[q] + 1]++;
+  for (size_t e = 1; e < cnt.size(); ++e) {
+    if (cnt[e]) s->nnz++;
+    cnt[e] += cnt[e - 1];
+  }
+  s->jptr = cnt;
+  s->jidx.resize(n_factors);
+  {
+    std::vector<int64_t> pos(cnt.begin(), cnt.end() - 1);
+    for (int i = 0; i < n_eq; ++i)
+      for (int64_t t = poly_ptr[i]; t < poly_ptr[i + 1]; ++t)
+        for (int64_t q = term_ptr[t]; q < term_ptr[t + 1]; ++q) s->jidx[pos[(size_t)i * n_var + var_idx[q]]++] = q;
+  }
+  // operation counts actually performed per point (generic path: 4k-3 CM per term with k >= 1,
+  // (E-1) CM + (E-1) integer scalings per variable in the power table)
+  for (int64_t t = 0; t < n_terms; ++t) {
+    const int64_t k = term_ptr[t + 1] - term_ptr[t];
+    if (k >= 1) s->cm_per_point += 4 * k - 3;
+  }
+  s->cm_per_point += (int64_t)n_var * std::max(0, s->E - 1);
+  s->ca_per_point = n_factors + n_terms;  // one add per contribution into a zero-initialised sum
+  phc::plan_blocks(*s, &s->plan);
+  s->ca_per_point = s->plan.usable ? s->plan.ca_per_point : s->ca_per_point;
+  DeviceState* d;
+  int rc = get_device_state(s.get(), device, &d);
+  if (rc) return rc;
+  *out = s.release();
+  return PHC_OK;
+}
+
+void phc_system_destroy(phc_system* s) {
+  if (!s) return;
+  {
+    DeviceGuard g(s->home);
+    if (s->hx) cudaFree(s->hx);
+    if (s->hf) cudaFree(s->hf);
+    if (s->hj) cudaFree(s->hj);
+    if (s->hstream) cudaStreamDestroy(s->hstream);
+  }
+  s->devs.clear();
+  delete s;
+}
+
+int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double* x, double* f, double* jac,
+                            const int32_t* devices, int32_t n_devices, void* stream) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
+  if (n_points == 0) return PHC_OK;
+  if (!x || !f || !jac) return fail(PHC_EINVAL, "NULL x/f/jac");
+  if ((((uintptr_t)x) | ((uintptr_t)f) | ((uintptr_t)jac)) & 31) return fail(PHC_EINVAL, "x/f/jac must be 32-byte aligned");
+  std::vector<int> devs;
+  if (!devices || n_devices <= 0)
+    devs.push_back(s->home);
+  else
+    devs.assign(devices, devices + n_devices);
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  for (int dv : devs)
+    if (dv < 0 || dv >= ndev) return fail(PHC_EINVAL, "device %d out of range", dv);
+  cudaStream_t st = (cudaStream_t)stream;
+  DeviceGuard g(s->home);
+  const int64_t cd = 2 * s->L;
+  const int64_t G = (int64_t)devs.size();
+  if (G == 1 && devs[0] == s->home) {
+    DeviceState* d;
+    int rc = get_device_state(s, s->home, &d);
+    if (rc) return rc;
+    return run_on_device(s, d, n_points, x, f, jac, st);
+  }
+  // sharded: contiguous equal ranges [g P / G, (g+1) P / G)
+  cudaEvent_t start;
+  CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(start, st));
+  std::vector<cudaEvent_t> dones;
+  int rc = PHC_OK;
+  for (int64_t gi = 0; gi < G && rc == PHC_OK; ++gi) {
+    const int64_t p0 = gi * n_points / G, p1 = (gi + 1) * n_points / G;
+    const int64_t np = p1 - p0;
+    if (np == 0) continue;
+    const int dv = devs[gi];
+    DeviceState* d;
+    if ((rc = get_device_state(s, dv, &d))) break;
+    if (dv == s->home) {
+      rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, f + p0 * s->n_eq * cd,
+                         jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st);
+      continue;
+    }
+    DeviceGuard gd(dv);
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, dv, s->home);
+    if (can) {
+      cudaError_t pe = cudaDeviceEnablePeerAccess(s->home, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+    }
+    if ((rc = ensure_stage(s, d, np))) break;
+    if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
+    if (cudaMemcpyPeerAsync(d->xs, dv, x + p0 * s->n_var * cd, s->home, np * s->n_var * cd * 8, d->stream) != cudaSuccess) {
+      rc = fail(PHC_ECUDA, "scatter copy failed");
+      break;
+    }
+    if ((rc = run_on_device(s, d, np, d->xs, d->fs, d->js, d->stream))) break;
+    if (cudaMemcpyPeerAsync(f + p0 * s->n_eq * cd, s->home, d->fs, dv, np * s->n_eq * cd * 8, d->stream) != cudaSuccess ||
+        cudaMemcpyPeerAsync(jac + p0 * (int64_t)s->n_eq * s->n_var * cd, s->home, d->js, dv,
+                            np * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream) != cudaSuccess) {
+      rc = fail(PHC_ECUDA, "gather copy failed");
+      break;
+    }
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, d->stream);
+    dones.push_back(e);
+  }
+  for (cudaEvent_t e : dones) {
+    cudaStreamWaitEvent(st, e, 0);
+    cudaEventDestroy(e);
+  }
+  cudaEventDestroy(start);
+  return rc;
+}
+
+int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* jac, void* stream) {
+  return phc_eval_jacobian_batch(s, 1, x, f, jac, nullptr, 0, stream);
+}
+
+int phc_eval_jacobian_batch_host(const phc_system* cs, int64_t n_points, const double* x_host, double* f_host,
+                                 double* jac_host, const int32_t* devices, int32_t n_devices) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
+  if (n_points == 0) return PHC_OK;
+  if (!x_host || !f_host || !jac_host) return fail(PHC_EINVAL, "NULL host pointer");
+  DeviceGuard g(s->home);
+  const int64_t cd = 2 * s->L;
+  if (!s->hstream) CUDA_TRY(cudaStreamCreateWithFlags(&s->hstream, cudaStreamNonBlocking));
+  if (n_points > s->h_cap) {
+    cudaStreamSynchronize(s->hstream);
+    if (s->hx) cudaFree(s->hx);
+    if (s->hf) cudaFree(s->hf);
+    if (s->hj) cudaFree(s->hj);
+    s->hx = s->hf = s->hj = nullptr;
+    s->h_cap = 0;
+    int rc;
+    if ((rc = dalloc(&s->hx, (size_t)(n_points * s->n_var * cd)))) return rc;
+    if ((rc = dalloc(&s->hf, (size_t)(n_points * s->n_eq * cd)))) return rc;
+    if ((rc = dalloc(&s->hj, (size_t)(n_points * (int64_t)s->n_eq * s->n_var * cd)))) return rc;
+    s->h_cap = n_points;
+  }
+  CUDA_TRY(cudaMemcpyAsync(s->hx, x_host, n_points * s->n_var * cd * 8, cudaMemcpyHostToDevice, s->hstream));
+  int rc = phc_eval_jacobian_batch(s, n_points, s->hx, s->hf, s->hj, devices, n_devices, s->hstream);
+  if (rc) return rc;
+  CUDA_TRY(cudaMemcpyAsync(f_host, s->hf, n_points * s->n_eq * cd * 8, cudaMemcpyDeviceToHost, s->hstream));
+  CUDA_TRY(cudaMemcpyAsync(jac_host, s->hj, n_points * (int64_t)s->n_eq * s->n_var * cd * 8, cudaMemcpyDeviceToHost,
+                           s->hstream));
+  CUDA_TRY(cudaStreamSynchronize(s->hstream));
+  return PHC_OK;
+}
+
+int phc_system_stats(const phc_system* s, int64_t out[8]) {
+  if (!s || !out) return fail(PHC_EINVAL, "NULL argument");
+  out[0] = s->n_terms;
+  out[1] = s->n_factors;
+  out[2] = s->kmax;
+  out[3] = s->E;
+  out[4] = s->nnz;
+  out[5] = s->plan.usable ? s->plan.cm_per_point : s->cm_per_point;
+  out[6] = s->ca_per_point;
+  out[7] = s->plan.usable ? s->plan.launches : 3;
+  return PHC_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// FP64 peak microbenchmark
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void dfma_chains_kernel(double* out, int iters, double a, double b) {
+  double r[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) r[c] = threadIdx.x * 1e-9 + c;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int c = 0; c < 8; ++c) r[c] = __fma_rn(r[c], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) s += r[c];
+  if (s == 12345.678) out[0] = s;
+}
+}  // namespace
+
+extern "C" int phc_fp64_peak(int32_t device, double ms_target, double* tflops) {
+  g_err.clear();
+  if (!tflops) return fail(PHC_EINVAL, "NULL out");
+  DeviceGuard g(device);
+  cudaDeviceProp p;
+  CUDA_TRY(cudaGetDeviceProperties(&p, device));
+  double* d;
+  CUDA_TRY(cudaMalloc(&d, 8));
+  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  for (int w = 0; w < 3; ++w) dfma_chains_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(e0);
+  dfma_chains_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms1;
+  cudaEventElapsedTime(&ms1, e0, e1);
+  int reps = std::max(1, (int)(ms_target / std::max(ms1, 1e-3f)));
+  cudaEventRecord(e0);
+  for (int r = 0; r < reps; ++r) dfma_chains_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
+  cudaEventRecord(e1);
+  cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  cudaError_t err = cudaGetLastError();
+  cudaFree(d);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (err != cudaSuccess) return fail(PHC_ECUDA, "peak kernel: %s", cudaGetErrorString(err));
+  *tflops = 2.0 * blocks * (double)threads * iters * 8 * reps / (ms * 1e-3) / 1e12;
+  return PHC_OK;
+}

@@ -1,0 +1,106 @@
+"""Object wrapper over the C ABI taking torch tensors (device memory) and torch streams."""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+
+def _ptr(a):
+    return ctypes.c_void_p(a.ctypes.data) if isinstance(a, np.ndarray) else ctypes.c_void_p(a.data_ptr())
+
+
+class System:
+    """A system handle: ``System(arrays, device=0)`` with ``arrays`` having the attributes
+    n_eq, n_var, limbs, poly_ptr, term_ptr, var_idx, exponent, coeff (include/phc.h layout)."""
+
+    def __init__(self, arrays, device: int = 0):
+        self.n_eq = int(arrays.n_eq)
+        self.n_var = int(arrays.n_var)
+        self.limbs = int(arrays.limbs)
+        self.device = int(device)
+        pp = np.ascontiguousarray(arrays.poly_ptr, dtype=np.int64)
+        tp = np.ascontiguousarray(arrays.term_ptr, dtype=np.int64)
+        vi = np.ascontiguousarray(arrays.var_idx, dtype=np.int32)
+        ex = np.ascontiguousarray(arrays.exponent, dtype=np.int32)
+        cf = np.ascontiguousarray(arrays.coeff, dtype=np.float64)
+        self.n_terms = int(tp.shape[0] - 1)
+        self._h = None
+        self._h = _lib.phc_system_create(self.n_eq, self.n_var, self.limbs, self.n_terms, _ptr(pp), _ptr(tp),
+                                         _ptr(vi), _ptr(ex), _ptr(cf), self.device)
+
+    def close(self):
+        if self._h is not None:
+            _lib.phc_system_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def stats(self):
+        keys = ("n_terms", "n_factors", "kmax", "D", "nnz_J", "cm_per_point", "ca_per_point", "launches")
+        return dict(zip(keys, _lib.phc_system_stats(self._h)))
+
+    def _check(self, t, shape):
+        import torch
+
+        if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+            raise ValueError("expected a contiguous float64 CUDA tensor")
+        if tuple(t.shape) != tuple(shape):
+            raise ValueError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
+
+    def eval(self, x, f=None, jac=None, stream=None):
+        """x: [n_var, 2, L] float64 on the home device -> (f [n_eq,2,L], jac [n_eq,n_var,2,L])."""
+        import torch
+
+        L = self.limbs
+        self._check(x, (self.n_var, 2, L))
+        if f is None:
+            f = torch.empty((self.n_eq, 2, L), dtype=torch.float64, device=x.device)
+        if jac is None:
+            jac = torch.empty((self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=x.device)
+        st = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+        _lib.phc_eval_jacobian(self._h, _ptr(x), _ptr(f), _ptr(jac), ctypes.c_void_p(st))
+        return f, jac
+
+    def eval_batch(self, X, F=None, J=None, devices=None, stream=None):
+        """X: [P, n_var, 2, L] on the home device -> (F [P,n_eq,2,L], J [P,n_eq,n_var,2,L])."""
+        import torch
+
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        if F is None:
+            F = torch.empty((P, self.n_eq, 2, L), dtype=torch.float64, device=X.device)
+        if J is None:
+            J = torch.empty((P, self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=X.device)
+        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        if devices:
+            dv = (ctypes.c_int32 * len(devices))(*devices)
+            nd = len(devices)
+        else:
+            dv, nd = None, 0
+        _lib.phc_eval_jacobian_batch(self._h, P, _ptr(X), _ptr(F), _ptr(J), dv, nd, ctypes.c_void_p(st))
+        return F, J
+
+    def eval_batch_host(self, X, F=None, J=None, devices=None):
+        """Host arrays (numpy or pinned CPU tensors) in and out; synchronous."""
+        L = self.limbs
+        P = int(X.shape[0])
+        if F is None:
+            F = np.empty((P, self.n_eq, 2, L))
+        if J is None:
+            J = np.empty((P, self.n_eq, self.n_var, 2, L))
+        if devices:
+            dv = (ctypes.c_int32 * len(devices))(*devices)
+            nd = len(devices)
+        else:
+            dv, nd = None, 0
+        _lib.phc_eval_jacobian_batch_host(self._h, P, _ptr(X), _ptr(F), _ptr(J), dv, nd)
+        return F, J

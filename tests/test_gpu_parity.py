@@ -1,0 +1,217 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+Element-by-element comparison on seeded BASELINE.json configs (tiny, c2, c3 full;
+batch and large on sampled points/rows at full size in the bench launch
+configuration), special systems with exactly representable results (bitwise),
+edge cases, metamorphic and determinism properties."""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from _parity import TOL, compare_point, limbs_normalised, oracle_point  # noqa: E402
+from oracle import ExactArith, evaluate_system  # noqa: E402
+from synthetic import (config_system, limbs_from_values, special_gaussian_system,  # noqa: E402
+                       special_linear_system, system_from_terms, random_system, homogeneous_system)
+
+
+@pytest.fixture(scope="module")
+def phc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1109_0545_b200 as m
+    return m
+
+
+def gpu_eval(phc, s, X, devices=None):
+    h = phc.System(s, device=0)
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    if X.shape[0] == 1 and devices is None:
+        f, j = h.eval(Xd[0])
+        torch.cuda.synchronize()
+        return f.cpu().numpy()[None], j.cpu().numpy()[None], h
+    F, J = h.eval_batch(Xd, devices=devices)
+    torch.cuda.synchronize()
+    return F.cpu().numpy(), J.cpu().numpy(), h
+
+
+@pytest.mark.parametrize("name,seed", [("tiny", 1), ("tiny", 2), ("tiny", 3), ("c2", 1), ("c2", 2), ("c2", 3),
+                                       ("c3", 1), ("c3", 2)])
+def test_config_full_exact(phc, name, seed):
+    s, X = config_system(name, seed=seed)
+    f, j, _ = gpu_eval(phc, s, X)
+    ar, F, J = oracle_point(s, X[0], arith="exact")
+    ef, ej = compare_point(ar, F, J, f[0], j[0], s.limbs)
+    assert ef <= TOL[s.limbs] and ej <= TOL[s.limbs], (ef, ej)
+    assert limbs_normalised(f) and limbs_normalised(j)
+    # structural zeros are exact zeros
+    nz = np.zeros((s.n_eq, s.n_var), bool)
+    for i in range(s.n_eq):
+        for _, fac in s.terms(i):
+            for v, _a in fac:
+                nz[i, v] = True
+    assert (j[0][~nz] == 0).all()
+
+
+def test_batch_config_sampled(phc):
+    """batch: n=32, m=32, k=16, 65,536 points, DD; exact oracle on sampled points including
+    the first and last point of every 8-way shard."""
+    s, X = config_system("batch", seed=1)
+    F, J, _ = gpu_eval(phc, s, X)
+    P = X.shape[0]
+    pts = sorted({0, P - 1, 12345, 40000} | {g * P // 8 for g in range(8)} | {(g + 1) * P // 8 - 1 for g in range(8)})
+    for p in pts:
+        ar, Fr, Jr = oracle_point(s, X[p], arith="exact")
+        ef, ej = compare_point(ar, Fr, Jr, F[p], J[p], 2)
+        assert ef <= TOL[2] and ej <= TOL[2], (p, ef, ej)
+
+
+def test_large_single_sampled_rows(phc):
+    """large: n=256, m=256, k=32, D=8, QD, single point; mp512 oracle on sampled rows."""
+    s, X = config_system("large", seed=1)
+    f, j, _ = gpu_eval(phc, s, X)
+    rows = [0, 77, 128, 255]
+    ar, F, J = oracle_point(s, X[0], rows=rows, arith="mp")
+    ef, ej = compare_point(ar, F, J, f[0], j[0], 4, rows)
+    assert ef <= TOL[4] and ej <= TOL[4], (ef, ej)
+    assert limbs_normalised(f) and limbs_normalised(j)
+
+
+def test_large_batch_point0_and_samples(phc):
+    """large x 4096: batch point p equals the single-point call at p (bitwise); sampled rows."""
+    s, X = config_system("large_batch", seed=1)
+    F, J, h = gpu_eval(phc, s, X)
+    Xd = torch.from_numpy(X[0]).cuda()
+    f0, j0 = h.eval(Xd)
+    torch.cuda.synchronize()
+    assert np.array_equal(F[0], f0.cpu().numpy()) and np.array_equal(J[0], j0.cpu().numpy())
+    for p in (1, 2047, 4095):
+        ar, Fr, Jr = oracle_point(s, X[p], rows=[3, 200], arith="mp")
+        ef, ej = compare_point(ar, Fr, Jr, F[p], J[p], 4, [3, 200])
+        assert ef <= TOL[4] and ej <= TOL[4], (p, ef, ej)
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_gaussian_integer_bitwise(phc, L):
+    """P5: Z[i] coefficients, x in {±1, ±i}: exact result, GPU must match bitwise."""
+    s, X = special_gaussian_system(12, 9, 5, 4, L, seed=7)
+    f, j, _ = gpu_eval(phc, s, X)
+    F, J = evaluate_system(s, X[0], "exact", workers=1)
+    ar = ExactArith()
+    from oracle import exact_equal_limbs
+    assert exact_equal_limbs(ar, F, f[0])
+    assert exact_equal_limbs(ar, [v for row in J for v in row], j[0].reshape(-1, 2, L))
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_linear_system_J_is_C(phc, L):
+    """P4: k = 1, a = 1 -> J equals the coefficient matrix bitwise."""
+    s, X, C, x = special_linear_system(33, L, seed=2)
+    f, j, _ = gpu_eval(phc, s, X)
+    assert np.array_equal(j[0][:, :, :, 0], C.astype(np.float64))
+    assert (j[0][:, :, :, 1:] == 0).all()
+    Cc = C[:, :, 0] + 1j * C[:, :, 1]
+    Fn = Cc @ (x[:, 0] + 1j * x[:, 1])
+    assert np.array_equal(f[0][:, 0, 0], Fn.real) and np.array_equal(f[0][:, 1, 0], Fn.imag)
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_edge_cases_mixed_k(phc, L):
+    """Constant terms (k=0), k=1, duplicate terms, an empty polynomial, zero coordinates,
+    a term in every variable, mixed k within a polynomial."""
+    n = 9
+    polys = [
+        [[], [(0, 1)], [(0, 1)], [(1, 3), (4, 1)]],            # constant, duplicates
+        [],                                                     # empty polynomial: F = 0, J row = 0
+        [[(v, 1 + v % 3) for v in range(n)]],                   # every variable (k = n)
+        [[(2, 2)], [(2, 2), (3, 1)], [(0, 1), (5, 7), (8, 2)]],  # mixed k
+        [[(3, 1)], [(3, 2), (6, 1)]],                           # x_3 = 0 below
+    ] + [[[(v, 2), ((v + 1) % n, 1)] if v + 1 < n else [(0, 1), (v, 2)]] for v in range(4)]
+    T = sum(len(p) for p in polys)
+    rng = np.random.default_rng(5)
+    vals = [complex(a, b) for a, b in rng.uniform(-1, 1, (T, 2))]
+    coeff = limbs_from_values(vals, L)
+    s = system_from_terms(len(polys), n, L, polys, coeff)
+    xv = [complex(a, b) for a, b in rng.uniform(-1, 1, (n, 2))]
+    xv[3] = 0
+    X = limbs_from_values(xv, L)[None]
+    f, j, _ = gpu_eval(phc, s, X)
+    ar, F, J = oracle_point(s, X[0], arith="exact")
+    ef, ej = compare_point(ar, F, J, f[0], j[0], L)
+    assert ef <= TOL[L] and ej <= TOL[L], (ef, ej)
+    assert (f[0][1] == 0).all() and (j[0][1] == 0).all()
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_ragged_and_many_points(phc, L):
+    """A ragged system (k varying 0..12, m not a multiple of 32) over 37 points."""
+    rng = np.random.default_rng(11)
+    n = 23
+    polys = []
+    for i in range(n):
+        terms = []
+        for t in range(int(rng.integers(1, 45))):
+            k = int(rng.integers(0, 13))
+            vs = sorted(rng.choice(n, k, replace=False).tolist())
+            terms.append([(v, int(rng.integers(1, 6))) for v in vs])
+        polys.append(terms)
+    T = sum(len(p) for p in polys)
+    s0, _ = random_system(2, 1, 1, 1, L, seed=1)  # unit-circle helpers
+    from synthetic.systems import unit_circle_limbs
+    coeff = unit_circle_limbs(rng.uniform(0, 6.283, T), L, 1)
+    s = system_from_terms(n, n, L, polys, coeff)
+    X = unit_circle_limbs(rng.uniform(0, 6.283, (37, n)), L, 1)
+    F, J, _ = gpu_eval(phc, s, X)
+    for p in (0, 17, 36):
+        ar, Fr, Jr = oracle_point(s, X[p], arith="exact")
+        ef, ej = compare_point(ar, Fr, Jr, F[p], J[p], L)
+        assert ef <= TOL[L] and ej <= TOL[L], (p, ef, ej)
+
+
+def test_euler_identity_full_batch(phc):
+    """P8 at size: homogeneous system over 2,048 points, sum_v x_v J_iv = d_i f_i checked in
+    float64 on every point (a property that needs no oracle)."""
+    s, X, degs = homogeneous_system(24, 20, 6, 9, 2, seed=9, points=2048)
+    F, J, _ = gpu_eval(phc, s, X)
+    f = F[:, :, 0, 0] + 1j * F[:, :, 1, 0]
+    jj = J[..., 0, 0] + 1j * J[..., 1, 0]
+    x = X[..., 0, 0] + 1j * X[..., 1, 0]
+    lhs = np.einsum("piv,pv->pi", jj, x)
+    rhs = f * np.asarray(degs)[None, :]
+    assert np.max(np.abs(lhs - rhs)) <= 1e-12 * np.max(np.abs(rhs))
+
+
+@pytest.mark.parametrize("name", ["c2", "c3"])
+def test_conjugation_and_scaling_bitwise(phc, name):
+    """P9: conj(inputs) -> conj(outputs) bitwise; coefficients * 2^s -> outputs * 2^s bitwise."""
+    s, X = config_system(name, seed=2, points=64)
+    F, J, _ = gpu_eval(phc, s, X)
+    sc = s.__class__(**{**s.__dict__})
+    sc.coeff = s.coeff.copy()
+    sc.coeff[:, 1, :] *= -1
+    Xc = X.copy()
+    Xc[:, :, 1, :] *= -1
+    Fc, Jc, _ = gpu_eval(phc, sc, Xc)
+    assert np.array_equal(Fc[:, :, 0], F[:, :, 0]) and np.array_equal(Fc[:, :, 1], -F[:, :, 1])
+    assert np.array_equal(Jc[..., 0, :], J[..., 0, :]) and np.array_equal(Jc[..., 1, :], -J[..., 1, :])
+    ss = s.__class__(**{**s.__dict__})
+    ss.coeff = s.coeff * 2.0 ** -7
+    Fs, Js, _ = gpu_eval(phc, ss, X)
+    assert np.array_equal(Fs, F * 2.0 ** -7) and np.array_equal(Js, J * 2.0 ** -7)
+
+
+def test_determinism_and_device_lists(phc):
+    """P10: repeated runs and device lists with repeats are bitwise equal; host API equals device API."""
+    s, X = config_system("batch", seed=3, points=1000)
+    F1, J1, h = gpu_eval(phc, s, X)
+    F2, J2, _ = gpu_eval(phc, s, X, devices=[0, 0, 0])
+    F3, J3, _ = gpu_eval(phc, s, X, devices=[0, 0, 0, 0, 0, 0, 0, 0])
+    assert np.array_equal(F1, F2) and np.array_equal(J1, J2)
+    assert np.array_equal(F1, F3) and np.array_equal(J1, J3)
+    Fh, Jh = h.eval_batch_host(np.ascontiguousarray(X))
+    assert np.array_equal(F1, Fh) and np.array_equal(J1, Jh)
+    Xd = torch.from_numpy(X[513]).cuda()
+    f, j = h.eval(Xd)
+    torch.cuda.synchronize()
+    assert np.array_equal(F1[513], f.cpu().numpy()) and np.array_equal(J1[513], j.cpu().numpy())
