@@ -112,6 +112,14 @@ int phc_system_stats(const phc_system* s, int64_t out[8]);
  * DFMA chains over `ms_target` milliseconds; the SURVEY.md §8(d) denominator. */
 int phc_fp64_peak(int32_t device, double ms_target, double* tflops);
 
+/* Kernel timing for measurement (bench.py's roofline).  When enabled, every kernel the
+ * handle launches on its HOME device is bracketed by CUDA events recorded on the stream
+ * it is launched on.  phc_profile_read synchronises those events and returns, per kernel
+ * class c (0 power table, 1 term/monomial stage, 2 reductions, 3 fused block kernel),
+ * the summed milliseconds ms[c] and launch counts launches[c]; reset != 0 clears them. */
+int phc_profile_enable(const phc_system* s, int enable);
+int phc_profile_read(const phc_system* s, double ms[4], int64_t launches[4], int reset);
+
 /* Thread-local message describing the last failure in this thread ("" if none). */
 const char* phc_last_error(void);
 

@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libphc.so")
+LIB_PATH = os.environ.get("PHC_LIB") or os.path.join(_HERE, "libphc.so")
 
 PHC_OK = 0
 PHC_EINVAL = -1
@@ -28,6 +28,8 @@ EXPORTED = (
     "phc_eval_jacobian_batch_host",
     "phc_system_stats",
     "phc_fp64_peak",
+    "phc_profile_enable",
+    "phc_profile_read",
     "phc_last_error",
     "phc_version",
 )
@@ -61,6 +63,10 @@ def _load():
     lib.phc_system_stats.restype = ctypes.c_int
     lib.phc_fp64_peak.argtypes = [i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
     lib.phc_fp64_peak.restype = ctypes.c_int
+    lib.phc_profile_enable.argtypes = [P, ctypes.c_int]
+    lib.phc_profile_enable.restype = ctypes.c_int
+    lib.phc_profile_read.argtypes = [P, P, P, ctypes.c_int]
+    lib.phc_profile_read.restype = ctypes.c_int
     lib.phc_last_error.argtypes = []
     lib.phc_last_error.restype = ctypes.c_char_p
     lib.phc_version.argtypes = []
@@ -112,6 +118,17 @@ def phc_fp64_peak(device=0, ms_target=200.0):
     v = ctypes.c_double()
     check(lib.phc_fp64_peak(device, ms_target, ctypes.byref(v)))
     return v.value
+
+
+def phc_profile_enable(h, enable=True):
+    return check(lib.phc_profile_enable(h, 1 if enable else 0))
+
+
+def phc_profile_read(h, reset=True):
+    ms = (ctypes.c_double * 4)()
+    n = (ctypes.c_int64 * 4)()
+    check(lib.phc_profile_read(h, ms, n, 1 if reset else 0))
+    return list(ms), list(n)
 
 
 def phc_last_error():

@@ -1,7 +1,37 @@
-// Warp-per-monomial-block kernels (placeholder: enabled in a later step).
+// Fused warp-per-monomial-block kernel: power table, Speelpenning products, coefficient
+// product and both reductions in one launch (BASELINE.json
+// north_star "one-warp-per-monomial-block Speelpenning products ... warp-shuffle DD/QD
+// reduction per polynomial and per Jacobian entry").
+//
+// Layout (host plan, plan_blocks below):
+//  * The terms of polynomial i are cut into blocks of <= 32 terms, one term per lane.
+//  * Every lane runs K factor slots (K = compiled bound >= max k; shorter terms are padded
+//    with a dummy variable whose power-table row is U = 1, Dd = 0).  The order of a term's
+//    factors over the slots is chosen by a bipartite edge colouring (lanes x variables) so
+//    that at any slot at most R lanes of a block touch the same variable, and each such
+//    lane owns a distinct replica r < R of the Jacobian row accumulator.  The Speelpenning
+//    scheme needs no particular factor order (P:549-561 only uses "the product of all
+//    factors but one"), so the colouring changes rounding order only.
+//  * fac[block][slot][lane] = var | exp << 16 | rep << 24   (coalesced 128 B per slot)
+//  * coef[block][lane][2][L]                                (256-bit vector loads)
+//
+// Per lane (= per term c * prod u_j, u_j = x_{v_j}^{a_j}, d_j = a_j x_{v_j}^{a_j-1}):
+//   backward: s_1 = u_K, s_q = s_{q-1} u_{K-q+1}              (suffixes, the paper's phi)
+//   forward : r_0 = c, g_m = r_{m-1} d_m s_{K-m}, r_m = r_{m-1} u_m  (prefixes psi with c)
+//   value y = r_K; g_m is added into row[rep][var] in shared memory (conflict-free by the
+//   colouring), slot after slot.  y is reduced over the warp with a shuffle tree.
+// That is 4K-3 complex products per term, against the paper's 6k-5.
+//
+// Work split (fixed per system, so every point is evaluated bitwise identically):
+//  * mode A (few blocks per polynomial): a CTA takes one point and a group of
+//    polynomials; warp w owns polynomials w, w+NW, ...; it accumulates all their blocks in
+//    its private rows and writes F[i] and J[i][:] itself.
+//  * mode B (many blocks per polynomial): a CTA takes one (point, polynomial); warp w owns
+//    blocks w, w+NW, ...; the CTA sums the warps' rows in warp order.
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <vector>
 
@@ -9,30 +39,557 @@
 
 namespace phc {
 
+constexpr int kWarp = 32;
+constexpr int kBlockWarps = 8;  // NW: warps per CTA
+constexpr uint32_t kDummyVar = 0xFFFFu;
+#ifndef PHC_DD_MINB
+#define PHC_DD_MINB 1  // CTAs per SM the DD block kernel is register-capped for
+#endif
+
 struct BlockTables {
   uint32_t* fac = nullptr;
   double* coeff = nullptr;
-  int32_t* blk = nullptr;
+  int32_t* blk = nullptr;  // poly_blk_ptr [n_eq + 1]
+  double* PT = nullptr;    // global power table scratch (PT_SMEM == false)
+  int64_t pt_cap = 0;
 };
 
 struct HostBlockPlan {
   bool usable = false;
+  int K = 0;           // slots per lane (compiled bound)
+  int R = 1;           // replicas per row
+  int E = 1;           // max exponent
+  int mode = 0;        // 0 = A, 1 = B
+  int polys_per_cta = 1;
+  bool pt_smem = true;
+  int64_t n_blocks = 0;
+  size_t smem_bytes = 0;
+  std::vector<uint32_t> fac;
+  std::vector<double> coeff;
+  std::vector<int32_t> blk;
   int64_t cm_per_point = 0;
   int64_t ca_per_point = 0;
-  int launches = 0;
+  int launches = 1;
 };
 
-template <class S>
-void plan_blocks(const S&, HostBlockPlan* plan) {
-  plan->usable = false;
+struct BlockArgs {
+  const uint32_t* fac;
+  const double* coef;
+  const int32_t* blk;
+  const double* X;
+  const double* PTg;
+  double* F;
+  double* J;
+  int64_t n_points;
+  int n_eq, n_var, E, R, mode, polys_per_cta;
+};
+
+// ---------------------------------------------------------------------------
+// device helpers: shared-memory complex access and warp shuffles
+// ---------------------------------------------------------------------------
+template <int L>
+PHC_DEV typename Prec<L>::C sload(const double* p) {
+  typename Prec<L>::C v;
+  const double2* q = reinterpret_cast<const double2*>(p);
+  if constexpr (L == 2) {
+    double2 a = q[0], b = q[1];
+    v.re.x[0] = a.x; v.re.x[1] = a.y; v.im.x[0] = b.x; v.im.x[1] = b.y;
+  } else {
+    double2 a = q[0], b = q[1], c = q[2], d = q[3];
+    v.re.x[0] = a.x; v.re.x[1] = a.y; v.re.x[2] = b.x; v.re.x[3] = b.y;
+    v.im.x[0] = c.x; v.im.x[1] = c.y; v.im.x[2] = d.x; v.im.x[3] = d.y;
+  }
+  return v;
+}
+template <int L>
+PHC_DEV void sstore(double* p, const typename Prec<L>::C& v) {
+  double2* q = reinterpret_cast<double2*>(p);
+  if constexpr (L == 2) {
+    q[0] = make_double2(v.re.x[0], v.re.x[1]);
+    q[1] = make_double2(v.im.x[0], v.im.x[1]);
+  } else {
+    q[0] = make_double2(v.re.x[0], v.re.x[1]);
+    q[1] = make_double2(v.re.x[2], v.re.x[3]);
+    q[2] = make_double2(v.im.x[0], v.im.x[1]);
+    q[3] = make_double2(v.im.x[2], v.im.x[3]);
+  }
+}
+template <int L>
+PHC_DEV typename Prec<L>::C shfl_down(const typename Prec<L>::C& v, int d) {
+  typename Prec<L>::C r;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    r.re.x[i] = __shfl_down_sync(0xffffffffu, v.re.x[i], d);
+    r.im.x[i] = __shfl_down_sync(0xffffffffu, v.im.x[i], d);
+  }
+  return r;
+}
+// lane 0 receives the sum over the warp in a fixed tree order
+template <int L>
+PHC_DEV typename Prec<L>::C warp_sum(typename Prec<L>::C v) {
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) v = Prec<L>::add(v, shfl_down<L>(v, d));
+  return v;
 }
 
-inline int upload_block_tables(const HostBlockPlan&, BlockTables*) { return 0; }
-
+// Power-table row of variable v (row a2): U[a-1] = x^a, Dd[a-1] = a x^(a-1), a = 1..E.
 template <int L>
-int run_block(const HostBlockPlan&, const BlockTables&, int, int, int64_t, const double*, double*, double*,
-              cudaStream_t) {
-  return -1;
+PHC_DEV void power_row(const typename Prec<L>::C& x, int E, double* row, bool smem) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  C pw = P::one();
+  for (int a = 1; a <= E; ++a) {
+    const C dd = (a == 1) ? pw : P::mul_int(pw, (double)a);
+    pw = (a == 1) ? x : P::mul(pw, x);
+    if (smem) {
+      sstore<L>(row + (E + a - 1) * 2 * L, dd);
+      sstore<L>(row + (a - 1) * 2 * L, pw);
+    } else {
+      cstore<L>(row + (E + a - 1) * 2 * L, dd);
+      cstore<L>(row + (a - 1) * 2 * L, pw);
+    }
+  }
+}
+template <int L>
+PHC_DEV void dummy_row(int E, double* row, bool smem) {
+  using P = Prec<L>;
+  for (int a = 1; a <= E; ++a) {
+    if (smem) {
+      sstore<L>(row + (a - 1) * 2 * L, P::one());
+      sstore<L>(row + (E + a - 1) * 2 * L, P::zero());
+    } else {
+      cstore<L>(row + (a - 1) * 2 * L, P::one());
+      cstore<L>(row + (E + a - 1) * 2 * L, P::zero());
+    }
+  }
+}
+
+// Global power table for configurations whose table does not fit in shared memory.
+template <int L>
+__global__ void block_power_table_kernel(const double* __restrict__ X, int n_var, int E, int64_t n_points,
+                                         double* __restrict__ PT) {
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per = n_var + 1;
+  if (gid >= n_points * per) return;
+  const int64_t p = gid / per;
+  const int v = (int)(gid % per);
+  double* row = PT + (p * per + v) * (2 * E) * (2 * L);
+  if (v == n_var)
+    dummy_row<L>(E, row, false);
+  else
+    power_row<L>(cload<L>(X + (p * n_var + v) * 2 * L), E, row, false);
+}
+
+// One block of 32 terms on one warp: Speelpenning chain + accumulation into `rows`
+// (R replicas of n_var complex) in shared memory; returns the warp-reduced term sum
+// on lane 0.
+template <int L, int K, bool PT_SMEM>
+PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double* pt, double* rows, int lane) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  const int twoE = 2 * a.E;
+  const uint32_t* fw = a.fac + (size_t)b * K * kWarp + lane;
+  auto ptr_u = [&](uint32_t word) {
+    uint32_t v = word & 0xffffu;
+    v = (v == kDummyVar) ? (uint32_t)a.n_var : v;
+    return pt + ((size_t)v * twoE + ((word >> 16) & 0xffu) - 1) * (2 * L);
+  };
+  auto ld = [&](const double* p) { return PT_SMEM ? sload<L>(p) : cload<L>(p); };
+  C s[K];  // suffix products: registers for DD (fully unrolled), local memory for QD
+  C r = cload<L>(a.coef + ((size_t)b * kWarp + lane) * 2 * L);
+  // forward step m (1-based): contribution g_m = r_{m-1} d_m s_{K-m}, then r_m = r_{m-1} u_m
+  auto fwd = [&](int m, uint32_t word) {
+    const double* pu = ptr_u(word);
+    C g = P::mul(r, ld(pu + a.E * 2 * L));
+    if (m < K) g = P::mul(g, s[K - m]);
+    const uint32_t v = word & 0xffffu;
+    if (v != kDummyVar) {
+      double* acc = rows + ((size_t)(word >> 24) * a.n_var + v) * 2 * L;
+      sstore<L>(acc, P::add(sload<L>(acc), g));
+    }
+    __syncwarp();
+    r = P::mul(r, ld(pu));
+  };
+  if constexpr (L == 2) {
+    uint32_t w[K];
+#pragma unroll
+    for (int q = 0; q < K; ++q) w[q] = __ldg(fw + q * kWarp);
+    s[1] = ld(ptr_u(w[K - 1]));
+#pragma unroll
+    for (int q = 2; q <= K - 1; ++q) s[q] = P::mul(s[q - 1], ld(ptr_u(w[K - q])));
+#pragma unroll
+    for (int m = 1; m <= K; ++m) fwd(m, w[m - 1]);
+  } else {
+    s[1] = ld(ptr_u(__ldg(fw + (K - 1) * kWarp)));
+#pragma unroll 1
+    for (int q = 2; q <= K - 1; ++q) s[q] = P::mul(s[q - 1], ld(ptr_u(__ldg(fw + (K - q) * kWarp))));
+#pragma unroll 1
+    for (int m = 1; m <= K; ++m) fwd(m, __ldg(fw + (m - 1) * kWarp));
+  }
+  return warp_sum<L>(r);
+}
+
+template <int L, int K, bool PT_SMEM>
+__global__ void __launch_bounds__(kBlockWarps * kWarp, (L == 2 ? PHC_DD_MINB : 1))
+block_kernel(const BlockArgs a) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  extern __shared__ __align__(16) double smem[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int cd = 2 * L;
+  const int twoE = 2 * a.E;
+  const int64_t units_per_point =
+      a.mode == 0 ? (a.n_eq + a.polys_per_cta - 1) / a.polys_per_cta : (int64_t)a.n_eq;
+  const int64_t p = blockIdx.x / units_per_point;
+  const int unit = (int)(blockIdx.x % units_per_point);
+  if (p >= a.n_points) return;
+
+  double* pt;
+  double* rows_all;
+  if constexpr (PT_SMEM) {
+    pt = smem;
+    rows_all = smem + (size_t)(a.n_var + 1) * twoE * cd;
+    for (int v = threadIdx.x; v <= a.n_var; v += blockDim.x) {
+      double* row = pt + (size_t)v * twoE * cd;
+      if (v == a.n_var)
+        dummy_row<L>(a.E, row, true);
+      else
+        power_row<L>(cload<L>(a.X + (p * a.n_var + v) * cd), a.E, row, true);
+    }
+  } else {
+    pt = const_cast<double*>(a.PTg) + p * (int64_t)(a.n_var + 1) * twoE * cd;
+    rows_all = smem;
+  }
+  const size_t row_elems = (size_t)a.R * a.n_var * cd;
+  double* rows = rows_all + warp * row_elems;
+  double* fpart = rows_all + kBlockWarps * row_elems;  // mode B: per-warp F partials
+  __syncthreads();
+
+  if (a.mode == 0) {
+    const int i0 = unit * a.polys_per_cta;
+    const int i1 = min(a.n_eq, i0 + a.polys_per_cta);
+    for (int i = i0 + warp; i < i1; i += kBlockWarps) {
+      for (size_t e = lane; e < row_elems; e += kWarp) rows[e] = 0.0;
+      __syncwarp();
+      C fsum = P::zero();
+      for (int b = a.blk[i]; b < a.blk[i + 1]; ++b) {
+        C y = do_block<L, K, PT_SMEM>(a, b, pt, rows, lane);
+        fsum = P::add(fsum, y);
+      }
+      __syncwarp();
+      if (lane == 0) cstore<L>(a.F + (p * a.n_eq + i) * cd, fsum);
+      double* jrow = a.J + (p * a.n_eq + i) * (int64_t)a.n_var * cd;
+      for (int v = lane; v < a.n_var; v += kWarp) {
+        C acc = sload<L>(rows + (size_t)v * cd);
+        for (int r = 1; r < a.R; ++r) acc = P::add(acc, sload<L>(rows + ((size_t)r * a.n_var + v) * cd));
+        cstore<L>(jrow + (size_t)v * cd, acc);
+      }
+      __syncwarp();
+    }
+  } else {
+    const int i = unit;
+    for (size_t e = lane; e < row_elems; e += kWarp) rows[e] = 0.0;
+    __syncwarp();
+    C fsum = P::zero();
+    for (int b = a.blk[i] + warp; b < a.blk[i + 1]; b += kBlockWarps) {
+      C y = do_block<L, K, PT_SMEM>(a, b, pt, rows, lane);
+      fsum = P::add(fsum, y);
+    }
+    if (lane == 0) sstore<L>(fpart + warp * cd, fsum);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      C f = sload<L>(fpart);
+      for (int w2 = 1; w2 < kBlockWarps; ++w2) f = P::add(f, sload<L>(fpart + w2 * cd));
+      cstore<L>(a.F + (p * a.n_eq + i) * cd, f);
+    }
+    double* jrow = a.J + (p * a.n_eq + i) * (int64_t)a.n_var * cd;
+    for (int v = threadIdx.x; v < a.n_var; v += blockDim.x) {
+      C acc = sload<L>(rows_all + (size_t)v * cd);
+      for (int w2 = 0; w2 < kBlockWarps; ++w2)
+        for (int r = (w2 == 0 ? 1 : 0); r < a.R; ++r)
+          acc = P::add(acc, sload<L>(rows_all + w2 * row_elems + ((size_t)r * a.n_var + v) * cd));
+      cstore<L>(jrow + (size_t)v * cd, acc);
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side: plan (blocks, edge colouring, packing), upload, launch
+// ---------------------------------------------------------------------------
+inline int compiled_K(int kmax) {
+  static const int ks[] = {2, 4, 8, 12, 16, 20, 24, 32};
+  for (int k : ks)
+    if (kmax <= k) return k;
+  return 0;
+}
+
+// Colour the edges (lane, var-replica) of one block with K colours so that no two edges
+// at a lane or at a replica node share a colour (Konig: possible when every degree <= K).
+// in: terms[lane] = list of (var, exp); out: slot[lane][j] for factor j, rep[lane][j].
+inline bool colour_block(const std::vector<std::vector<std::pair<int, int>>>& terms, int n_var, int K, int R,
+                         std::vector<std::vector<int>>* slot, std::vector<std::vector<int>>* rep) {
+  const int nl = (int)terms.size();
+  // replica assignment: round-robin over the occurrences of each variable (lane order)
+  std::vector<int> seen(n_var, 0);
+  rep->assign(nl, {});
+  slot->assign(nl, {});
+  for (int l = 0; l < nl; ++l) {
+    for (auto& f : terms[l]) (*rep)[l].push_back(seen[f.first]++ % R);
+    (*slot)[l].assign(terms[l].size(), -1);
+  }
+  const int nodes = n_var * R;
+  std::vector<int> atL((size_t)nl * K, -1), atR((size_t)nodes * K, -1);  // colour -> neighbour
+  std::vector<int> eL((size_t)nl * K, -1), eR((size_t)nodes * K, -1);    // colour -> factor index j
+  for (int l = 0; l < nl; ++l) {
+    for (int j = 0; j < (int)terms[l].size(); ++j) {
+      const int w = terms[l][j].first * R + (*rep)[l][j];
+      int ca = -1, cb = -1;
+      for (int c = 0; c < K && ca < 0; ++c)
+        if (atL[(size_t)l * K + c] < 0) ca = c;
+      for (int c = 0; c < K && cb < 0; ++c)
+        if (atR[(size_t)w * K + c] < 0) cb = c;
+      if (ca < 0 || cb < 0) return false;
+      if (atR[(size_t)w * K + ca] >= 0) {
+        // flip the ca/cb alternating path starting at replica node w
+        std::vector<std::pair<int, int>> path;  // (right node, left node) pairs along the path
+        int rn = w, c = ca;
+        while (true) {
+          const int ln = atR[(size_t)rn * K + c];
+          if (ln < 0) break;
+          path.push_back({rn, ln});
+          const int c2 = (c == ca) ? cb : ca;
+          const int rn2 = atL[(size_t)ln * K + c2];
+          if (rn2 < 0) break;
+          path.push_back({rn2, ln});
+          rn = rn2;
+          c = (c2 == ca) ? cb : ca;
+          if (path.size() > (size_t)4 * (nl + nodes)) return false;
+        }
+        // recolour every edge on the path: swap ca <-> cb
+        struct Ed { int l, r, j, c; };
+        std::vector<Ed> eds;
+        for (size_t q = 0; q < path.size(); ++q) {
+          const int rr = path[q].first, ll = path[q].second;
+          const int cc = (q % 2 == 0) ? ca : cb;
+          eds.push_back({ll, rr, eL[(size_t)ll * K + cc], cc});
+        }
+        for (auto& e : eds) {
+          atL[(size_t)e.l * K + e.c] = -1;
+          atR[(size_t)e.r * K + e.c] = -1;
+          eL[(size_t)e.l * K + e.c] = -1;
+          eR[(size_t)e.r * K + e.c] = -1;
+        }
+        for (auto& e : eds) {
+          const int nc = (e.c == ca) ? cb : ca;
+          atL[(size_t)e.l * K + nc] = e.r;
+          atR[(size_t)e.r * K + nc] = e.l;
+          eL[(size_t)e.l * K + nc] = e.j;
+          eR[(size_t)e.r * K + nc] = e.j;
+          (*slot)[e.l][e.j] = nc;
+        }
+        if (atR[(size_t)w * K + ca] >= 0 || atL[(size_t)l * K + ca] >= 0) return false;
+      }
+      atL[(size_t)l * K + ca] = w;
+      atR[(size_t)w * K + ca] = l;
+      eL[(size_t)l * K + ca] = j;
+      eR[(size_t)w * K + ca] = j;
+      (*slot)[l][j] = ca;
+    }
+  }
+  return true;
+}
+
+template <class S>
+void plan_blocks(const S& s, HostBlockPlan* plan) {
+  plan->usable = false;
+  const int K = compiled_K(std::max(s.kmax, 1));
+  if (K == 0 || s.n_var >= (int)kDummyVar) return;
+  const int L = s.L;
+  const int E = s.E;
+  // blocks
+  std::vector<int32_t> blk(1, 0);
+  std::vector<std::vector<int64_t>> bterms;
+  int max_blocks_per_poly = 0;
+  for (int i = 0; i < s.n_eq; ++i) {
+    int nb = 0;
+    for (int64_t t = s.poly_ptr[i]; t < s.poly_ptr[i + 1]; t += kWarp, ++nb) {
+      std::vector<int64_t> ts;
+      for (int64_t u = t; u < std::min<int64_t>(t + kWarp, s.poly_ptr[i + 1]); ++u) ts.push_back(u);
+      bterms.push_back(ts);
+    }
+    blk.push_back((int32_t)bterms.size());
+    max_blocks_per_poly = std::max(max_blocks_per_poly, nb);
+  }
+  const int64_t nb = (int64_t)bterms.size();
+  // replicas needed: max over blocks and variables of ceil(d_v / K)
+  int R = 1;
+  for (auto& ts : bterms) {
+    std::vector<int> d(s.n_var, 0);
+    for (int64_t t : ts)
+      for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q) d[s.fac[q] & 0xffffu]++;
+    for (int v = 0; v < s.n_var; ++v) R = std::max(R, (d[v] + K - 1) / K);
+  }
+  if (R > 255) return;
+  std::vector<uint32_t> fac((size_t)nb * K * kWarp);
+  std::vector<double> coef((size_t)nb * kWarp * 2 * L, 0.0);
+  for (int64_t b = 0; b < nb; ++b) {
+    std::vector<std::vector<std::pair<int, int>>> terms;
+    for (int64_t t : bterms[b]) {
+      std::vector<std::pair<int, int>> f;
+      for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q)
+        f.push_back({(int)(s.fac[q] & 0xffffu), (int)((s.fac[q] >> 16) & 0xffu)});
+      terms.push_back(f);
+    }
+    std::vector<std::vector<int>> slot, rep;
+    if (!colour_block(terms, s.n_var, K, R, &slot, &rep)) return;
+    for (int l = 0; l < kWarp; ++l) {
+      for (int q = 0; q < K; ++q) fac[((size_t)b * K + q) * kWarp + l] = kDummyVar | (1u << 16);
+      if (l >= (int)terms.size()) continue;
+      for (size_t j = 0; j < terms[l].size(); ++j) {
+        const int q = slot[l][j];
+        fac[((size_t)b * K + q) * kWarp + l] =
+            (uint32_t)terms[l][j].first | ((uint32_t)terms[l][j].second << 16) | ((uint32_t)rep[l][j] << 24);
+      }
+      const int64_t t = bterms[b][l];
+      for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
+    }
+  }
+  const size_t cdb = (size_t)2 * L * sizeof(double);
+  const size_t pt_bytes = (size_t)(s.n_var + 1) * 2 * E * cdb;
+  const size_t rows_bytes = (size_t)kBlockWarps * R * s.n_var * cdb + kBlockWarps * cdb;
+  plan->pt_smem = pt_bytes + rows_bytes <= (size_t)160 * 1024;
+  plan->smem_bytes = (plan->pt_smem ? pt_bytes : 0) + rows_bytes;
+  if (plan->smem_bytes > (size_t)200 * 1024) return;
+  plan->mode = max_blocks_per_poly >= 4 ? 1 : 0;
+  plan->polys_per_cta = plan->mode == 0 ? std::min(s.n_eq, 4 * kBlockWarps) : 1;
+  plan->K = K;
+  plan->R = R;
+  plan->E = E;
+  plan->n_blocks = nb;
+  plan->fac.swap(fac);
+  plan->coeff.swap(coef);
+  plan->blk.swap(blk);
+  // operation counts per point (useful work: real terms and factors only)
+  int64_t cm = (int64_t)s.n_var * std::max(0, E - 1);
+  for (int64_t t = 0; t < s.n_terms; ++t) {
+    const int64_t k = s.term_ptr[t + 1] - s.term_ptr[t];
+    if (k >= 1) cm += 4 * k - 3;
+  }
+  plan->cm_per_point = cm;
+  plan->ca_per_point = s.n_factors + s.n_terms + (int64_t)s.n_eq * s.n_var * (R - 1);
+  plan->launches = plan->pt_smem ? 1 : 2;
+  plan->usable = true;
+}
+
+inline int upload_block_tables(const HostBlockPlan& plan, BlockTables* bt) {
+  if (cudaMalloc(&bt->fac, std::max<size_t>(4, plan.fac.size() * 4)) != cudaSuccess) return -2;
+  if (cudaMalloc(&bt->coeff, std::max<size_t>(8, plan.coeff.size() * 8)) != cudaSuccess) return -2;
+  if (cudaMalloc(&bt->blk, plan.blk.size() * 4) != cudaSuccess) return -2;
+  if (cudaMemcpy(bt->fac, plan.fac.data(), plan.fac.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return -3;
+  if (cudaMemcpy(bt->coeff, plan.coeff.data(), plan.coeff.size() * 8, cudaMemcpyHostToDevice) != cudaSuccess) return -3;
+  if (cudaMemcpy(bt->blk, plan.blk.data(), plan.blk.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess) return -3;
+  return 0;
+}
+
+template <int L, int K, bool PTS>
+int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_points, cudaStream_t st) {
+  auto kern = block_kernel<L, K, PTS>;
+  if (plan.smem_bytes > 48 * 1024)
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes) != cudaSuccess)
+      return -3;
+  const int64_t units = a.mode == 0 ? (a.n_eq + a.polys_per_cta - 1) / a.polys_per_cta : a.n_eq;
+  const int64_t max_grid = (int64_t)1 << 30;
+  for (int64_t p0 = 0; p0 < n_points;) {
+    const int64_t np = std::min<int64_t>(n_points - p0, max_grid / units);
+    BlockArgs b = a;
+    b.X = a.X + p0 * a.n_var * 2 * L;
+    b.F = a.F + p0 * a.n_eq * 2 * L;
+    b.J = a.J + p0 * (int64_t)a.n_eq * a.n_var * 2 * L;
+    if (!PTS) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
+    b.n_points = np;
+    kern<<<(unsigned)(np * units), kBlockWarps * kWarp, plan.smem_bytes, st>>>(b);
+    if (cudaGetLastError() != cudaSuccess) return -3;
+    p0 += np;
+  }
+  return 0;
+}
+
+// The block kernels are instantiated in separate translation units (generated by
+// __graft_entry__.build(), compiled in parallel); everyone else sees extern declarations.
+#define PHC_FOR_EACH_K(X, L, P) X(L, 2, P) X(L, 4, P) X(L, 8, P) X(L, 12, P) X(L, 16, P) X(L, 20, P) X(L, 24, P) X(L, 32, P)
+#ifndef PHC_INSTANTIATE_BLOCK
+#define PHC_EXTERN_K(L, K, P) \
+  extern template int launch_block_k<L, K, P>(const HostBlockPlan&, const BlockArgs&, int64_t, cudaStream_t);
+PHC_FOR_EACH_K(PHC_EXTERN_K, 2, true)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 2, false)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 4, true)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 4, false)
+#undef PHC_EXTERN_K
+#endif
+
+template <int L, bool PTS>
+int launch_block_pts(const HostBlockPlan& plan, const BlockArgs& a, int64_t np, cudaStream_t st) {
+  switch (plan.K) {
+    case 2: return launch_block_k<L, 2, PTS>(plan, a, np, st);
+    case 4: return launch_block_k<L, 4, PTS>(plan, a, np, st);
+    case 8: return launch_block_k<L, 8, PTS>(plan, a, np, st);
+    case 12: return launch_block_k<L, 12, PTS>(plan, a, np, st);
+    case 16: return launch_block_k<L, 16, PTS>(plan, a, np, st);
+    case 20: return launch_block_k<L, 20, PTS>(plan, a, np, st);
+    case 24: return launch_block_k<L, 24, PTS>(plan, a, np, st);
+    case 32: return launch_block_k<L, 32, PTS>(plan, a, np, st);
+  }
+  return -4;
+}
+
+// Runs the fused path for n_points points resident on the current device.
+template <int L>
+int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, int64_t n_points, const double* x,
+              double* f, double* jac, cudaStream_t st) {
+  BlockArgs a;
+  a.fac = bt.fac;
+  a.coef = bt.coeff;
+  a.blk = bt.blk;
+  a.X = x;
+  a.PTg = nullptr;
+  a.F = f;
+  a.J = jac;
+  a.n_points = n_points;
+  a.n_eq = n_eq;
+  a.n_var = n_var;
+  a.E = plan.E;
+  a.R = plan.R;
+  a.mode = plan.mode;
+  // mode A: results do not depend on how polynomials are grouped into CTAs (each warp
+  // owns whole polynomials), so the grouping is chosen per call: one polynomial per warp
+  // for few points (latency), up to 32 per CTA for batches (amortises the power table).
+  a.polys_per_cta = plan.mode == 0 ? (n_points >= 4 * 148 ? std::min(n_eq, 4 * kBlockWarps) : std::min(n_eq, kBlockWarps)) : 1;
+  if (plan.pt_smem) return launch_block_pts<L, true>(plan, a, n_points, st);
+  // global power table, in chunks of points that fit a 512 MiB scratch
+  const int64_t per_point = (int64_t)(n_var + 1) * 2 * plan.E * 2 * L;
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)64 << 20) / per_point));
+  if (bt.pt_cap < chunk) {
+    if (bt.PT) cudaFree(bt.PT);
+    bt.PT = nullptr;
+    bt.pt_cap = 0;
+    if (cudaMalloc(&bt.PT, (size_t)(chunk * per_point * 8)) != cudaSuccess) return -2;
+    bt.pt_cap = chunk;
+  }
+  for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
+    const int64_t np = std::min(chunk, n_points - p0);
+    const int64_t nth = np * (n_var + 1);
+    block_power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * n_var * 2 * L, n_var,
+                                                                               plan.E, np, bt.PT);
+    BlockArgs b = a;
+    b.X = x + p0 * n_var * 2 * L;
+    b.F = f + p0 * n_eq * 2 * L;
+    b.J = jac + p0 * (int64_t)n_eq * n_var * 2 * L;
+    b.PTg = bt.PT;
+    b.n_points = np;
+    int rc = launch_block_pts<L, false>(plan, b, np, st);
+    if (rc) return rc;
+  }
+  return 0;
 }
 
 }  // namespace phc

@@ -91,7 +91,7 @@ struct DeviceState {
     DeviceGuard g(dev);
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)bt.fac, (void*)bt.coeff,
-                    (void*)bt.blk})
+                    (void*)bt.blk, (void*)bt.PT})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (done) cudaEventDestroy(done);
@@ -118,9 +118,46 @@ struct phc_system {
   double *hx = nullptr, *hf = nullptr, *hj = nullptr;
   int64_t h_cap = 0;
   cudaStream_t hstream = nullptr;
+  // kernel timing (phc_profile_*): events on the launch stream, home device only
+  bool prof = false;
+  struct Rec { int cls; cudaEvent_t a, b; };
+  std::vector<Rec> recs;
+  std::vector<cudaEvent_t> pool;
+  double prof_ms[4] = {0, 0, 0, 0};
+  int64_t prof_n[4] = {0, 0, 0, 0};
 };
 
 namespace {
+
+cudaEvent_t pool_event(phc_system* s) {
+  if (!s->pool.empty()) {
+    cudaEvent_t e = s->pool.back();
+    s->pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e = nullptr;
+  cudaEventCreate(&e);
+  return e;
+}
+
+// Brackets one kernel launch with events on its stream when profiling is on.
+struct ProfScope {
+  phc_system* s;
+  int cls;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  ProfScope(const phc_system* cs, int dev, int cls_, cudaStream_t st_) : s(const_cast<phc_system*>(cs)), cls(cls_), st(st_) {
+    if (!s->prof || dev != s->home) { s = nullptr; return; }
+    a = pool_event(s);
+    cudaEventRecord(a, st);
+  }
+  ~ProfScope() {
+    if (!s) return;
+    cudaEvent_t b = pool_event(s);
+    cudaEventRecord(b, st);
+    s->recs.push_back({cls, a, b});
+  }
+};
 
 size_t cbytes(const phc_system* s) { return (size_t)2 * s->L * sizeof(double); }
 
@@ -189,6 +226,7 @@ int ensure_scratch(const phc_system* s, DeviceState* d, int64_t want_points) {
 template <int L, int MAXK>
 void launch_term(const phc_system* s, DeviceState* d, int64_t np, cudaStream_t st) {
   dim3 grid((unsigned)((s->n_terms + 127) / 128), (unsigned)np);
+  ProfScope ps(s, d->dev, 1, st);
   phc::term_kernel<L, MAXK><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, d->PT, s->n_var, s->E, s->n_terms,
                                                   s->n_factors, np, d->Y, d->G);
 }
@@ -202,8 +240,11 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
   for (int64_t p0 = 0; p0 < n_points; p0 += d->chunk_cap) {
     const int64_t np = std::min(d->chunk_cap, n_points - p0);
     const int64_t nth = np * (s->n_var + 1);
+    {
+    ProfScope ps(s, d->dev, 0, st);
     phc::power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * s->n_var * cd, s->n_var, s->E,
                                                                               np, d->PT);
+    }
     if (s->kmax <= 8)
       launch_term<L, 8>(s, d, np, st);
     else if (s->kmax <= 16)
@@ -214,6 +255,7 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
       launch_term<L, PHC_MAX_K>(s, d, np, st);
     const int64_t ne = (int64_t)s->n_eq * s->n_var + s->n_eq;
     dim3 grid((unsigned)((ne + 127) / 128), (unsigned)np);
+    ProfScope ps(s, d->dev, 2, st);
     phc::reduce_kernel<L><<<grid, 128, 0, st>>>(d->jptr, d->jidx, d->poly_ptr, d->Y, d->G, s->n_eq, s->n_var,
                                                  s->n_terms, s->n_factors, np, f + p0 * s->n_eq * cd,
                                                  jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
@@ -227,6 +269,7 @@ int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const d
                   cudaStream_t st) {
   if (n_points <= 0) return PHC_OK;
   if (d->have_block) {
+    ProfScope ps(s, d->dev, 3, st);
     int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, f, jac, st)
                        : phc::run_block<4>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, f, jac, st);
     if (rc) return fail(PHC_ECUDA, "block kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
@@ -361,6 +404,11 @@ void phc_system_destroy(phc_system* s) {
     if (s->hstream) cudaStreamDestroy(s->hstream);
   }
   s->devs.clear();
+  {
+    DeviceGuard g(s->home);
+    for (auto& r : s->recs) { cudaEventDestroy(r.a); cudaEventDestroy(r.b); }
+    for (auto e : s->pool) cudaEventDestroy(e);
+  }
   delete s;
 }
 
@@ -478,6 +526,35 @@ int phc_eval_jacobian_batch_host(const phc_system* cs, int64_t n_points, const d
   CUDA_TRY(cudaMemcpyAsync(jac_host, s->hj, n_points * (int64_t)s->n_eq * s->n_var * cd * 8, cudaMemcpyDeviceToHost,
                            s->hstream));
   CUDA_TRY(cudaStreamSynchronize(s->hstream));
+  return PHC_OK;
+}
+
+int phc_profile_enable(const phc_system* cs, int enable) {
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  s->prof = enable != 0;
+  return PHC_OK;
+}
+
+int phc_profile_read(const phc_system* cs, double ms[4], int64_t launches[4], int reset) {
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s || !ms || !launches) return fail(PHC_EINVAL, "NULL argument");
+  DeviceGuard g(s->home);
+  for (auto& r : s->recs) {
+    CUDA_TRY(cudaEventSynchronize(r.b));
+    float t = 0;
+    CUDA_TRY(cudaEventElapsedTime(&t, r.a, r.b));
+    s->prof_ms[r.cls] += t;
+    s->prof_n[r.cls] += 1;
+    s->pool.push_back(r.a);
+    s->pool.push_back(r.b);
+  }
+  s->recs.clear();
+  for (int c = 0; c < 4; ++c) {
+    ms[c] = s->prof_ms[c];
+    launches[c] = s->prof_n[c];
+    if (reset) { s->prof_ms[c] = 0; s->prof_n[c] = 0; }
+  }
   return PHC_OK;
 }
 
