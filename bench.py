@@ -28,11 +28,6 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# Executed FP64 flops per operation of the arithmetic core (DADD = DMUL = 1, DFMA = 2),
-# counted from arith.cuh and checked against ncu's sm__sass_thread_inst_executed_op_d*
-# counters (profiles/).  Keys: complex mul, complex add, complex
-# times small integer.
-EXEC_FLOPS = {2: dict(cm=50, ca=22, ci=16), 4: dict(cm=714, ca=182, ci=130)}
 # SURVEY.md §8(d) frozen model (paper-faithful op counts, standard DD costs)
 MODEL_FLOPS = {2: dict(cm=80, ca=40), 4: dict(cm=800, ca=200)}
 
@@ -87,10 +82,9 @@ def model_counts(s, st):
 
 
 def exec_flops_per_point(s, st):
-    """Executed FP64 flops per point of the kernels as built (their op counts x core costs)."""
-    e = EXEC_FLOPS[s.limbs]
-    ci = s.n_var * max(0, int(st["D"]) - 1)
-    return st["cm_per_point"] * e["cm"] + st["ca_per_point"] * e["ca"] + ci * e["ci"]
+    """Executed FP64 flops per point of the kernels' useful work, as counted by the library
+    (phc_system_stats out[8]; per-op costs from arith.cuh, checked against ncu)."""
+    return int(st["exec_flops_per_point"])
 
 
 class ClockSampler:
@@ -290,14 +284,9 @@ def main():
         names = ["power_table", "term", "reduce", "fused_block"]
         dom = max(range(4), key=lambda i: kms[i])
         dom_ms = kms[dom] / max(kn[dom], 1)
-        if dom == 3:
-            dom_flops = exec_pp * P / max(kn[dom] / args.steps, 1)
-        elif dom == 1:
-            e = EXEC_FLOPS[s.limbs]
-            tm = st["cm_per_point"] - s.n_var * max(0, int(st["D"]) - 1)
-            dom_flops = tm * e["cm"] * P / max(kn[dom] / args.steps, 1)
-        else:
-            dom_flops = 0.0
+        # the dominant kernel does (nearly) all of the step's FP64 work: the fused block
+        # kernel all of it, the generic term kernel all but the power table and sums
+        dom_flops = exec_pp * P / max(kn[dom] / args.steps, 1) if dom in (1, 3) else 0.0
         achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
         step_exec_tflops = exec_pp * P / (ms / args.steps * 1e-3) / 1e12
         step_model_tflops = model_flops_pp * P / (ms / args.steps * 1e-3) / 1e12

@@ -105,8 +105,12 @@ int phc_eval_jacobian_batch_host(const phc_system* s, int64_t n_points, const do
  * out[0] = n_terms, out[1] = n_factors, out[2] = max k, out[3] = max exponent D,
  * out[4] = nnz(J) (structurally nonzero entries), out[5] = complex multiplies per point
  * performed by the kernels, out[6] = complex additions per point performed by the kernels,
- * out[7] = kernel launches per eval call (single point). */
-int phc_system_stats(const phc_system* s, int64_t out[8]);
+ * out[7] = kernel launches per eval call (single point), out[8] = executed FP64 flops per
+ * point of the kernels' useful work (DADD = DMUL = 1, DFMA = 2; padding lanes/slots not
+ * counted), out[9] = path (0 generic, 1 fused block), out[10] = block layout,
+ * out[11] = slots per lane K. */
+#define PHC_STATS_LEN 12
+int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]);
 
 /* FP64 pipe peak of `device` in TFLOP/s (2 flops per DFMA), measured with independent
  * DFMA chains over `ms_target` milliseconds; the SURVEY.md §8(d) denominator. */

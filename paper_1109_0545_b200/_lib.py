@@ -109,7 +109,7 @@ def phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices):
 
 
 def phc_system_stats(h):
-    out = (ctypes.c_int64 * 8)()
+    out = (ctypes.c_int64 * 12)()
     check(lib.phc_system_stats(h, out))
     return list(out)
 

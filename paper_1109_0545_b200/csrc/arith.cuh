@@ -202,6 +202,59 @@ template <> struct Prec<2> {
     }
     return r;
   }
+  // "lazy" product: the same dot products, without the final renormalisation of each real
+  // part, so (hi, lo) may have |lo| a few ulps of hi (or exceed hi after cancellation).
+  // Every later product forms hi*hi exactly and the cross terms with FMA, so the
+  // normwise error stays O(u^2 |a||b|).
+  PHC_DEV static C mul_lazy(const C& a, const C& b) {
+    C r;
+    {
+      double p1, e1, p2, e2, s, t;
+      two_prod(a.re.x[0], b.re.x[0], p1, e1);
+      two_prod(a.im.x[0], b.im.x[0], p2, e2);
+      two_sum(p1, -p2, s, t);
+      t = add_(t, sub_(e1, e2));
+      t = fma_(a.re.x[0], b.re.x[1], t);
+      t = fma_(a.re.x[1], b.re.x[0], t);
+      t = fma_(-a.im.x[0], b.im.x[1], t);
+      t = fma_(-a.im.x[1], b.im.x[0], t);
+      r.re.x[0] = s;
+      r.re.x[1] = t;
+    }
+    {
+      double p1, e1, p2, e2, s, t;
+      two_prod(a.re.x[0], b.im.x[0], p1, e1);
+      two_prod(a.im.x[0], b.re.x[0], p2, e2);
+      two_sum(p1, p2, s, t);
+      t = add_(t, add_(e1, e2));
+      t = fma_(a.re.x[0], b.im.x[1], t);
+      t = fma_(a.re.x[1], b.im.x[0], t);
+      t = fma_(a.im.x[0], b.re.x[1], t);
+      t = fma_(a.im.x[1], b.re.x[0], t);
+      r.im.x[0] = s;
+      r.im.x[1] = t;
+    }
+    return r;
+  }
+  // lazy sum: exact two_sum of the leading parts, low parts summed without renormalising
+  PHC_DEV static C add_lazy(const C& a, const C& b) {
+    C r;
+    double s, e;
+    two_sum(a.re.x[0], b.re.x[0], s, e);
+    r.re.x[0] = s;
+    r.re.x[1] = add_(add_(a.re.x[1], b.re.x[1]), e);
+    two_sum(a.im.x[0], b.im.x[0], s, e);
+    r.im.x[0] = s;
+    r.im.x[1] = add_(add_(a.im.x[1], b.im.x[1]), e);
+    return r;
+  }
+  // renormalise a lazy value: (hi, lo) -> two_sum(hi, lo)
+  PHC_DEV static C norm(const C& a) {
+    C r;
+    two_sum(a.re.x[0], a.re.x[1], r.re.x[0], r.re.x[1]);
+    two_sum(a.im.x[0], a.im.x[1], r.im.x[0], r.im.x[1]);
+    return r;
+  }
   // multiply by a small positive integer s (exact in binary64): product exact via two_prod
   PHC_DEV static real mul_int_real(const real& a, double s) {
     double p, e;
@@ -227,6 +280,9 @@ template <> struct Prec<4> {
     r.im = qd_add(qd_mul(a.re, b.im), qd_mul(a.im, b.re));
     return r;
   }
+  PHC_DEV static C mul_lazy(const C& a, const C& b) { return mul(a, b); }
+  PHC_DEV static C add_lazy(const C& a, const C& b) { return add(a, b); }
+  PHC_DEV static C norm(const C& a) { return a; }
   PHC_DEV static real mul_int_real(const real& a, double s) {
     // a_j * s = p_j + e_j exactly; collect by order of magnitude
     double p0, p1, p2, p3, e0, e1, e2;

@@ -50,7 +50,7 @@ struct BlockTables {
   uint32_t* fac = nullptr;
   double* coeff = nullptr;
   int32_t* blk = nullptr;  // poly_blk_ptr [n_eq + 1]
-  double* PT = nullptr;    // global power table scratch (PT_SMEM == false)
+  double* PT = nullptr;    // global power table scratch (layout 0)
   int64_t pt_cap = 0;
 };
 
@@ -61,7 +61,7 @@ struct HostBlockPlan {
   int E = 1;           // max exponent
   int mode = 0;        // 0 = A, 1 = B
   int polys_per_cta = 1;
-  bool pt_smem = true;
+  int layout = 1;      // see LAYOUT above
   int64_t n_blocks = 0;
   size_t smem_bytes = 0;
   std::vector<uint32_t> fac;
@@ -69,8 +69,19 @@ struct HostBlockPlan {
   std::vector<int32_t> blk;
   int64_t cm_per_point = 0;
   int64_t ca_per_point = 0;
+  int64_t exec_flops_per_point = 0;
   int launches = 1;
 };
+
+// Executed FP64 flops (DADD = DMUL = 1, DFMA = 2) of the arithmetic core's operations,
+// counted from arith.cuh (and checked against ncu's sm__sass_thread_inst_executed_op_d*):
+// complex mul, lazy complex mul, complex add, lazy complex add, renormalisation,
+// complex times small integer.
+struct OpFlops { int cm, cm_lazy, ca, ca_lazy, norm, ci; };
+inline OpFlops op_flops(int L) {
+  if (L == 2) return {50, 44, 22, 16, 12, 16};
+  return {714, 714, 182, 182, 0, 130};
+}
 
 struct BlockArgs {
   const uint32_t* fac;
@@ -180,56 +191,159 @@ __global__ void block_power_table_kernel(const double* __restrict__ X, int n_var
     power_row<L>(cload<L>(X + (p * n_var + v) * 2 * L), E, row, false);
 }
 
-// One block of 32 terms on one warp: Speelpenning chain + accumulation into `rows`
-// (R replicas of n_var complex) in shared memory; returns the warp-reduced term sum
-// on lane 0.
-template <int L, int K, bool PT_SMEM>
+// Shared-memory layouts of the power table (PT) and of the Jacobian row accumulators.
+//  LAYOUT 0: PT in global memory ([v][2E][2L], per point), rows in shared memory as R
+//            replicas [r][v][2L] per warp.
+//  LAYOUT 1: PT in shared memory ([v][2E][2L]), rows as in layout 0.
+//  LAYOUT 2: "class-interleaved" (small n): lane class c = lane & 7 owns a private copy of
+//            the PT and of the rows; chunk j (a double2) of entry e of class c lives at
+//            double2 index (j * NE + e) * 8 + c.  The 8 lanes of a quarter-warp (which one
+//            LDS.128/STS.128 wavefront serves) are the 8 classes, so every access is
+//            bank-conflict free whatever variables the lanes touch.  Rows need no replicas:
+//            the edge colouring keeps the 4 lanes of a class on distinct variables per slot.
+constexpr int kClasses = 8;
+
+template <int L>
+PHC_DEV void cls_store(double2* base, int NE, int e, int c, const typename Prec<L>::C& v) {
+  double d[2 * L];
+#pragma unroll
+  for (int i = 0; i < L; ++i) { d[i] = v.re.x[i]; d[L + i] = v.im.x[i]; }
+#pragma unroll
+  for (int j = 0; j < L; ++j) base[((size_t)j * NE + e) * kClasses + c] = make_double2(d[2 * j], d[2 * j + 1]);
+}
+template <int L>
+PHC_DEV typename Prec<L>::C cls_load(const double2* base, int NE, int e, int c) {
+  double d[2 * L];
+#pragma unroll
+  for (int j = 0; j < L; ++j) {
+    const double2 q = base[((size_t)j * NE + e) * kClasses + c];
+    d[2 * j] = q.x;
+    d[2 * j + 1] = q.y;
+  }
+  typename Prec<L>::C v;
+#pragma unroll
+  for (int i = 0; i < L; ++i) { v.re.x[i] = d[i]; v.im.x[i] = d[L + i]; }
+  return v;
+}
+
+// One block of 32 terms on one warp: Speelpenning products + accumulation into the
+// warp's rows in shared memory; returns the warp-reduced term sum on lane 0.
+//
+// Per lane, factors j = 1..K (slot order), u_j = x^{a_j}, d_j = a_j x^{a_j - 1}:
+//   prefixes P_0 = c, P_j = P_{j-1} u_j          (the paper's psi_j with c folded in)
+//   suffixes S_0 = 1, S_q = S_{q-1} u_{K-q+1}    (the paper's phi_q)
+//   g_m = P_{m-1} S_{K-m} d_m                     (c * d/dx of the term for factor m)
+//   y   = P_K                                      (the term's value)
+// Both chains run at once (the paper's psi and phi recurrences): in phase 1
+// (t = 1..H, H = K/2) P_1..P_H and S_1..S_H are formed and P_0..P_{H-1}, S_1..S_{H-1}
+// kept; in phase 2 (t = 1..H) the running P_{H+t-1} and S_{H+t-1} each meet a kept
+// partner, giving g_{H+t} = P_{H+t-1} S_{H-t} d_{H+t} and g_{H-t+1} = P_{H-t} S_{H+t-1}
+// d_{H-t+1}, before both chains advance.  4K-3 complex products, critical path K
+// products (two independent chains) instead of 2K-2 for a backward-then-forward sweep.
+template <int L, int K, int LAYOUT>
 PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double* pt, double* rows, int lane) {
   using P = Prec<L>;
   using C = typename P::C;
+  constexpr int H = K / 2;
+  static_assert(K % 2 == 0, "K must be even");
   const int twoE = 2 * a.E;
+  const int cls = lane & (kClasses - 1);
+  const int NE = (a.n_var + 1) * twoE;
   const uint32_t* fw = a.fac + (size_t)b * K * kWarp + lane;
-  auto ptr_u = [&](uint32_t word) {
+  // entry index of U(var, exp) in the power table; Dd is E entries further
+  auto entry = [&](uint32_t word) {
     uint32_t v = word & 0xffffu;
     v = (v == kDummyVar) ? (uint32_t)a.n_var : v;
-    return pt + ((size_t)v * twoE + ((word >> 16) & 0xffu) - 1) * (2 * L);
+    return (int)(v * twoE + ((word >> 16) & 0xffu) - 1);
   };
-  auto ld = [&](const double* p) { return PT_SMEM ? sload<L>(p) : cload<L>(p); };
-  C s[K];  // suffix products: registers for DD (fully unrolled), local memory for QD
-  C r = cload<L>(a.coef + ((size_t)b * kWarp + lane) * 2 * L);
-  // forward step m (1-based): contribution g_m = r_{m-1} d_m s_{K-m}, then r_m = r_{m-1} u_m
-  auto fwd = [&](int m, uint32_t word) {
-    const double* pu = ptr_u(word);
-    C g = P::mul(r, ld(pu + a.E * 2 * L));
-    if (m < K) g = P::mul(g, s[K - m]);
+  auto ld = [&](int e) -> C {
+    if constexpr (LAYOUT == 2) return cls_load<L>(reinterpret_cast<const double2*>(pt), NE, e, cls);
+    else if constexpr (LAYOUT == 1) return sload<L>(pt + (size_t)e * 2 * L);
+    else return cload<L>(pt + (size_t)e * 2 * L);
+  };
+  auto word_at = [&](int j) { return __ldg(fw + (j - 1) * kWarp); };  // factor j, 1-based
+  // accumulate contribution g of factor word into the warp's row (all lanes in step)
+  auto rmw = [&](uint32_t word, const C& g) {
     const uint32_t v = word & 0xffffu;
     if (v != kDummyVar) {
-      double* acc = rows + ((size_t)(word >> 24) * a.n_var + v) * 2 * L;
-      sstore<L>(acc, P::add(sload<L>(acc), g));
+      if constexpr (LAYOUT == 2) {
+        double2* rw = reinterpret_cast<double2*>(rows);
+        cls_store<L>(rw, a.n_var, (int)v, cls, P::add_lazy(cls_load<L>(rw, a.n_var, (int)v, cls), g));
+      } else {
+        double* acc = rows + ((size_t)(word >> 24) * a.n_var + v) * 2 * L;
+        sstore<L>(acc, P::add_lazy(sload<L>(acc), g));
+      }
     }
     __syncwarp();
-    r = P::mul(r, ld(pu));
+  };
+  C Pk[H];  // P_0 .. P_{H-1}
+  C Sk[H];  // S_1 .. S_{H-1} at Sk[1..H-1]
+  C p = cload<L>(a.coef + ((size_t)b * kWarp + lane) * 2 * L);  // running P
+  C q;                                                           // running S
+  // phase 1
+  auto phase1 = [&](int t) {
+    Pk[t - 1] = p;
+    p = P::mul_lazy(p, ld(entry(word_at(t))));
+    const C u = ld(entry(word_at(K - t + 1)));
+    if (t == 1) {
+      q = u;
+    } else {
+      Sk[t - 1] = q;
+      q = P::mul_lazy(q, u);
+    }
+  };
+  // phase 2
+  auto phase2 = [&](int t) {
+    const uint32_t wa = word_at(H + t), wb = word_at(H - t + 1);
+    const int ea = entry(wa), eb = entry(wb);
+    C ga = P::mul_lazy(p, ld(ea + a.E));
+    if (t < H) ga = P::mul_lazy(ga, Sk[H - t]);
+    C gb = P::mul_lazy(Pk[H - t], ld(eb + a.E));
+    gb = P::mul_lazy(gb, q);
+    p = P::mul_lazy(p, ld(ea));
+    if (t < H) q = P::mul_lazy(q, ld(eb));
+    rmw(wa, ga);
+    rmw(wb, gb);
   };
   if constexpr (L == 2) {
-    uint32_t w[K];
 #pragma unroll
-    for (int q = 0; q < K; ++q) w[q] = __ldg(fw + q * kWarp);
-    s[1] = ld(ptr_u(w[K - 1]));
+    for (int t = 1; t <= H; ++t) phase1(t);
 #pragma unroll
-    for (int q = 2; q <= K - 1; ++q) s[q] = P::mul(s[q - 1], ld(ptr_u(w[K - q])));
-#pragma unroll
-    for (int m = 1; m <= K; ++m) fwd(m, w[m - 1]);
+    for (int t = 1; t <= H; ++t) phase2(t);
   } else {
-    s[1] = ld(ptr_u(__ldg(fw + (K - 1) * kWarp)));
 #pragma unroll 1
-    for (int q = 2; q <= K - 1; ++q) s[q] = P::mul(s[q - 1], ld(ptr_u(__ldg(fw + (K - q) * kWarp))));
+    for (int t = 1; t <= H; ++t) phase1(t);
 #pragma unroll 1
-    for (int m = 1; m <= K; ++m) fwd(m, __ldg(fw + (m - 1) * kWarp));
+    for (int t = 1; t <= H; ++t) phase2(t);
   }
-  return warp_sum<L>(r);
+  return warp_sum<L>(P::norm(p));
 }
 
-template <int L, int K, bool PT_SMEM>
+// Number of doubles of one warp's row accumulators.
+PHC_DEV size_t row_doubles(int layout, int R, int n_var, int L) {
+  return layout == 2 ? (size_t)kClasses * n_var * 2 * L : (size_t)R * n_var * 2 * L;
+}
+
+// Sum of warp w's accumulators for variable v (replicas r = 0..R-1 or classes c = 0..7, in order).
+template <int L, int LAYOUT>
+PHC_DEV typename Prec<L>::C row_total(const double* rows, int R, int n_var, int v) {
+  using P = Prec<L>;
+  typename P::C acc;
+  if constexpr (LAYOUT == 2) {
+    // classes are visited in the order v, v+1, ... (mod 8): a fixed order per variable that
+    // keeps the 8 lanes of a quarter-warp on 8 different banks
+    const double2* rw = reinterpret_cast<const double2*>(rows);
+    acc = P::norm(cls_load<L>(rw, n_var, v, v & (kClasses - 1)));
+    for (int c = 1; c < kClasses; ++c)
+      acc = P::add(acc, P::norm(cls_load<L>(rw, n_var, v, (v + c) & (kClasses - 1))));
+  } else {
+    acc = P::norm(sload<L>(rows + (size_t)v * 2 * L));
+    for (int r = 1; r < R; ++r) acc = P::add(acc, P::norm(sload<L>(rows + ((size_t)r * n_var + v) * 2 * L)));
+  }
+  return acc;
+}
+
+template <int L, int K, int LAYOUT>
 __global__ void __launch_bounds__(kBlockWarps * kWarp, (L == 2 ? PHC_DD_MINB : 1))
 block_kernel(const BlockArgs a) {
   using P = Prec<L>;
@@ -246,21 +360,39 @@ block_kernel(const BlockArgs a) {
 
   double* pt;
   double* rows_all;
-  if constexpr (PT_SMEM) {
-    pt = smem;
-    rows_all = smem + (size_t)(a.n_var + 1) * twoE * cd;
-    for (int v = threadIdx.x; v <= a.n_var; v += blockDim.x) {
-      double* row = pt + (size_t)v * twoE * cd;
-      if (v == a.n_var)
-        dummy_row<L>(a.E, row, true);
-      else
-        power_row<L>(cload<L>(a.X + (p * a.n_var + v) * cd), a.E, row, true);
-    }
-  } else {
+  if constexpr (LAYOUT == 0) {
     pt = const_cast<double*>(a.PTg) + p * (int64_t)(a.n_var + 1) * twoE * cd;
     rows_all = smem;
+  } else {
+    pt = smem;
+    const int NE = (a.n_var + 1) * twoE;
+    rows_all = smem + (size_t)NE * cd * (LAYOUT == 2 ? kClasses : 1);
+    for (int v = threadIdx.x; v <= a.n_var; v += blockDim.x) {
+      if constexpr (LAYOUT == 1) {
+        double* row = pt + (size_t)v * twoE * cd;
+        if (v == a.n_var)
+          dummy_row<L>(a.E, row, true);
+        else
+          power_row<L>(cload<L>(a.X + (p * a.n_var + v) * cd), a.E, row, true);
+      } else {
+        // compute the row once, store it in all 8 class copies
+        double2* pt2 = reinterpret_cast<double2*>(pt);
+        C pw = P::one();
+        const C x = (v == a.n_var) ? P::one() : cload<L>(a.X + (p * a.n_var + v) * cd);
+        for (int e = 1; e <= a.E; ++e) {
+          C dd = (e == 1) ? pw : P::mul_int(pw, (double)e);
+          pw = (e == 1) ? x : P::mul(pw, x);
+          if (v == a.n_var) { dd = P::zero(); pw = P::one(); }
+          for (int c0 = 0; c0 < kClasses; ++c0) {
+            const int c = (c0 + v) & (kClasses - 1);  // rotated: conflict-free stores
+            cls_store<L>(pt2, NE, v * twoE + e - 1, c, pw);
+            cls_store<L>(pt2, NE, v * twoE + a.E + e - 1, c, dd);
+          }
+        }
+      }
+    }
   }
-  const size_t row_elems = (size_t)a.R * a.n_var * cd;
+  const size_t row_elems = row_doubles(LAYOUT, a.R, a.n_var, L);
   double* rows = rows_all + warp * row_elems;
   double* fpart = rows_all + kBlockWarps * row_elems;  // mode B: per-warp F partials
   __syncthreads();
@@ -273,17 +405,13 @@ block_kernel(const BlockArgs a) {
       __syncwarp();
       C fsum = P::zero();
       for (int b = a.blk[i]; b < a.blk[i + 1]; ++b) {
-        C y = do_block<L, K, PT_SMEM>(a, b, pt, rows, lane);
+        C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane);
         fsum = P::add(fsum, y);
       }
       __syncwarp();
       if (lane == 0) cstore<L>(a.F + (p * a.n_eq + i) * cd, fsum);
       double* jrow = a.J + (p * a.n_eq + i) * (int64_t)a.n_var * cd;
-      for (int v = lane; v < a.n_var; v += kWarp) {
-        C acc = sload<L>(rows + (size_t)v * cd);
-        for (int r = 1; r < a.R; ++r) acc = P::add(acc, sload<L>(rows + ((size_t)r * a.n_var + v) * cd));
-        cstore<L>(jrow + (size_t)v * cd, acc);
-      }
+      for (int v = lane; v < a.n_var; v += kWarp) cstore<L>(jrow + (size_t)v * cd, row_total<L, LAYOUT>(rows, a.R, a.n_var, v));
       __syncwarp();
     }
   } else {
@@ -292,7 +420,7 @@ block_kernel(const BlockArgs a) {
     __syncwarp();
     C fsum = P::zero();
     for (int b = a.blk[i] + warp; b < a.blk[i + 1]; b += kBlockWarps) {
-      C y = do_block<L, K, PT_SMEM>(a, b, pt, rows, lane);
+      C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane);
       fsum = P::add(fsum, y);
     }
     if (lane == 0) sstore<L>(fpart + warp * cd, fsum);
@@ -304,10 +432,9 @@ block_kernel(const BlockArgs a) {
     }
     double* jrow = a.J + (p * a.n_eq + i) * (int64_t)a.n_var * cd;
     for (int v = threadIdx.x; v < a.n_var; v += blockDim.x) {
-      C acc = sload<L>(rows_all + (size_t)v * cd);
-      for (int w2 = 0; w2 < kBlockWarps; ++w2)
-        for (int r = (w2 == 0 ? 1 : 0); r < a.R; ++r)
-          acc = P::add(acc, sload<L>(rows_all + w2 * row_elems + ((size_t)r * a.n_var + v) * cd));
+      C acc = row_total<L, LAYOUT>(rows_all, a.R, a.n_var, v);
+      for (int w2 = 1; w2 < kBlockWarps; ++w2)
+        acc = P::add(acc, row_total<L, LAYOUT>(rows_all + w2 * row_elems, a.R, a.n_var, v));
       cstore<L>(jrow + (size_t)v * cd, acc);
     }
   }
@@ -402,10 +529,15 @@ inline bool colour_block(const std::vector<std::vector<std::pair<int, int>>>& te
 template <class S>
 void plan_blocks(const S& s, HostBlockPlan* plan) {
   plan->usable = false;
-  const int K = compiled_K(std::max(s.kmax, 1));
-  if (K == 0 || s.n_var >= (int)kDummyVar) return;
   const int L = s.L;
   const int E = s.E;
+  const size_t cdb = (size_t)2 * L * sizeof(double);
+  // layout 2 (class-interleaved, DD only) when it fits in shared memory
+  const size_t pt1 = (size_t)(s.n_var + 1) * 2 * E * cdb;
+  const size_t l2_bytes = pt1 * kClasses + (size_t)kBlockWarps * kClasses * s.n_var * cdb + kBlockWarps * cdb;
+  const int layout = (L == 2 && l2_bytes <= (size_t)200 * 1024) ? 2 : 1;
+  const int K = compiled_K(std::max(s.kmax, layout == 2 ? 4 : 1));
+  if (K == 0 || s.n_var >= (int)kDummyVar) return;
   // blocks
   std::vector<int32_t> blk(1, 0);
   std::vector<std::vector<int64_t>> bterms;
@@ -424,6 +556,7 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
   // replicas needed: max over blocks and variables of ceil(d_v / K)
   int R = 1;
   for (auto& ts : bterms) {
+    if (layout == 2) break;  // classes of 4 lanes: every (class, var) degree <= 4 <= K
     std::vector<int> d(s.n_var, 0);
     for (int64_t t : ts)
       for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q) d[s.fac[q] & 0xffffu]++;
@@ -441,7 +574,15 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       terms.push_back(f);
     }
     std::vector<std::vector<int>> slot, rep;
-    if (!colour_block(terms, s.n_var, K, R, &slot, &rep)) return;
+    if (layout == 2) {
+      // right nodes are (class, var): lanes of different classes never share an accumulator
+      auto cterms = terms;
+      for (size_t l = 0; l < cterms.size(); ++l)
+        for (auto& f : cterms[l]) f.first += s.n_var * (int)(l % kClasses);
+      if (!colour_block(cterms, s.n_var * kClasses, K, 1, &slot, &rep)) return;
+    } else if (!colour_block(terms, s.n_var, K, R, &slot, &rep)) {
+      return;
+    }
     for (int l = 0; l < kWarp; ++l) {
       for (int q = 0; q < K; ++q) fac[((size_t)b * K + q) * kWarp + l] = kDummyVar | (1u << 16);
       if (l >= (int)terms.size()) continue;
@@ -454,12 +595,15 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
     }
   }
-  const size_t cdb = (size_t)2 * L * sizeof(double);
-  const size_t pt_bytes = (size_t)(s.n_var + 1) * 2 * E * cdb;
-  const size_t rows_bytes = (size_t)kBlockWarps * R * s.n_var * cdb + kBlockWarps * cdb;
-  plan->pt_smem = pt_bytes + rows_bytes <= (size_t)160 * 1024;
-  plan->smem_bytes = (plan->pt_smem ? pt_bytes : 0) + rows_bytes;
-  if (plan->smem_bytes > (size_t)200 * 1024) return;
+  if (layout == 2) {
+    plan->layout = 2;
+    plan->smem_bytes = l2_bytes;
+  } else {
+    const size_t rows_bytes = (size_t)kBlockWarps * R * s.n_var * cdb + kBlockWarps * cdb;
+    plan->layout = pt1 + rows_bytes <= (size_t)160 * 1024 ? 1 : 0;
+    plan->smem_bytes = (plan->layout == 1 ? pt1 : 0) + rows_bytes;
+    if (plan->smem_bytes > (size_t)200 * 1024) return;
+  }
   plan->mode = max_blocks_per_poly >= 4 ? 1 : 0;
   plan->polys_per_cta = plan->mode == 0 ? std::min(s.n_eq, 4 * kBlockWarps) : 1;
   plan->K = K;
@@ -476,8 +620,22 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
     if (k >= 1) cm += 4 * k - 3;
   }
   plan->cm_per_point = cm;
-  plan->ca_per_point = s.n_factors + s.n_terms + (int64_t)s.n_eq * s.n_var * (R - 1);
-  plan->launches = plan->pt_smem ? 1 : 2;
+  plan->ca_per_point = s.n_factors + s.n_terms +
+                       (int64_t)s.n_eq * s.n_var * (plan->layout == 2 ? kClasses - 1 : R - 1);
+  plan->launches = plan->layout == 0 ? 2 : 1;
+  {
+    const OpFlops f = op_flops(L);
+    int64_t fl = (int64_t)s.n_var * std::max(0, E - 1) * (f.cm + f.ci);  // power table
+    for (int64_t t = 0; t < s.n_terms; ++t) {
+      const int64_t k = s.term_ptr[t + 1] - s.term_ptr[t];
+      if (k >= 1) fl += (4 * k - 3) * f.cm_lazy + k * f.ca_lazy;
+    }
+    fl += nb * kWarp * (f.norm + 5 * f.ca);  // warp shuffle tree of each block's term values
+    const int parts = plan->layout == 2 ? kClasses : R;
+    fl += (int64_t)s.n_eq * s.n_var * (parts * f.norm + (parts - 1) * f.ca);  // row totals
+    fl += (int64_t)(nb - s.n_eq) * f.ca;  // block sums of F
+    plan->exec_flops_per_point = fl;
+  }
   plan->usable = true;
 }
 
@@ -491,9 +649,9 @@ inline int upload_block_tables(const HostBlockPlan& plan, BlockTables* bt) {
   return 0;
 }
 
-template <int L, int K, bool PTS>
+template <int L, int K, int LAYOUT>
 int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_points, cudaStream_t st) {
-  auto kern = block_kernel<L, K, PTS>;
+  auto kern = block_kernel<L, K, LAYOUT>;
   if (plan.smem_bytes > 48 * 1024)
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes) != cudaSuccess)
       return -3;
@@ -505,7 +663,7 @@ int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_poin
     b.X = a.X + p0 * a.n_var * 2 * L;
     b.F = a.F + p0 * a.n_eq * 2 * L;
     b.J = a.J + p0 * (int64_t)a.n_eq * a.n_var * 2 * L;
-    if (!PTS) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
+    if (LAYOUT == 0) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
     b.n_points = np;
     kern<<<(unsigned)(np * units), kBlockWarps * kWarp, plan.smem_bytes, st>>>(b);
     if (cudaGetLastError() != cudaSuccess) return -3;
@@ -520,24 +678,25 @@ int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_poin
 #ifndef PHC_INSTANTIATE_BLOCK
 #define PHC_EXTERN_K(L, K, P) \
   extern template int launch_block_k<L, K, P>(const HostBlockPlan&, const BlockArgs&, int64_t, cudaStream_t);
-PHC_FOR_EACH_K(PHC_EXTERN_K, 2, true)
-PHC_FOR_EACH_K(PHC_EXTERN_K, 2, false)
-PHC_FOR_EACH_K(PHC_EXTERN_K, 4, true)
-PHC_FOR_EACH_K(PHC_EXTERN_K, 4, false)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 2, 0)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 2, 1)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 2, 2)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 4, 0)
+PHC_FOR_EACH_K(PHC_EXTERN_K, 4, 1)
 #undef PHC_EXTERN_K
 #endif
 
-template <int L, bool PTS>
+template <int L, int LAYOUT>
 int launch_block_pts(const HostBlockPlan& plan, const BlockArgs& a, int64_t np, cudaStream_t st) {
   switch (plan.K) {
-    case 2: return launch_block_k<L, 2, PTS>(plan, a, np, st);
-    case 4: return launch_block_k<L, 4, PTS>(plan, a, np, st);
-    case 8: return launch_block_k<L, 8, PTS>(plan, a, np, st);
-    case 12: return launch_block_k<L, 12, PTS>(plan, a, np, st);
-    case 16: return launch_block_k<L, 16, PTS>(plan, a, np, st);
-    case 20: return launch_block_k<L, 20, PTS>(plan, a, np, st);
-    case 24: return launch_block_k<L, 24, PTS>(plan, a, np, st);
-    case 32: return launch_block_k<L, 32, PTS>(plan, a, np, st);
+    case 2: return launch_block_k<L, 2, LAYOUT>(plan, a, np, st);
+    case 4: return launch_block_k<L, 4, LAYOUT>(plan, a, np, st);
+    case 8: return launch_block_k<L, 8, LAYOUT>(plan, a, np, st);
+    case 12: return launch_block_k<L, 12, LAYOUT>(plan, a, np, st);
+    case 16: return launch_block_k<L, 16, LAYOUT>(plan, a, np, st);
+    case 20: return launch_block_k<L, 20, LAYOUT>(plan, a, np, st);
+    case 24: return launch_block_k<L, 24, LAYOUT>(plan, a, np, st);
+    case 32: return launch_block_k<L, 32, LAYOUT>(plan, a, np, st);
   }
   return -4;
 }
@@ -564,7 +723,11 @@ int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, i
   // owns whole polynomials), so the grouping is chosen per call: one polynomial per warp
   // for few points (latency), up to 32 per CTA for batches (amortises the power table).
   a.polys_per_cta = plan.mode == 0 ? (n_points >= 4 * 148 ? std::min(n_eq, 4 * kBlockWarps) : std::min(n_eq, kBlockWarps)) : 1;
-  if (plan.pt_smem) return launch_block_pts<L, true>(plan, a, n_points, st);
+  if (plan.layout == 2) {
+    if constexpr (L == 2) return launch_block_pts<L, 2>(plan, a, n_points, st);
+    return -4;
+  }
+  if (plan.layout == 1) return launch_block_pts<L, 1>(plan, a, n_points, st);
   // global power table, in chunks of points that fit a 512 MiB scratch
   const int64_t per_point = (int64_t)(n_var + 1) * 2 * plan.E * 2 * L;
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)64 << 20) / per_point));
@@ -586,7 +749,7 @@ int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, i
     b.J = jac + p0 * (int64_t)n_eq * n_var * 2 * L;
     b.PTg = bt.PT;
     b.n_points = np;
-    int rc = launch_block_pts<L, false>(plan, b, np, st);
+    int rc = launch_block_pts<L, 0>(plan, b, np, st);
     if (rc) return rc;
   }
   return 0;

@@ -558,7 +558,7 @@ int phc_profile_read(const phc_system* cs, double ms[4], int64_t launches[4], in
   return PHC_OK;
 }
 
-int phc_system_stats(const phc_system* s, int64_t out[8]) {
+int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
   if (!s || !out) return fail(PHC_EINVAL, "NULL argument");
   out[0] = s->n_terms;
   out[1] = s->n_factors;
@@ -568,6 +568,15 @@ int phc_system_stats(const phc_system* s, int64_t out[8]) {
   out[5] = s->plan.usable ? s->plan.cm_per_point : s->cm_per_point;
   out[6] = s->ca_per_point;
   out[7] = s->plan.usable ? s->plan.launches : 3;
+  if (s->plan.usable) {
+    out[8] = s->plan.exec_flops_per_point;
+  } else {
+    const phc::OpFlops f = phc::op_flops(s->L);
+    out[8] = s->cm_per_point * f.cm + s->ca_per_point * f.ca + (int64_t)s->n_var * std::max(0, s->E - 1) * f.ci;
+  }
+  out[9] = s->plan.usable ? 1 : 0;
+  out[10] = s->plan.usable ? s->plan.layout : -1;
+  out[11] = s->plan.usable ? s->plan.K : s->kmax;
   return PHC_OK;
 }
 
