@@ -80,7 +80,7 @@ struct HostBlockPlan {
 struct OpFlops { int cm, cm_lazy, ca, ca_lazy, norm, ci; };
 inline OpFlops op_flops(int L) {
   if (L == 2) return {50, 44, 22, 16, 12, 16};
-  return {714, 714, 182, 182, 0, 130};
+  return {480, 480, 183, 183, 0, 130};
 }
 
 struct BlockArgs {
@@ -293,12 +293,12 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
     }
   };
   // phase 2
-  auto phase2 = [&](int t) {
+  auto phase2 = [&](int t, const C& pk, const C& sk) {  // pk = P_{H-t}, sk = S_{H-t}
     const uint32_t wa = word_at(H + t), wb = word_at(H - t + 1);
     const int ea = entry(wa), eb = entry(wb);
     C ga = P::mul_lazy(p, ld(ea + a.E));
-    if (t < H) ga = P::mul_lazy(ga, Sk[H - t]);
-    C gb = P::mul_lazy(Pk[H - t], ld(eb + a.E));
+    if (t < H) ga = P::mul_lazy(ga, sk);
+    C gb = P::mul_lazy(pk, ld(eb + a.E));
     gb = P::mul_lazy(gb, q);
     p = P::mul_lazy(p, ld(ea));
     if (t < H) q = P::mul_lazy(q, ld(eb));
@@ -309,12 +309,21 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
 #pragma unroll
     for (int t = 1; t <= H; ++t) phase1(t);
 #pragma unroll
-    for (int t = 1; t <= H; ++t) phase2(t);
+    for (int t = 1; t <= H; ++t) phase2(t, Pk[H - t], t < H ? Sk[H - t] : P::one());
   } else {
 #pragma unroll 1
     for (int t = 1; t <= H; ++t) phase1(t);
+    // the kept values live in local memory here: fetch them one step ahead
+    C pk_n = Pk[H - 1], sk_n = (H > 1) ? Sk[H - 1] : P::one();
 #pragma unroll 1
-    for (int t = 1; t <= H; ++t) phase2(t);
+    for (int t = 1; t <= H; ++t) {
+      const C pk = pk_n, sk = sk_n;
+      if (t < H) {
+        pk_n = Pk[H - t - 1];
+        sk_n = (t + 1 < H) ? Sk[H - t - 1] : P::one();
+      }
+      phase2(t, pk, sk);
+    }
   }
   return warp_sum<L>(P::norm(p));
 }
@@ -397,45 +406,44 @@ block_kernel(const BlockArgs a) {
   double* fpart = rows_all + kBlockWarps * row_elems;  // mode B: per-warp F partials
   __syncthreads();
 
-  if (a.mode == 0) {
-    const int i0 = unit * a.polys_per_cta;
-    const int i1 = min(a.n_eq, i0 + a.polys_per_cta);
-    for (int i = i0 + warp; i < i1; i += kBlockWarps) {
-      for (size_t e = lane; e < row_elems; e += kWarp) rows[e] = 0.0;
-      __syncwarp();
-      C fsum = P::zero();
-      for (int b = a.blk[i]; b < a.blk[i + 1]; ++b) {
-        C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane);
-        fsum = P::add(fsum, y);
-      }
-      __syncwarp();
-      if (lane == 0) cstore<L>(a.F + (p * a.n_eq + i) * cd, fsum);
-      double* jrow = a.J + (p * a.n_eq + i) * (int64_t)a.n_var * cd;
-      for (int v = lane; v < a.n_var; v += kWarp) cstore<L>(jrow + (size_t)v * cd, row_total<L, LAYOUT>(rows, a.R, a.n_var, v));
-      __syncwarp();
-    }
-  } else {
-    const int i = unit;
+  // One loop for both modes, with a single call site of do_block (the QD instance is
+  // thousands of instructions; two call sites would double the kernel's code footprint).
+  //  mode A: warp w takes polynomials i0+w, i0+w+NW, ... and all their blocks;
+  //  mode B: every warp takes polynomial `unit`, blocks blk[i]+w, blk[i]+w+NW, ...
+  const bool mA = (a.mode == 0);
+  const int i_first = mA ? unit * a.polys_per_cta + warp : unit;
+  const int i_end = mA ? min(a.n_eq, (unit + 1) * a.polys_per_cta) : unit + 1;
+  const int i_step = mA ? kBlockWarps : 1;
+  for (int i = i_first; i < i_end; i += i_step) {
     for (size_t e = lane; e < row_elems; e += kWarp) rows[e] = 0.0;
     __syncwarp();
     C fsum = P::zero();
-    for (int b = a.blk[i] + warp; b < a.blk[i + 1]; b += kBlockWarps) {
+    const int b_step = mA ? 1 : kBlockWarps;
+    for (int b = a.blk[i] + (mA ? 0 : warp); b < a.blk[i + 1]; b += b_step) {
       C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane);
       fsum = P::add(fsum, y);
     }
-    if (lane == 0) sstore<L>(fpart + warp * cd, fsum);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      C f = sload<L>(fpart);
-      for (int w2 = 1; w2 < kBlockWarps; ++w2) f = P::add(f, sload<L>(fpart + w2 * cd));
-      cstore<L>(a.F + (p * a.n_eq + i) * cd, f);
-    }
+    __syncwarp();
     double* jrow = a.J + (p * a.n_eq + i) * (int64_t)a.n_var * cd;
-    for (int v = threadIdx.x; v < a.n_var; v += blockDim.x) {
-      C acc = row_total<L, LAYOUT>(rows_all, a.R, a.n_var, v);
-      for (int w2 = 1; w2 < kBlockWarps; ++w2)
-        acc = P::add(acc, row_total<L, LAYOUT>(rows_all + w2 * row_elems, a.R, a.n_var, v));
-      cstore<L>(jrow + (size_t)v * cd, acc);
+    if (mA) {
+      if (lane == 0) cstore<L>(a.F + (p * a.n_eq + i) * cd, fsum);
+      for (int v = lane; v < a.n_var; v += kWarp)
+        cstore<L>(jrow + (size_t)v * cd, row_total<L, LAYOUT>(rows, a.R, a.n_var, v));
+      __syncwarp();
+    } else {
+      if (lane == 0) sstore<L>(fpart + warp * cd, fsum);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        C f = sload<L>(fpart);
+        for (int w2 = 1; w2 < kBlockWarps; ++w2) f = P::add(f, sload<L>(fpart + w2 * cd));
+        cstore<L>(a.F + (p * a.n_eq + i) * cd, f);
+      }
+      for (int v = threadIdx.x; v < a.n_var; v += blockDim.x) {
+        C acc = row_total<L, LAYOUT>(rows_all, a.R, a.n_var, v);
+        for (int w2 = 1; w2 < kBlockWarps; ++w2)
+          acc = P::add(acc, row_total<L, LAYOUT>(rows_all + w2 * row_elems, a.R, a.n_var, v));
+        cstore<L>(jrow + (size_t)v * cd, acc);
+      }
     }
   }
 }
