@@ -53,6 +53,27 @@ def dist_env():
     return rank, world, local
 
 
+def rank_seed(rank):
+    """Weak scaling: every rank evaluates its own batch of the workload, drawn with seed 1 + rank."""
+    return 1 + rank
+
+
+def max_over_ranks(value, world, device=None):
+    """The timing rule: the slowest rank defines the step time (all_reduce MAX)."""
+    if world <= 1:
+        return float(value)
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def aggregate_value(world, points_per_rank, steps, ms_max):
+    """Whole-job throughput: the units all ranks processed / the max-over-ranks time."""
+    return world * points_per_rank * steps / (ms_max * 1e-3)
+
+
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -214,7 +235,7 @@ def main():
     dev = torch.device("cuda", local)
     c = CONFIGS[args.workload]
     P = args.points or c["points"]
-    s, X = config_system(args.workload, seed=1 + rank, points=P)
+    s, X = config_system(args.workload, seed=rank_seed(rank), points=P)
     h = phc.System(s, device=local)
     st = h.stats
     Xd = torch.from_numpy(X).to(dev)
@@ -250,10 +271,7 @@ def main():
     ms = sum(a.elapsed_time(b) for a, b in ev)
     kms, kn = phc.phc_profile_read(h._h, reset=True)
     phc.phc_profile_enable(h._h, False)
-    if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, dev)
     clocks = clk.summary()
 
     # end to end through the C-ABI host call: pinned host buffers, H2D + eval + D2H every step
@@ -267,10 +285,7 @@ def main():
     for _ in range(args.e2e_steps):
         h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy())
     e2e_s = time.perf_counter() - t0
-    if world > 1:
-        t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s, world, dev)
     ok = bool(torch.isfinite(F).all().item()) and bool(torch.isfinite(J).all().item())
 
     if rank == 0:
@@ -278,7 +293,7 @@ def main():
         mf = MODEL_FLOPS[s.limbs]
         model_flops_pp = cm_model * mf["cm"] + ca_model * mf["ca"]
         exec_pp = exec_flops_per_point(s, st)
-        value = world * P * args.steps / (ms * 1e-3)
+        value = aggregate_value(world, P, args.steps, ms)
         peak = peak_now
         # dominant kernel (largest summed time among the classes)
         names = ["power_table", "term", "reduce", "fused_block"]
@@ -330,7 +345,7 @@ def main():
             "kernels_ms_per_step": {names[i]: kms[i] / args.steps for i in range(4) if kn[i]},
             "clocks": clocks,
             "e2e": {
-                "value": world * P * args.e2e_steps / e2e_s,
+                "value": aggregate_value(world, P, args.e2e_steps, e2e_s * 1e3),
                 "unit": "evals/s",
                 "h2d_bytes_per_step": bytes_in,
                 "d2h_bytes_per_step": bytes_out,

@@ -40,11 +40,16 @@
 namespace phc {
 
 constexpr int kWarp = 32;
-constexpr int kBlockWarps = 8;  // NW: warps per CTA
-constexpr uint32_t kDummyVar = 0xFFFFu;
-#ifndef PHC_DD_MINB
-#define PHC_DD_MINB 1  // CTAs per SM the DD block kernel is register-capped for
+// Warps per CTA (NW).  Layout 2 (DD, small n) runs 16 warps in one CTA per SM: the CTA
+// shares the 8-way replicated power table and the register file caps a thread at 128
+// registers; the other layouts run 8 warps.
+#ifndef PHC_DD_L2_WARPS
+#define PHC_DD_L2_WARPS 8
 #endif
+__host__ __device__ constexpr int block_warps(int L, int layout) {
+  return (L == 2 && layout == 2) ? PHC_DD_L2_WARPS : 8;
+}
+constexpr uint32_t kDummyVar = 0xFFFFu;
 
 struct BlockTables {
   uint32_t* fac = nullptr;
@@ -353,10 +358,11 @@ PHC_DEV typename Prec<L>::C row_total(const double* rows, int R, int n_var, int 
 }
 
 template <int L, int K, int LAYOUT>
-__global__ void __launch_bounds__(kBlockWarps * kWarp, (L == 2 ? PHC_DD_MINB : 1))
+__global__ void __launch_bounds__(block_warps(L, LAYOUT) * kWarp, 1)
 block_kernel(const BlockArgs a) {
   using P = Prec<L>;
   using C = typename P::C;
+  constexpr int kBlockWarps = block_warps(L, LAYOUT);
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cd = 2 * L;
@@ -542,7 +548,8 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
   const size_t cdb = (size_t)2 * L * sizeof(double);
   // layout 2 (class-interleaved, DD only) when it fits in shared memory
   const size_t pt1 = (size_t)(s.n_var + 1) * 2 * E * cdb;
-  const size_t l2_bytes = pt1 * kClasses + (size_t)kBlockWarps * kClasses * s.n_var * cdb + kBlockWarps * cdb;
+  const int nw2 = block_warps(L, 2);
+  const size_t l2_bytes = pt1 * kClasses + (size_t)nw2 * kClasses * s.n_var * cdb + nw2 * cdb;
   const int layout = (L == 2 && l2_bytes <= (size_t)200 * 1024) ? 2 : 1;
   const int K = compiled_K(std::max(s.kmax, layout == 2 ? 4 : 1));
   if (K == 0 || s.n_var >= (int)kDummyVar) return;
@@ -607,13 +614,14 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
     plan->layout = 2;
     plan->smem_bytes = l2_bytes;
   } else {
-    const size_t rows_bytes = (size_t)kBlockWarps * R * s.n_var * cdb + kBlockWarps * cdb;
+    const int nw = block_warps(L, 1);
+    const size_t rows_bytes = (size_t)nw * R * s.n_var * cdb + nw * cdb;
     plan->layout = pt1 + rows_bytes <= (size_t)160 * 1024 ? 1 : 0;
     plan->smem_bytes = (plan->layout == 1 ? pt1 : 0) + rows_bytes;
     if (plan->smem_bytes > (size_t)200 * 1024) return;
   }
   plan->mode = max_blocks_per_poly >= 4 ? 1 : 0;
-  plan->polys_per_cta = plan->mode == 0 ? std::min(s.n_eq, 4 * kBlockWarps) : 1;
+  plan->polys_per_cta = 1;
   plan->K = K;
   plan->R = R;
   plan->E = E;
@@ -673,7 +681,7 @@ int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_poin
     b.J = a.J + p0 * (int64_t)a.n_eq * a.n_var * 2 * L;
     if (LAYOUT == 0) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
     b.n_points = np;
-    kern<<<(unsigned)(np * units), kBlockWarps * kWarp, plan.smem_bytes, st>>>(b);
+    kern<<<(unsigned)(np * units), block_warps(L, LAYOUT) * kWarp, plan.smem_bytes, st>>>(b);
     if (cudaGetLastError() != cudaSuccess) return -3;
     p0 += np;
   }
@@ -730,7 +738,8 @@ int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, i
   // mode A: results do not depend on how polynomials are grouped into CTAs (each warp
   // owns whole polynomials), so the grouping is chosen per call: one polynomial per warp
   // for few points (latency), up to 32 per CTA for batches (amortises the power table).
-  a.polys_per_cta = plan.mode == 0 ? (n_points >= 4 * 148 ? std::min(n_eq, 4 * kBlockWarps) : std::min(n_eq, kBlockWarps)) : 1;
+  const int nw = block_warps(L, plan.layout);
+  a.polys_per_cta = plan.mode == 0 ? (n_points >= 4 * 148 ? std::min(n_eq, 4 * nw) : std::min(n_eq, nw)) : 1;
   if (plan.layout == 2) {
     if constexpr (L == 2) return launch_block_pts<L, 2>(plan, a, n_points, st);
     return -4;
