@@ -140,12 +140,13 @@ PHC_DEV typename Prec<L>::C shfl_down(const typename Prec<L>::C& v, int d) {
   }
   return r;
 }
-// lane 0 receives the sum over the warp in a fixed tree order
+// lane 0 receives the sum over the warp in a fixed tree order (lazy adds, one final
+// renormalisation)
 template <int L>
 PHC_DEV typename Prec<L>::C warp_sum(typename Prec<L>::C v) {
 #pragma unroll
-  for (int d = 16; d >= 1; d >>= 1) v = Prec<L>::add(v, shfl_down<L>(v, d));
-  return v;
+  for (int d = 16; d >= 1; d >>= 1) v = Prec<L>::add_lazy(v, shfl_down<L>(v, d));
+  return Prec<L>::norm(v);
 }
 
 // Power-table row of variable v (row a2): U[a-1] = x^a, Dd[a-1] = a x^(a-1), a = 1..E.
@@ -338,7 +339,8 @@ PHC_DEV size_t row_doubles(int layout, int R, int n_var, int L) {
   return layout == 2 ? (size_t)kClasses * n_var * 2 * L : (size_t)R * n_var * 2 * L;
 }
 
-// Sum of warp w's accumulators for variable v (replicas r = 0..R-1 or classes c = 0..7, in order).
+// Sum of a warp's accumulators for variable v (replicas r = 0..R-1 or classes, in a fixed
+// order); lazy adds, NOT renormalised (the caller renormalises once).
 template <int L, int LAYOUT>
 PHC_DEV typename Prec<L>::C row_total(const double* rows, int R, int n_var, int v) {
   using P = Prec<L>;
@@ -347,12 +349,11 @@ PHC_DEV typename Prec<L>::C row_total(const double* rows, int R, int n_var, int 
     // classes are visited in the order v, v+1, ... (mod 8): a fixed order per variable that
     // keeps the 8 lanes of a quarter-warp on 8 different banks
     const double2* rw = reinterpret_cast<const double2*>(rows);
-    acc = P::norm(cls_load<L>(rw, n_var, v, v & (kClasses - 1)));
-    for (int c = 1; c < kClasses; ++c)
-      acc = P::add(acc, P::norm(cls_load<L>(rw, n_var, v, (v + c) & (kClasses - 1))));
+    acc = cls_load<L>(rw, n_var, v, v & (kClasses - 1));
+    for (int c = 1; c < kClasses; ++c) acc = P::add_lazy(acc, cls_load<L>(rw, n_var, v, (v + c) & (kClasses - 1)));
   } else {
-    acc = P::norm(sload<L>(rows + (size_t)v * 2 * L));
-    for (int r = 1; r < R; ++r) acc = P::add(acc, P::norm(sload<L>(rows + ((size_t)r * n_var + v) * 2 * L)));
+    acc = sload<L>(rows + (size_t)v * 2 * L);
+    for (int r = 1; r < R; ++r) acc = P::add_lazy(acc, sload<L>(rows + ((size_t)r * n_var + v) * 2 * L));
   }
   return acc;
 }
@@ -382,27 +383,29 @@ block_kernel(const BlockArgs a) {
     pt = smem;
     const int NE = (a.n_var + 1) * twoE;
     rows_all = smem + (size_t)NE * cd * (LAYOUT == 2 ? kClasses : 1);
-    for (int v = threadIdx.x; v <= a.n_var; v += blockDim.x) {
-      if constexpr (LAYOUT == 1) {
+    if constexpr (LAYOUT == 1) {
+      for (int v = threadIdx.x; v <= a.n_var; v += blockDim.x) {
         double* row = pt + (size_t)v * twoE * cd;
         if (v == a.n_var)
           dummy_row<L>(a.E, row, true);
         else
           power_row<L>(cload<L>(a.X + (p * a.n_var + v) * cd), a.E, row, true);
-      } else {
-        // compute the row once, store it in all 8 class copies
-        double2* pt2 = reinterpret_cast<double2*>(pt);
+      }
+    } else {
+      // one thread per (variable, class): each computes the row (E-1 products; cheap)
+      // and stores its class copy; the 8 threads of a quarter-warp write 8 classes of the
+      // same entry, i.e. 8 different banks
+      double2* pt2 = reinterpret_cast<double2*>(pt);
+      for (int idx = threadIdx.x; idx < (a.n_var + 1) * kClasses; idx += blockDim.x) {
+        const int v = idx / kClasses, c = idx % kClasses;
         C pw = P::one();
         const C x = (v == a.n_var) ? P::one() : cload<L>(a.X + (p * a.n_var + v) * cd);
         for (int e = 1; e <= a.E; ++e) {
           C dd = (e == 1) ? pw : P::mul_int(pw, (double)e);
           pw = (e == 1) ? x : P::mul(pw, x);
-          if (v == a.n_var) { dd = P::zero(); pw = P::one(); }
-          for (int c0 = 0; c0 < kClasses; ++c0) {
-            const int c = (c0 + v) & (kClasses - 1);  // rotated: conflict-free stores
-            cls_store<L>(pt2, NE, v * twoE + e - 1, c, pw);
-            cls_store<L>(pt2, NE, v * twoE + a.E + e - 1, c, dd);
-          }
+          if (v == a.n_var) dd = P::zero();
+          cls_store<L>(pt2, NE, v * twoE + e - 1, c, pw);
+          cls_store<L>(pt2, NE, v * twoE + a.E + e - 1, c, dd);
         }
       }
     }
@@ -421,7 +424,7 @@ block_kernel(const BlockArgs a) {
   const int i_end = mA ? min(a.n_eq, (unit + 1) * a.polys_per_cta) : unit + 1;
   const int i_step = mA ? kBlockWarps : 1;
   for (int i = i_first; i < i_end; i += i_step) {
-    for (size_t e = lane; e < row_elems; e += kWarp) rows[e] = 0.0;
+    for (size_t e = lane; e < row_elems / 2; e += kWarp) reinterpret_cast<double2*>(rows)[e] = make_double2(0.0, 0.0);
     __syncwarp();
     C fsum = P::zero();
     const int b_step = mA ? 1 : kBlockWarps;
@@ -434,7 +437,7 @@ block_kernel(const BlockArgs a) {
     if (mA) {
       if (lane == 0) cstore<L>(a.F + (p * a.n_eq + i) * cd, fsum);
       for (int v = lane; v < a.n_var; v += kWarp)
-        cstore<L>(jrow + (size_t)v * cd, row_total<L, LAYOUT>(rows, a.R, a.n_var, v));
+        cstore<L>(jrow + (size_t)v * cd, P::norm(row_total<L, LAYOUT>(rows, a.R, a.n_var, v)));
       __syncwarp();
     } else {
       if (lane == 0) sstore<L>(fpart + warp * cd, fsum);
@@ -447,8 +450,8 @@ block_kernel(const BlockArgs a) {
       for (int v = threadIdx.x; v < a.n_var; v += blockDim.x) {
         C acc = row_total<L, LAYOUT>(rows_all, a.R, a.n_var, v);
         for (int w2 = 1; w2 < kBlockWarps; ++w2)
-          acc = P::add(acc, row_total<L, LAYOUT>(rows_all + w2 * row_elems, a.R, a.n_var, v));
-        cstore<L>(jrow + (size_t)v * cd, acc);
+          acc = P::add_lazy(acc, row_total<L, LAYOUT>(rows_all + w2 * row_elems, a.R, a.n_var, v));
+        cstore<L>(jrow + (size_t)v * cd, P::norm(acc));
       }
     }
   }
@@ -646,9 +649,9 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       const int64_t k = s.term_ptr[t + 1] - s.term_ptr[t];
       if (k >= 1) fl += (4 * k - 3) * f.cm_lazy + k * f.ca_lazy;
     }
-    fl += nb * kWarp * (f.norm + 5 * f.ca);  // warp shuffle tree of each block's term values
+    fl += nb * kWarp * (2 * f.norm + 5 * f.ca_lazy);  // warp shuffle tree of each block's term values
     const int parts = plan->layout == 2 ? kClasses : R;
-    fl += (int64_t)s.n_eq * s.n_var * (parts * f.norm + (parts - 1) * f.ca);  // row totals
+    fl += (int64_t)s.n_eq * s.n_var * (f.norm + (parts - 1) * f.ca_lazy);  // row totals
     fl += (int64_t)(nb - s.n_eq) * f.ca;  // block sums of F
     plan->exec_flops_per_point = fl;
   }
