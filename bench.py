@@ -53,6 +53,15 @@ def dist_env():
     return rank, world, local
 
 
+def traffic_per_launch(workload, points):
+    """roofline.traffic: DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[workload]
+        return t["bytes_per_point"] * points
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def rank_seed(rank):
     """Weak scaling: every rank evaluates its own batch of the workload, drawn with seed 1 + rank."""
     return 1 + rank
@@ -329,7 +338,8 @@ def main():
                 "peak": peak,
                 "unit": "TFLOP/s",
                 "frac": achieved / peak if peak else None,
-                "traffic": None,
+                "traffic": traffic_per_launch(args.workload, P / max(kn[dom] / args.steps, 1)),
+                "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per point x points per launch)",
                 "flops": "executed FP64 flops (DADD=DMUL=1, DFMA=2) per launch from the kernel op counts",
                 "peak_source": "phc_fp64_peak: DFMA chains measured in this run (profiles/fp64_peak_r01.jsonl: 34.2 sustained)",
             },
