@@ -65,6 +65,7 @@ struct HostBlockPlan {
   int R = 1;           // replicas per row
   int E = 1;           // max exponent
   int mode = 0;        // 0 = A, 1 = B
+  int nw = 8;          // warps per CTA (mode B: min(8, blocks per polynomial)); fixed per system
   int polys_per_cta = 1;
   int layout = 1;      // see LAYOUT above
   int64_t n_blocks = 0;
@@ -363,7 +364,7 @@ __global__ void __launch_bounds__(block_warps(L, LAYOUT) * kWarp, 1)
 block_kernel(const BlockArgs a) {
   using P = Prec<L>;
   using C = typename P::C;
-  constexpr int kBlockWarps = block_warps(L, LAYOUT);
+  const int kBlockWarps = blockDim.x >> 5;  // the plan's warps per CTA
   extern __shared__ __align__(16) double smem[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int cd = 2 * L;
@@ -613,17 +614,20 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
     }
   }
+  // mode A (a warp owns whole polynomials) when every polynomial is one block; mode B (a CTA
+  // owns a polynomial, its warps split the blocks) otherwise, with one warp per block up to 8
+  plan->mode = max_blocks_per_poly >= 2 ? 1 : 0;
+  const int nw = plan->mode == 1 ? std::min(max_blocks_per_poly, 8) : block_warps(L, layout);
+  plan->nw = nw;
   if (layout == 2) {
     plan->layout = 2;
-    plan->smem_bytes = l2_bytes;
+    plan->smem_bytes = pt1 * kClasses + (size_t)nw * kClasses * s.n_var * cdb + nw * cdb;
   } else {
-    const int nw = block_warps(L, 1);
     const size_t rows_bytes = (size_t)nw * R * s.n_var * cdb + nw * cdb;
     plan->layout = pt1 + rows_bytes <= (size_t)160 * 1024 ? 1 : 0;
     plan->smem_bytes = (plan->layout == 1 ? pt1 : 0) + rows_bytes;
     if (plan->smem_bytes > (size_t)200 * 1024) return;
   }
-  plan->mode = max_blocks_per_poly >= 4 ? 1 : 0;
   plan->polys_per_cta = 1;
   plan->K = K;
   plan->R = R;
@@ -684,7 +688,7 @@ int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_poin
     b.J = a.J + p0 * (int64_t)a.n_eq * a.n_var * 2 * L;
     if (LAYOUT == 0) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
     b.n_points = np;
-    kern<<<(unsigned)(np * units), block_warps(L, LAYOUT) * kWarp, plan.smem_bytes, st>>>(b);
+    kern<<<(unsigned)(np * units), plan.nw * kWarp, plan.smem_bytes, st>>>(b);
     if (cudaGetLastError() != cudaSuccess) return -3;
     p0 += np;
   }
@@ -741,7 +745,7 @@ int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, i
   // mode A: results do not depend on how polynomials are grouped into CTAs (each warp
   // owns whole polynomials), so the grouping is chosen per call: one polynomial per warp
   // for few points (latency), up to 32 per CTA for batches (amortises the power table).
-  const int nw = block_warps(L, plan.layout);
+  const int nw = plan.nw;
   a.polys_per_cta = plan.mode == 0 ? (n_points >= 4 * 148 ? std::min(n_eq, 4 * nw) : std::min(n_eq, nw)) : 1;
   if (plan.layout == 2) {
     if constexpr (L == 2) return launch_block_pts<L, 2>(plan, a, n_points, st);
