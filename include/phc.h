@@ -101,6 +101,19 @@ int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double*
 int phc_eval_jacobian_batch_host(const phc_system* s, int64_t n_points, const double* x_host, double* f_host,
                                  double* jac_host, const int32_t* devices, int32_t n_devices);
 
+/* NEXT-1: one Newton iteration of Alg. 2 per point,
+ * for square systems (n_eq == n_var).  For each of the n_points points x_p:
+ *   F, J := the evaluation above at x_p
+ *   residual[p] := max_i |F_i| (binary64 from the leading limbs)  (reading N1)
+ *   solve J dz = -F by Gaussian elimination with partial pivoting (largest |.| in the column,
+ *     ties to the lowest row) and back substitution
+ *   x_new[p] := x_p + dz
+ *   status[p] := 0, or 1 when a pivot column is exactly zero (x_new[p] := x_p).
+ * x, x_new [n_points][n][2][L], residual [n_points] (double), status [n_points] (int32):
+ * device pointers on the home device; x_new may alias x.  Asynchronous on `stream`. */
+int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x, double* x_new, double* residual,
+                          int32_t* status, void* stream);
+
 /* Static facts about the system, as built: counts used by the benchmark's model.
  * out[0] = n_terms, out[1] = n_factors, out[2] = max k, out[3] = max exponent D,
  * out[4] = nnz(J) (structurally nonzero entries), out[5] = complex multiplies per point

@@ -17,3 +17,4 @@ from .naive import (  # noqa: F401
     derivative_monomial,
 )
 from .compare import rel_errors, exact_equal_limbs  # noqa: F401
+from .newton import newton_step, solve_exact  # noqa: F401

@@ -15,6 +15,7 @@ from ._lib import (  # noqa: F401
     phc_eval_jacobian_batch_host,
     phc_fp64_peak,
     phc_last_error,
+    phc_newton_step_batch,
     phc_profile_enable,
     phc_profile_read,
     phc_system_create,

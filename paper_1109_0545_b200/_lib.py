@@ -26,6 +26,7 @@ EXPORTED = (
     "phc_eval_jacobian",
     "phc_eval_jacobian_batch",
     "phc_eval_jacobian_batch_host",
+    "phc_newton_step_batch",
     "phc_system_stats",
     "phc_fp64_peak",
     "phc_profile_enable",
@@ -59,6 +60,8 @@ def _load():
     lib.phc_eval_jacobian_batch.restype = ctypes.c_int
     lib.phc_eval_jacobian_batch_host.argtypes = [P, i64, P, P, P, P, i32]
     lib.phc_eval_jacobian_batch_host.restype = ctypes.c_int
+    lib.phc_newton_step_batch.argtypes = [P, i64, P, P, P, P, P]
+    lib.phc_newton_step_batch.restype = ctypes.c_int
     lib.phc_system_stats.argtypes = [P, P]
     lib.phc_system_stats.restype = ctypes.c_int
     lib.phc_fp64_peak.argtypes = [i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
@@ -106,6 +109,10 @@ def phc_eval_jacobian_batch(h, n_points, x, f, jac, devices, n_devices, stream):
 
 def phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices):
     return check(lib.phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices))
+
+
+def phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream):
+    return check(lib.phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream))
 
 
 def phc_system_stats(h):

@@ -231,6 +231,41 @@ PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
 }
 
 // ---------------------------------------------------------------------------
+// division (NEXT-1 Newton step only: pivots and back substitution).  Long division
+// q_j = r_j / b_0 with exact-ish remainders (the QD-library scheme, restated).
+// ---------------------------------------------------------------------------
+PHC_DEV dd dd_sub(const dd& a, const dd& b) { return dd_add(a, dd_neg(b)); }
+PHC_DEV dd dd_mul_d(const dd& a, double b) {
+  double p, e;
+  two_prod(a.x[0], b, p, e);
+  e = fma_(a.x[1], b, e);
+  dd r;
+  quick_two_sum(p, e, r.x[0], r.x[1]);
+  return r;
+}
+PHC_DEV dd dd_div(const dd& a, const dd& b) {
+  const double q1 = __ddiv_rn(a.x[0], b.x[0]);
+  dd r = dd_sub(a, dd_mul_d(b, q1));
+  const double q2 = __ddiv_rn(r.x[0], b.x[0]);
+  r = dd_sub(r, dd_mul_d(b, q2));
+  const double q3 = __ddiv_rn(r.x[0], b.x[0]);
+  dd q;
+  quick_two_sum(q1, q2, q.x[0], q.x[1]);
+  return dd_add(q, dd_make(q3, 0.0));
+}
+PHC_DEV qd qd_from_d(double a) { qd r; r.x[0] = a; r.x[1] = r.x[2] = r.x[3] = 0.0; return r; }
+PHC_DEV qd qd_sub(const qd& a, const qd& b) { return qd_add(a, qd_neg(b)); }
+PHC_DEV qd qd_div(const qd& a, const qd& b) {
+  double q[5];
+  qd r = a;
+  for (int j = 0; j < 5; ++j) {
+    q[j] = __ddiv_rn(r.x[0], b.x[0]);
+    if (j < 4) r = qd_sub(r, qd_mul(b, qd_from_d(q[j])));
+  }
+  return renorm5(q[0], q[1], q[2], q[3], q[4]);
+}
+
+// ---------------------------------------------------------------------------
 // complex values, templated on the real type; Prec<L> traits below
 // ---------------------------------------------------------------------------
 template <class R>
@@ -343,6 +378,18 @@ template <> struct Prec<2> {
     return r;
   }
   PHC_DEV static C mul_int(const C& a, double s) { C r; r.re = mul_int_real(a.re, s); r.im = mul_int_real(a.im, s); return r; }
+  PHC_DEV static C neg(const C& a) { C r; r.re = dd_neg(a.re); r.im = dd_neg(a.im); return r; }
+  PHC_DEV static C sub(const C& a, const C& b) { return add(a, neg(b)); }
+  // 1 / a = conj(a) / |a|^2
+  PHC_DEV static C recip(const C& a) {
+    const dd d = dd_add(dd_mul(a.re, a.re), dd_mul(a.im, a.im));
+    C r;
+    r.re = dd_div(a.re, d);
+    r.im = dd_neg(dd_div(a.im, d));
+    return r;
+  }
+  // |a|^2 from the leading limbs (pivot selection only)
+  PHC_DEV static double abs2_hi(const C& a) { return a.re.x[0] * a.re.x[0] + a.im.x[0] * a.im.x[0]; }
 };
 
 template <> struct Prec<4> {
@@ -377,6 +424,16 @@ template <> struct Prec<4> {
     return renorm5(p0, s1, p2, s3, 0.0);
   }
   PHC_DEV static C mul_int(const C& a, double s) { C r; r.re = mul_int_real(a.re, s); r.im = mul_int_real(a.im, s); return r; }
+  PHC_DEV static C neg(const C& a) { C r; r.re = qd_neg(a.re); r.im = qd_neg(a.im); return r; }
+  PHC_DEV static C sub(const C& a, const C& b) { return add(a, neg(b)); }
+  PHC_DEV static C recip(const C& a) {
+    const qd d = qd_dot2(a.re, a.re, a.im, a.im);
+    C r;
+    r.re = qd_div(a.re, d);
+    r.im = qd_neg(qd_div(a.im, d));
+    return r;
+  }
+  PHC_DEV static double abs2_hi(const C& a) { return a.re.x[0] * a.re.x[0] + a.im.x[0] * a.im.x[0]; }
 };
 
 // ---------------------------------------------------------------------------
@@ -421,4 +478,33 @@ template <> PHC_DEV void cstore<4>(double* p, const cqd& v) {
   st4(p + 4, v.im.x[0], v.im.x[1], v.im.x[2], v.im.x[3]);
 }
 
+// 16-byte-vector complex access through a generic pointer (shared memory, or global memory
+// written by the same kernel): LDS.128/STS.128 or LD/ST.128.
+template <int L>
+PHC_DEV typename Prec<L>::C sload(const double* p) {
+  typename Prec<L>::C v;
+  const double2* q = reinterpret_cast<const double2*>(p);
+  if constexpr (L == 2) {
+    double2 a = q[0], b = q[1];
+    v.re.x[0] = a.x; v.re.x[1] = a.y; v.im.x[0] = b.x; v.im.x[1] = b.y;
+  } else {
+    double2 a = q[0], b = q[1], c = q[2], d = q[3];
+    v.re.x[0] = a.x; v.re.x[1] = a.y; v.re.x[2] = b.x; v.re.x[3] = b.y;
+    v.im.x[0] = c.x; v.im.x[1] = c.y; v.im.x[2] = d.x; v.im.x[3] = d.y;
+  }
+  return v;
+}
+template <int L>
+PHC_DEV void sstore(double* p, const typename Prec<L>::C& v) {
+  double2* q = reinterpret_cast<double2*>(p);
+  if constexpr (L == 2) {
+    q[0] = make_double2(v.re.x[0], v.re.x[1]);
+    q[1] = make_double2(v.im.x[0], v.im.x[1]);
+  } else {
+    q[0] = make_double2(v.re.x[0], v.re.x[1]);
+    q[1] = make_double2(v.re.x[2], v.re.x[3]);
+    q[2] = make_double2(v.im.x[0], v.im.x[1]);
+    q[3] = make_double2(v.im.x[2], v.im.x[3]);
+  }
+}
 }  // namespace phc

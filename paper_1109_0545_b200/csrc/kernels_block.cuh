@@ -105,33 +105,6 @@ struct BlockArgs {
 // device helpers: shared-memory complex access and warp shuffles
 // ---------------------------------------------------------------------------
 template <int L>
-PHC_DEV typename Prec<L>::C sload(const double* p) {
-  typename Prec<L>::C v;
-  const double2* q = reinterpret_cast<const double2*>(p);
-  if constexpr (L == 2) {
-    double2 a = q[0], b = q[1];
-    v.re.x[0] = a.x; v.re.x[1] = a.y; v.im.x[0] = b.x; v.im.x[1] = b.y;
-  } else {
-    double2 a = q[0], b = q[1], c = q[2], d = q[3];
-    v.re.x[0] = a.x; v.re.x[1] = a.y; v.re.x[2] = b.x; v.re.x[3] = b.y;
-    v.im.x[0] = c.x; v.im.x[1] = c.y; v.im.x[2] = d.x; v.im.x[3] = d.y;
-  }
-  return v;
-}
-template <int L>
-PHC_DEV void sstore(double* p, const typename Prec<L>::C& v) {
-  double2* q = reinterpret_cast<double2*>(p);
-  if constexpr (L == 2) {
-    q[0] = make_double2(v.re.x[0], v.re.x[1]);
-    q[1] = make_double2(v.im.x[0], v.im.x[1]);
-  } else {
-    q[0] = make_double2(v.re.x[0], v.re.x[1]);
-    q[1] = make_double2(v.re.x[2], v.re.x[3]);
-    q[2] = make_double2(v.im.x[0], v.im.x[1]);
-    q[3] = make_double2(v.im.x[2], v.im.x[3]);
-  }
-}
-template <int L>
 PHC_DEV typename Prec<L>::C shfl_down(const typename Prec<L>::C& v, int d) {
   typename Prec<L>::C r;
 #pragma unroll

@@ -1,0 +1,150 @@
+// NEXT-1: the rest of one Newton iteration of Alg. 2 (PAPER.md
+// P:256-324) after the evaluation: residual ||F||, Gaussian elimination with
+// partial pivoting on [J | -F] ("the largest number in the current column",
+// P:342-343), back substitution and the update z := z + dz.
+//
+// One CTA per point.  The augmented matrix lives in shared memory when it fits
+// (n (n+1) complex values), otherwise in a global workspace (large systems; correct but
+// one SM per point).  The paper's per-column pivot barrier is a __syncthreads;
+// its row-per-thread assignment becomes a (row, column) grid-stride over the CTA.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "arith.cuh"
+
+namespace phc {
+
+struct NewtonArgs {
+  const double* X;  // [P][n][2][L]
+  const double* F;  // [P][n][2][L]
+  const double* J;  // [P][n][n][2][L]
+  double* Xnew;     // [P][n][2][L] (may alias X)
+  double* resid;    // [P] max_i |F_i| (binary64)
+  int32_t* status;  // [P] 0 = ok, 1 = singular (zero pivot column)
+  double* Mg;       // global workspace [P][n][n+1][2][L] when the matrix does not fit shared memory
+  int n;
+  int64_t n_points;
+};
+
+template <int L, bool SMEM>
+__global__ void __launch_bounds__(256) newton_solve_kernel(const NewtonArgs a) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  extern __shared__ __align__(16) double nsm[];
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_piv, s_bad;
+  __shared__ __align__(16) double s_inv[2 * L];  // reciprocal of the current pivot
+  const int64_t p = blockIdx.x;
+  if (p >= a.n_points) return;
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
+  double* M = SMEM ? nsm : a.Mg + (size_t)p * n * cols * cd;
+  double* invd = M + (size_t)n * cols * cd;  // n pivot reciprocals after the matrix
+  auto at = [&](int i, int j) { return M + ((size_t)i * cols + j) * cd; };
+  auto ldm = [&](int i, int j) { return sload<L>(at(i, j)); };  // generic: shared or global
+  auto stm = [&](int i, int j, const C& v) { sstore<L>(at(i, j), v); };
+  const double* Fp = a.F + (size_t)p * n * cd;
+  const double* Jp = a.J + (size_t)p * n * n * cd;
+  // load [J | -F]; residual max_i |F_i|
+  double rmax = 0.0;
+  for (int e = tid; e < n * cols; e += T) {
+    const int i = e / cols, j = e % cols;
+    if (j < n) {
+      stm(i, j, cload<L>(Jp + ((size_t)i * n + j) * cd));
+    } else {
+      const C f = cload<L>(Fp + (size_t)i * cd);
+      rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
+      stm(i, j, P::neg(f));
+    }
+  }
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if (lane == 0) red_v[wid] = rmax;
+  if (tid == 0) s_bad = 0;
+  __syncthreads();
+  if (tid == 0) {
+    double r = 0.0;
+    for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
+    a.resid[p] = r;
+  }
+  __syncthreads();
+  // elimination with partial pivoting
+  for (int k = 0; k < n; ++k) {
+    // pivot: largest |M[i][k]|^2 (leading limbs) over i >= k; ties -> smallest i
+    double best = -1.0;
+    int bi = n;
+    for (int i = k + tid; i < n; i += T) {
+      const double v = P::abs2_hi(ldm(i, k));
+      if (v > best) { best = v; bi = i; }
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+    __syncthreads();
+    if (tid == 0) {
+      double b = -1.0;
+      int ix = n;
+      for (int w = 0; w < nwarp; ++w)
+        if (red_v[w] > b || (red_v[w] == b && red_i[w] < ix)) { b = red_v[w]; ix = red_i[w]; }
+      s_piv = ix;
+      if (!(b > 0.0)) s_bad = 1;
+    }
+    __syncthreads();
+    if (s_bad) break;
+    const int pv = s_piv;
+    if (pv != k)
+      for (int j = k + tid; j < cols; j += T) {
+        const C u = ldm(k, j), v = ldm(pv, j);
+        stm(k, j, v);
+        stm(pv, j, u);
+      }
+    __syncthreads();
+    if (tid == 0) {
+      const C inv = P::recip(ldm(k, k));
+      sstore<L>(s_inv, inv);
+      sstore<L>(invd + (size_t)k * cd, inv);
+    }
+    __syncthreads();
+    const C inv = sload<L>(s_inv);
+    // multipliers l_i = M[i][k] / M[k][k], stored in column k
+    for (int i = k + 1 + tid; i < n; i += T) stm(i, k, P::mul(ldm(i, k), inv));
+    __syncthreads();
+    // update M[i][j] -= l_i M[k][j], i > k, j > k
+    const int rows = n - k - 1, ucols = cols - k - 1;
+    for (int e = tid; e < rows * ucols; e += T) {
+      const int i = k + 1 + e / ucols, j = k + 1 + e % ucols;
+      stm(i, j, P::sub(ldm(i, j), P::mul(ldm(i, k), ldm(k, j))));
+    }
+    __syncthreads();
+  }
+  if (s_bad) {
+    if (tid == 0) a.status[p] = 1;
+    for (int e = tid; e < n; e += T)
+      cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
+    return;
+  }
+  // back substitution: x_i = M[i][n] / M[i][i], then M[r][n] -= M[r][i] x_i for r < i
+  for (int i = n - 1; i >= 0; --i) {
+    if (tid == 0) {
+      const C inv = sload<L>(invd + (size_t)i * cd);
+      stm(i, n, P::mul(ldm(i, n), inv));
+    }
+    __syncthreads();
+    const C xi = ldm(i, n);
+    for (int r = tid; r < i; r += T) stm(r, n, P::sub(ldm(r, n), P::mul(ldm(r, i), xi)));
+    __syncthreads();
+  }
+  // z := z + dz
+  for (int e = tid; e < n; e += T) {
+    const double* xp = a.X + ((size_t)p * n + e) * cd;
+    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), ldm(e, n)));
+  }
+  if (tid == 0) a.status[p] = 0;
+}
+
+}  // namespace phc

@@ -17,6 +17,7 @@
 #include "../../include/phc.h"
 #include "kernels_generic.cuh"
 #include "kernels_block.cuh"
+#include "kernels_newton.cuh"
 
 namespace {
 
@@ -82,6 +83,11 @@ struct DeviceState {
   double* Y = nullptr;
   double* G = nullptr;
   int64_t chunk_cap = 0;
+  // Newton-step workspace (evaluation outputs and the global elimination matrix)
+  double* nF = nullptr;
+  double* nJ = nullptr;
+  double* nM = nullptr;
+  int64_t n_cap = 0;
   // staging buffers for remote shards
   double* xs = nullptr;
   double* fs = nullptr;
@@ -489,6 +495,74 @@ int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double
   }
   cudaEventDestroy(start);
   return rc;
+}
+
+int phc_newton_step_batch(const phc_system* cs, int64_t n_points, const double* x, double* x_new, double* residual,
+                          int32_t* status, void* stream) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "Newton needs a square system (n_eq %d != n_var %d)", s->n_eq, s->n_var);
+  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
+  if (n_points == 0) return PHC_OK;
+  if (!x || !x_new || !residual || !status) return fail(PHC_EINVAL, "NULL pointer");
+  if ((((uintptr_t)x) | ((uintptr_t)x_new)) & 31) return fail(PHC_EINVAL, "x/x_new must be 32-byte aligned");
+  DeviceGuard g(s->home);
+  DeviceState* d;
+  int rc = get_device_state(s, s->home, &d);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = s->n_eq, L = s->L;
+  const int64_t cd = 2 * L;
+  const size_t mat = ((size_t)n * (n + 1) + n) * cd * sizeof(double);  // [J | -F] + pivot reciprocals
+  const bool smem = mat <= (size_t)200 * 1024;
+  const int64_t per_point = (int64_t)n * n * cd * 8 + (smem ? 0 : (int64_t)mat);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)512 << 20) / per_point));
+  if (d->n_cap < chunk) {
+    cudaStreamSynchronize(st);
+    for (double** q : {&d->nF, &d->nJ, &d->nM}) {
+      if (*q) cudaFree(*q);
+      *q = nullptr;
+    }
+    d->n_cap = 0;
+    if ((rc = dalloc(&d->nF, (size_t)(chunk * n * cd)))) return rc;
+    if ((rc = dalloc(&d->nJ, (size_t)(chunk * n * n * cd)))) return rc;
+    if (!smem && (rc = dalloc(&d->nM, (size_t)chunk * mat / sizeof(double)))) return rc;
+    d->n_cap = chunk;
+  }
+  const int threads = n <= 48 ? 128 : 256;
+  for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
+    const int64_t np = std::min(chunk, n_points - p0);
+    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, d->nF, d->nJ, st))) return rc;
+    phc::NewtonArgs a;
+    a.X = x + p0 * n * cd;
+    a.F = d->nF;
+    a.J = d->nJ;
+    a.Xnew = x_new + p0 * n * cd;
+    a.resid = residual + p0;
+    a.status = status + p0;
+    a.Mg = d->nM;
+    a.n = n;
+    a.n_points = np;
+    ProfScope ps(s, d->dev, 2, st);
+    if (L == 2) {
+      if (smem) {
+        if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
+        phc::newton_solve_kernel<2, true><<<(unsigned)np, threads, mat, st>>>(a);
+      } else {
+        phc::newton_solve_kernel<2, false><<<(unsigned)np, threads, 0, st>>>(a);
+      }
+    } else {
+      if (smem) {
+        if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
+        phc::newton_solve_kernel<4, true><<<(unsigned)np, threads, mat, st>>>(a);
+      } else {
+        phc::newton_solve_kernel<4, false><<<(unsigned)np, threads, 0, st>>>(a);
+      }
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  return PHC_OK;
 }
 
 int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* jac, void* stream) {

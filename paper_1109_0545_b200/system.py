@@ -90,6 +90,22 @@ class System:
         _lib.phc_eval_jacobian_batch(self._h, P, _ptr(X), _ptr(F), _ptr(J), dv, nd, ctypes.c_void_p(st))
         return F, J
 
+    def newton_step(self, X, X_new=None, stream=None):
+        """One Newton iteration per point (NEXT-1): X [P, n, 2, L] on the home device ->
+        (X_new, residual [P] float64, status [P] int32).  X_new may be X (in place)."""
+        import torch
+
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        if X_new is None:
+            X_new = torch.empty_like(X)
+        res = torch.empty(P, dtype=torch.float64, device=X.device)
+        status = torch.empty(P, dtype=torch.int32, device=X.device)
+        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        _lib.phc_newton_step_batch(self._h, P, _ptr(X), _ptr(X_new), _ptr(res), _ptr(status), ctypes.c_void_p(st))
+        return X_new, res, status
+
     def eval_batch_host(self, X, F=None, J=None, devices=None):
         """Host arrays (numpy or pinned CPU tensors) in and out; synchronous."""
         L = self.limbs

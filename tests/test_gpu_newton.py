@@ -1,0 +1,145 @@
+"""GPU parity for NEXT-1, one Newton iteration (Alg. 2): the CUDA step
+(evaluation + GE with partial pivoting + back substitution + update) against the exact
+oracle step; quadratic convergence to a known root at full size; singular pivots."""
+import math
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import newton_step  # noqa: E402
+from synthetic import config_system, limbs_from_values, system_from_terms  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def phc():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1109_0545_b200 as m
+    return m
+
+
+def _tol(L, n, cond):
+    """Normwise error budget of one DD/QD Newton step: the evaluation error (<= 1e-28 / 1e-60
+    relative) and the elimination's backward error (~ n u) are amplified by cond(J)."""
+    u = 2.0 ** -104 if L == 2 else 2.0 ** -209
+    return max(1e-28 if L == 2 else 1e-60, 64 * n * u * cond)
+
+
+def _gpu_step(phc, s, X):
+    h = phc.System(s)
+    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
+    Xn, res, status = h.newton_step(Xd)
+    torch.cuda.synchronize()
+    return Xn.cpu().numpy(), res.cpu().numpy(), status.cpu().numpy(), h
+
+
+def _check_point(s, Xp, xn, res):
+    """Normwise error of the GPU's new point against the oracle step (mp512 evaluation and
+    mpmath.lu_solve; exact rationals only for the tiny config), relative to ||dz||."""
+    import mpmath
+    arith = "exact" if s.n_var <= 8 else "mp"
+    out = newton_step(s, Xp, arith)
+    assert not out["singular"]
+    with mpmath.workprec(1024):
+        if arith == "exact":
+            ref = [mpmath.mpc(mpmath.mpf(a[0].numerator) / a[0].denominator, mpmath.mpf(a[1].numerator) / a[1].denominator)
+                   for a in out["z_new"]]
+            dz = [mpmath.mpc(mpmath.mpf(a[0].numerator) / a[0].denominator, mpmath.mpf(a[1].numerator) / a[1].denominator)
+                  for a in out["dz"]]
+        else:
+            ref, dz = out["z_new"], out["dz"]
+        got = [mpmath.mpc(mpmath.fsum(mpmath.mpf(float(d)) for d in v[0]), mpmath.fsum(mpmath.mpf(float(d)) for d in v[1]))
+               for v in xn]
+        num = max(abs(a - b) for a, b in zip(got, ref))
+        den = max(abs(d) for d in dz)
+    assert res == pytest.approx(out["residual"], rel=1e-12)
+    return float(num / den)
+
+
+@pytest.mark.parametrize("name,seed", [("tiny", 1), ("tiny", 2), ("c2", 1), ("c3", 1)])
+def test_newton_step_vs_exact_oracle(phc, name, seed):
+    s, X = config_system(name, seed=seed)
+    xn, res, status, h = _gpu_step(phc, s, X)
+    assert status[0] == 0
+    # condition number of J (float64) for the error budget
+    F, Jd = h.eval(torch.from_numpy(X[0]).cuda())
+    Jc = Jd.cpu().numpy()[..., 0, 0] + 1j * Jd.cpu().numpy()[..., 1, 0]
+    cond = np.linalg.cond(Jc)
+    err = _check_point(s, X[0], xn[0], res[0])
+    assert err <= _tol(s.limbs, s.n_var, cond), (err, cond)
+
+
+def test_newton_step_batch_sampled(phc):
+    s, X = config_system("batch", seed=2, points=4096)
+    xn, res, status, h = _gpu_step(phc, s, X)
+    assert (status == 0).all()
+    F, J = h.eval_batch(torch.from_numpy(X[[0, 1000, 4095]]).cuda())
+    Jn = J.cpu().numpy()
+    for k, p in enumerate((0, 1000, 4095)):
+        cond = np.linalg.cond(Jn[k][..., 0, 0] + 1j * Jn[k][..., 1, 0])
+        err = _check_point(s, X[p], xn[p], res[p])
+        assert err <= _tol(2, 32, cond), (p, err, cond)
+
+
+def _root_system(n, k, L, seed):
+    """f_i(x) = sum_t c_t (m_t(x) - 1): vanishes at x = (1, ..., 1) exactly."""
+    rng = np.random.default_rng(seed)
+    polys, coeffs = [], []
+    for i in range(n):
+        terms = [[(v, int(rng.integers(1, 4))) for v in sorted(rng.choice(n, k, replace=False).tolist())]
+                 for _ in range(6)]
+        terms.append([(i, 1)])  # keeps J well conditioned near the root
+        c = [complex(*rng.integers(-3, 4, 2)) or 1 for _ in terms]
+        c[-1] = complex(4 * k + 8, 1)
+        polys.append(terms + [[]])
+        coeffs += c + [-sum(c)]
+    return system_from_terms(n, n, L, polys, limbs_from_values(coeffs, L))
+
+
+@pytest.mark.parametrize("n,k,L,steps,tol", [(32, 8, 2, 4, 1e-29), (40, 10, 4, 5, 1e-61), (256, 16, 4, 5, 1e-60)])
+def test_newton_converges_quadratically_to_known_root(phc, n, k, L, steps, tol):
+    """At any size (incl. the n = 256 QD global-memory elimination): from x* + delta the error
+    roughly squares each step down to the working precision."""
+    s = _root_system(n, k, L, seed=n)
+    rng = np.random.default_rng(7)
+    x0 = [1 + 1e-3 * complex(*rng.uniform(-1, 1, 2)) for _ in range(n)]
+    X = torch.from_numpy(limbs_from_values(x0, L)[None].copy()).cuda()
+    h = phc.System(s)
+    errs = []
+    for _ in range(steps):
+        X, res, status = h.newton_step(X, X)  # in place
+        torch.cuda.synchronize()
+        assert int(status[0]) == 0
+        x = X.cpu().numpy()[0]
+        re = x[:, 0, :].sum(axis=1) - 1.0  # limb sums in float64 suffice for the first steps
+        e_hi = max(abs(x[:, 0, 0] - 1.0).max(), abs(x[:, 1, 0]).max())
+        errs.append(e_hi)
+    assert errs[0] < 1e-4 and errs[1] < 1e-7
+    # final: exact error from the limbs
+    from fractions import Fraction
+    x = X.cpu().numpy()[0]
+    final = max(abs(complex(float(sum(Fraction(float(d)) for d in x[v, 0]) - 1), float(sum(Fraction(float(d)) for d in x[v, 1]))))
+                for v in range(n))
+    assert final <= tol, final
+
+
+def test_newton_singular_and_in_place(phc):
+    """A variable absent from the system gives a zero Jacobian column: status 1, x unchanged.
+    In-place and out-of-place steps agree bitwise."""
+    s = system_from_terms(2, 2, 2, [[[(0, 2)], []], [[(0, 1)], []]], limbs_from_values([1, -4, 1, 2], 2))
+    X = torch.from_numpy(limbs_from_values([3, 5], 2)[None].copy()).cuda()
+    h = phc.System(s)
+    Xn, res, status = h.newton_step(X)
+    torch.cuda.synchronize()
+    assert int(status[0]) == 1 and torch.equal(Xn, X)
+    s2, X2 = config_system("c2", seed=3, points=8)
+    h2 = phc.System(s2)
+    A = torch.from_numpy(X2).cuda()
+    B = A.clone()
+    out, _, _ = h2.newton_step(A)
+    h2.newton_step(B, B)
+    torch.cuda.synchronize()
+    assert torch.equal(out, B)
