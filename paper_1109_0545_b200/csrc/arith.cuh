@@ -19,6 +19,11 @@ namespace phc {
 
 #define PHC_DEV __device__ __forceinline__
 
+// QD dot product summation shape (1 = balanced trees, 0 = the sequential chains)
+#ifndef PHC_QD_TREE
+#define PHC_QD_TREE 1
+#endif
+
 PHC_DEV double add_(double a, double b) { return __dadd_rn(a, b); }
 PHC_DEV double sub_(double a, double b) { return __dadd_rn(a, -b); }
 PHC_DEV double mul_(double a, double b) { return __dmul_rn(a, b); }
@@ -202,6 +207,48 @@ PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
   // level 0
   double a0, e;
   two_sum(p0, r0, a0, e);
+#if PHC_QD_TREE
+  // Same exact transformations as below, summed as balanced trees instead of chains: the
+  // dependent-DADD depth per product falls from ~29 two_sums to ~14 (the profile's top
+  // stall was the fixed-latency dependency wait).
+  // level 1 (7 terms): e, q0, t0, p1, p2, r1, r2 -> a1, errors f1..f6 (order 2)
+  double a1, f1, f2, f3, f4, f5, f6;
+  {
+    double u1, u2, u3, u4, u5;
+    two_sum(e, q0, u1, f1);
+    two_sum(t0, p1, u2, f2);
+    two_sum(p2, r1, u3, f3);
+    two_sum(u1, u2, u4, f4);
+    two_sum(u3, r2, u5, f5);
+    two_sum(u4, u5, a1, f6);
+  }
+  // level 2 (16 terms) -> a2; the 15 errors (order 3) are summed plainly into o
+  double a2;
+  {
+    double v0, v1, v2, v3, v4, v5, v6, v7, g0, g1, g2, g3, g4, g5, g6, g7;
+    two_sum(f1, f2, v0, g0);
+    two_sum(f3, f4, v1, g1);
+    two_sum(f5, f6, v2, g2);
+    two_sum(q1, q2, v3, g3);
+    two_sum(t1, t2, v4, g4);
+    two_sum(p3, p4, v5, g5);
+    two_sum(p5, r3, v6, g6);
+    two_sum(r4, r5, v7, g7);
+    double w0, w1, w2, w3, h0, h1, h2, h3;
+    two_sum(v0, v1, w0, h0);
+    two_sum(v2, v3, w1, h1);
+    two_sum(v4, v5, w2, h2);
+    two_sum(v6, v7, w3, h3);
+    double z0, z1, k0, k1, k2;
+    two_sum(w0, w1, z0, k0);
+    two_sum(w2, w3, z1, k1);
+    two_sum(z0, z1, a2, k2);
+    const double gs = add_(add_(add_(g0, g1), add_(g2, g3)), add_(add_(g4, g5), add_(g6, g7)));
+    const double hs = add_(add_(h0, h1), add_(h2, h3));
+    o = add_(o, add_(add_(gs, hs), add_(add_(k0, k1), k2)));
+  }
+  return renorm4_robust(a0, a1, a2, o);
+#else
   // level 1: e, q0, t0, p1, p2, r1, r2 -> a1, errors f1..f6 (order 2)
   double a1 = e, f1, f2, f3, f4, f5, f6;
   two_sum(a1, q0, a1, f1);
@@ -228,6 +275,7 @@ PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
   two_sum(a2, r4, a2, g); o = add_(o, g);
   two_sum(a2, r5, a2, g); o = add_(o, g);
   return renorm4_robust(a0, a1, a2, o);
+#endif
 }
 
 // ---------------------------------------------------------------------------

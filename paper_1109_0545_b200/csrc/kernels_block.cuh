@@ -155,20 +155,48 @@ PHC_DEV void dummy_row(int E, double* row, bool smem) {
   }
 }
 
-// Global power table for configurations whose table does not fit in shared memory.
+// x^e for 0 <= e < 256 by binary powering (square-and-multiply from the top bit): at most
+// 2 log2(e) products on the dependency path instead of e - 1.
+template <int L>
+PHC_DEV typename Prec<L>::C cpow(const typename Prec<L>::C& x, int e) {
+  using P = Prec<L>;
+  if (e == 0) return P::one();
+  int top = 31 - __clz(e);
+  typename P::C r = x;
+  for (int b = top - 1; b >= 0; --b) {
+    r = P::mul(r, r);
+    if ((e >> b) & 1) r = P::mul(r, x);
+  }
+  return r;
+}
+
+// Global power table for configurations whose table does not fit in shared memory (row
+// a2, reading C4): one thread per entry (point, variable, a), U[a-1] = x^a and
+// Dd[a-1] = a x^(a-1), both from one binary powering x^(a-1); the dummy row is U = 1,
+// Dd = 0.  Dependency path <= 4 products (E <= 8) instead of 2E - 1 for a sequential row.
+// Launched as the primary of a programmatic dependent launch: the block kernel starts
+// while this one runs and waits (griddepcontrol.wait) before it reads the table.
 template <int L>
 __global__ void block_power_table_kernel(const double* __restrict__ X, int n_var, int E, int64_t n_points,
                                          double* __restrict__ PT) {
+  using P = Prec<L>;
+  asm volatile("griddepcontrol.launch_dependents;");
   const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t per = n_var + 1;
+  const int64_t per = (int64_t)(n_var + 1) * E;
   if (gid >= n_points * per) return;
   const int64_t p = gid / per;
-  const int v = (int)(gid % per);
-  double* row = PT + (p * per + v) * (2 * E) * (2 * L);
-  if (v == n_var)
-    dummy_row<L>(E, row, false);
-  else
-    power_row<L>(cload<L>(X + (p * n_var + v) * 2 * L), E, row, false);
+  const int r = (int)(gid % per);
+  const int v = r / E, a = r % E + 1;
+  double* row = PT + (p * (n_var + 1) + v) * (2 * E) * (2 * L);
+  if (v == n_var) {
+    cstore<L>(row + (a - 1) * 2 * L, P::one());
+    cstore<L>(row + (E + a - 1) * 2 * L, P::zero());
+    return;
+  }
+  const typename P::C x = cload<L>(X + (p * n_var + v) * 2 * L);
+  const typename P::C pm = cpow<L>(x, a - 1);
+  cstore<L>(row + (a - 1) * 2 * L, a == 1 ? x : P::mul(pm, x));
+  cstore<L>(row + (E + a - 1) * 2 * L, a == 1 ? pm : P::mul_int(pm, (double)a));
 }
 
 // Shared-memory layouts of the power table (PT) and of the Jacobian row accumulators.
@@ -261,10 +289,10 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   C p = cload<L>(a.coef + ((size_t)b * kWarp + lane) * 2 * L);  // running P
   C q;                                                           // running S
   // phase 1
-  auto phase1 = [&](int t) {
+  auto phase1 = [&](int t, uint32_t w1, uint32_t w2) {  // w1 = word_at(t), w2 = word_at(K - t + 1)
     Pk[t - 1] = p;
-    p = P::mul_lazy(p, ld(entry(word_at(t))));
-    const C u = ld(entry(word_at(K - t + 1)));
+    p = P::mul_lazy(p, ld(entry(w1)));
+    const C u = ld(entry(w2));
     if (t == 1) {
       q = u;
     } else {
@@ -273,8 +301,8 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
     }
   };
   // phase 2
-  auto phase2 = [&](int t, const C& pk, const C& sk) {  // pk = P_{H-t}, sk = S_{H-t}
-    const uint32_t wa = word_at(H + t), wb = word_at(H - t + 1);
+  // pk = P_{H-t}, sk = S_{H-t}; wa = word_at(H + t), wb = word_at(H - t + 1)
+  auto phase2 = [&](int t, const C& pk, const C& sk, uint32_t wa, uint32_t wb) {
     const int ea = entry(wa), eb = entry(wb);
     C ga = P::mul_lazy(p, ld(ea + a.E));
     if (t < H) ga = P::mul_lazy(ga, sk);
@@ -287,22 +315,39 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   };
   if constexpr (L == 2) {
 #pragma unroll
-    for (int t = 1; t <= H; ++t) phase1(t);
+    for (int t = 1; t <= H; ++t) phase1(t, word_at(t), word_at(K - t + 1));
 #pragma unroll
-    for (int t = 1; t <= H; ++t) phase2(t, Pk[H - t], t < H ? Sk[H - t] : P::one());
+    for (int t = 1; t <= H; ++t)
+      phase2(t, Pk[H - t], t < H ? Sk[H - t] : P::one(), word_at(H + t), word_at(H - t + 1));
   } else {
+    // rolled loops (the QD body is thousands of instructions): the factor words are
+    // fetched one step ahead, so the table gathers of a step do not wait on them
+    uint32_t w1 = word_at(1), w2 = word_at(K);
 #pragma unroll 1
-    for (int t = 1; t <= H; ++t) phase1(t);
+    for (int t = 1; t <= H; ++t) {
+      const uint32_t c1 = w1, c2 = w2;
+      if (t < H) {
+        w1 = word_at(t + 1);
+        w2 = word_at(K - t);
+      } else {
+        w1 = word_at(H + 1);
+        w2 = word_at(H);
+      }
+      phase1(t, c1, c2);
+    }
     // the kept values live in local memory here: fetch them one step ahead
     C pk_n = Pk[H - 1], sk_n = (H > 1) ? Sk[H - 1] : P::one();
 #pragma unroll 1
     for (int t = 1; t <= H; ++t) {
       const C pk = pk_n, sk = sk_n;
+      const uint32_t wa = w1, wb = w2;
       if (t < H) {
         pk_n = Pk[H - t - 1];
         sk_n = (t + 1 < H) ? Sk[H - t - 1] : P::one();
+        w1 = word_at(H + t + 1);
+        w2 = word_at(H - t);
       }
-      phase2(t, pk, sk);
+      phase2(t, pk, sk, wa, wb);
     }
   }
   return warp_sum<L>(P::norm(p));
@@ -353,6 +398,8 @@ block_kernel(const BlockArgs a) {
   if constexpr (LAYOUT == 0) {
     pt = const_cast<double*>(a.PTg) + p * (int64_t)(a.n_var + 1) * twoE * cd;
     rows_all = smem;
+    // dependent launch: the power table of the primary kernel is complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
   } else {
     pt = smem;
     const int NE = (a.n_var + 1) * twoE;
@@ -661,7 +708,22 @@ int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_poin
     b.J = a.J + p0 * (int64_t)a.n_eq * a.n_var * 2 * L;
     if (LAYOUT == 0) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
     b.n_points = np;
-    kern<<<(unsigned)(np * units), plan.nw * kWarp, plan.smem_bytes, st>>>(b);
+    if (LAYOUT == 0) {
+      // programmatic dependent launch after block_power_table_kernel (same stream)
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)(np * units));
+      cfg.blockDim = dim3(plan.nw * kWarp);
+      cfg.dynamicSmemBytes = plan.smem_bytes;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+      attr[0].val.programmaticStreamSerializationAllowed = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      if (cudaLaunchKernelEx(&cfg, kern, b) != cudaSuccess) return -3;
+    } else {
+      kern<<<(unsigned)(np * units), plan.nw * kWarp, plan.smem_bytes, st>>>(b);
+    }
     if (cudaGetLastError() != cudaSuccess) return -3;
     p0 += np;
   }
@@ -737,7 +799,7 @@ int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, i
   }
   for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
     const int64_t np = std::min(chunk, n_points - p0);
-    const int64_t nth = np * (n_var + 1);
+    const int64_t nth = np * (n_var + 1) * plan.E;
     block_power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * n_var * 2 * L, n_var,
                                                                                plan.E, np, bt.PT);
     BlockArgs b = a;
