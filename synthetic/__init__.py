@@ -17,4 +17,7 @@ from .systems import (  # noqa: F401
     special_univariate_system,
     homogeneous_system,
     system_from_terms,
+    homotopy_target,
+    real_limbs,
+    random_t,
 )

@@ -276,3 +276,47 @@ def homogeneous_system(n, m, k, d, limbs, seed, points=1):
     coeff = unit_circle_limbs(thetas_c, limbs, 1)
     X = unit_circle_limbs(thetas_x, limbs, 1)
     return system_from_terms(n, n, limbs, polys, coeff), X, degs
+
+
+# ---------------------------------------------------------------------------
+# Homotopy inputs (NEXT-3): target coefficients on the same support, and real t values
+# ---------------------------------------------------------------------------
+
+def homotopy_target(system, seed, workers=None) -> np.ndarray:
+    """Target coefficients c_target [n_terms][2][L] on the system's support: unit-circle,
+    angles from ``PCG64(seed)`` (the start coefficients are the system's own)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    thetas = rng.uniform(0.0, 2.0 * math.pi, size=system.n_terms)
+    return unit_circle_limbs(thetas, system.limbs, workers)
+
+
+def real_limbs(values, limbs: int) -> np.ndarray:
+    """Real numbers (float, int or Fraction) → [len][limbs] float64 limbs (greedy split)."""
+    prec = 64 * limbs + 64
+    out = np.zeros((len(values), limbs))
+    for j, v in enumerate(values):
+        if hasattr(v, "numerator") and not isinstance(v, (int, float)):
+            mp = from_rational(v.numerator, v.denominator, prec)
+        elif isinstance(v, int):
+            mp = from_int(v)
+        else:
+            mp = from_float(float(v))
+        out[j] = split_limbs(mp, limbs, prec)
+    return out
+
+
+def random_t(P, limbs, seed) -> np.ndarray:
+    """P seeded values of t in (0, 1) with full DD/QD limbs: t = u / 2^(53 L) for a uniform
+    integer u, so every limb is significant (the tracker's t are sums of step sizes)."""
+    from fractions import Fraction
+
+    rng = np.random.Generator(np.random.PCG64(seed))
+    bits = 53 * limbs
+    vals = []
+    for _ in range(P):
+        u = 0
+        for _w in range((bits + 31) // 32):
+            u = (u << 32) | int(rng.integers(0, 1 << 32))
+        u >>= (((bits + 31) // 32) * 32 - bits)
+        vals.append(Fraction(u, 1 << bits))
+    return real_limbs(vals, limbs)
