@@ -114,6 +114,45 @@ int phc_eval_jacobian_batch_host(const phc_system* s, int64_t n_points, const do
 int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x, double* x_new, double* residual,
                           int32_t* status, void* stream);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-3: homotopy coefficients.  PAPER.md §7 P:647-649 (Table 6,
+ * P:651-668): the "new" evaluator handles the continuation parameter t through the
+ * coefficients, the "old" one treats t "as just another variable".  With start
+ * coefficients c_s (the system's own, given to phc_system_create) and target coefficients
+ * c_f on the same support, the homotopy is (reading H1)
+ *     h_i(x, t) = sum_{t' in T_i} ((1 - t) c_s + t c_f) x^{a_t'} .
+ * --------------------------------------------------------------------------------------- */
+
+/* Attach target coefficients coeff_target [n_terms][2][limbs] (HOST pointer, deep-copied,
+ * same term order as coeff) and upload them to every device the handle uses.  Calling it
+ * again replaces them (the home device is synchronised first).  PHC_EINVAL on NULL or
+ * non-finite limbs.  The plain eval calls keep evaluating the start coefficients. */
+int phc_system_set_target(phc_system* s, const double* coeff_target);
+
+/* h(., t_p) and its Jacobian in x at n_points points, each with its own real t_p:
+ * t [n_points][limbs] (DD/QD limbs of a real, device pointer on the home device); x, f,
+ * jac, devices, stream as in phc_eval_jacobian_batch.  The blend c(t) is formed per term
+ * inside the kernels (one complex-by-real product per coefficient, 2 per term).
+ * PHC_EINVAL if no target is attached. */
+int phc_eval_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t, double* f,
+                            double* jac, const int32_t* devices, int32_t n_devices, void* stream);
+
+/* One Newton iteration on h(., t_p) = 0 per point (phc_newton_step_batch with the homotopy
+ * coefficients at t [n_points][limbs], device pointer). */
+int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t,
+                                   double* x_new, double* residual, int32_t* status, void* stream);
+
+/* The "old" evaluator of Table 6: a handle for the (n_var + 1)-variable system
+ * in which every term c x^a of the homotopy becomes c_s x^a - c_s t x^a + c_f t x^a with t
+ * the variable n_var.  Evaluating it with phc_eval_jacobian[_batch] at (x, t) (t as a
+ * complex coordinate with zero imaginary part) gives h, and a Jacobian of n_var + 1 columns
+ * whose last column is dh/dt.  Same arguments and validation as phc_system_create plus
+ * coeff_target. */
+int phc_homotopy_old_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_terms,
+                            const int64_t* poly_ptr, const int64_t* term_ptr, const int32_t* var_idx,
+                            const int32_t* exponent, const double* coeff_start, const double* coeff_target,
+                            int32_t device);
+
 /* Static facts about the system, as built: counts used by the benchmark's model.
  * out[0] = n_terms, out[1] = n_factors, out[2] = max k, out[3] = max exponent D,
  * out[4] = nnz(J) (structurally nonzero entries), out[5] = complex multiplies per point

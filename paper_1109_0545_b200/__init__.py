@@ -16,6 +16,10 @@ from ._lib import (  # noqa: F401
     phc_fp64_peak,
     phc_last_error,
     phc_newton_step_batch,
+    phc_newton_step_homotopy_batch,
+    phc_eval_homotopy_batch,
+    phc_system_set_target,
+    phc_homotopy_old_create,
     phc_profile_enable,
     phc_profile_read,
     phc_system_create,

@@ -27,6 +27,10 @@ EXPORTED = (
     "phc_eval_jacobian_batch",
     "phc_eval_jacobian_batch_host",
     "phc_newton_step_batch",
+    "phc_system_set_target",
+    "phc_eval_homotopy_batch",
+    "phc_newton_step_homotopy_batch",
+    "phc_homotopy_old_create",
     "phc_system_stats",
     "phc_fp64_peak",
     "phc_profile_enable",
@@ -62,6 +66,14 @@ def _load():
     lib.phc_eval_jacobian_batch_host.restype = ctypes.c_int
     lib.phc_newton_step_batch.argtypes = [P, i64, P, P, P, P, P]
     lib.phc_newton_step_batch.restype = ctypes.c_int
+    lib.phc_system_set_target.argtypes = [P, P]
+    lib.phc_system_set_target.restype = ctypes.c_int
+    lib.phc_eval_homotopy_batch.argtypes = [P, i64, P, P, P, P, P, i32, P]
+    lib.phc_eval_homotopy_batch.restype = ctypes.c_int
+    lib.phc_newton_step_homotopy_batch.argtypes = [P, i64, P, P, P, P, P, P]
+    lib.phc_newton_step_homotopy_batch.restype = ctypes.c_int
+    lib.phc_homotopy_old_create.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, P, P, i32]
+    lib.phc_homotopy_old_create.restype = ctypes.c_int
     lib.phc_system_stats.argtypes = [P, P]
     lib.phc_system_stats.restype = ctypes.c_int
     lib.phc_fp64_peak.argtypes = [i32, ctypes.c_double, ctypes.POINTER(ctypes.c_double)]
@@ -113,6 +125,26 @@ def phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices):
 
 def phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream):
     return check(lib.phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream))
+
+
+def phc_system_set_target(h, coeff_target):
+    return check(lib.phc_system_set_target(h, coeff_target))
+
+
+def phc_eval_homotopy_batch(h, n_points, x, t, f, jac, devices, n_devices, stream):
+    return check(lib.phc_eval_homotopy_batch(h, n_points, x, t, f, jac, devices, n_devices, stream))
+
+
+def phc_newton_step_homotopy_batch(h, n_points, x, t, x_new, residual, status, stream):
+    return check(lib.phc_newton_step_homotopy_batch(h, n_points, x, t, x_new, residual, status, stream))
+
+
+def phc_homotopy_old_create(n_eq, n_var, limbs, n_terms, poly_ptr, term_ptr, var_idx, exponent, coeff_start,
+                            coeff_target, device):
+    h = ctypes.c_void_p()
+    check(lib.phc_homotopy_old_create(ctypes.byref(h), n_eq, n_var, limbs, n_terms, poly_ptr, term_ptr, var_idx,
+                                      exponent, coeff_start, coeff_target, device))
+    return h
 
 
 def phc_system_stats(h):

@@ -333,6 +333,10 @@ template <> struct Prec<2> {
   PHC_DEV static C zero() { C z; z.re = dd_make(0, 0); z.im = dd_make(0, 0); return z; }
   PHC_DEV static C one() { C z; z.re = dd_make(1, 0); z.im = dd_make(0, 0); return z; }
   PHC_DEV static C add(const C& a, const C& b) { C r; r.re = dd_add(a.re, b.re); r.im = dd_add(a.im, b.im); return r; }
+  // real helpers (homotopy parameter t, NEXT-3)
+  PHC_DEV static real rload(const double* p) { return dd_make(p[0], p[1]); }
+  PHC_DEV static real one_minus(const real& t) { return dd_add(dd_make(1, 0), dd_neg(t)); }
+  PHC_DEV static C mul_real(const C& a, const real& s) { C r; r.re = dd_mul(a.re, s); r.im = dd_mul(a.im, s); return r; }
   // fused complex DD product: each real part is a 2-term dot product accumulated
   // in one error term, with one renormalisation (normwise error ~ u^2 |a||b|).
   PHC_DEV static C mul(const C& a, const C& b) {
@@ -447,6 +451,10 @@ template <> struct Prec<4> {
   PHC_DEV static C zero() { C z; for (int i = 0; i < 4; ++i) { z.re.x[i] = 0; z.im.x[i] = 0; } return z; }
   PHC_DEV static C one() { C z = zero(); z.re.x[0] = 1; return z; }
   PHC_DEV static C add(const C& a, const C& b) { C r; r.re = qd_add(a.re, b.re); r.im = qd_add(a.im, b.im); return r; }
+  // real helpers (homotopy parameter t, NEXT-3)
+  PHC_DEV static real rload(const double* p) { qd r; for (int i = 0; i < 4; ++i) r.x[i] = p[i]; return r; }
+  PHC_DEV static real one_minus(const real& t) { return qd_add(qd_from_d(1.0), qd_neg(t)); }
+  PHC_DEV static C mul_real(const C& a, const real& s) { C r; r.re = qd_mul(a.re, s); r.im = qd_mul(a.im, s); return r; }
   // fused complex QD product: each real part is a QD dot product x*y + z*w evaluated in
   // one pass (qd_dot2), instead of two qd_mul and a qd_add (~440 vs ~680 FP64 instructions).
   PHC_DEV static C mul(const C& a, const C& b) {

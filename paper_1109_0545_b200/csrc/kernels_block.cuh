@@ -54,6 +54,7 @@ constexpr uint32_t kDummyVar = 0xFFFFu;
 struct BlockTables {
   uint32_t* fac = nullptr;
   double* coeff = nullptr;
+  double* coeff2 = nullptr;  // homotopy target coefficients (NEXT-3), packed like coeff
   int32_t* blk = nullptr;  // poly_blk_ptr [n_eq + 1]
   double* PT = nullptr;    // global power table scratch (layout 0)
   int64_t pt_cap = 0;
@@ -73,6 +74,7 @@ struct HostBlockPlan {
   std::vector<uint32_t> fac;
   std::vector<double> coeff;
   std::vector<int32_t> blk;
+  std::vector<int64_t> slot_term;  // [n_blocks * 32]: term of (block, lane), -1 for padding
   int64_t cm_per_point = 0;
   int64_t ca_per_point = 0;
   int64_t exec_flops_per_point = 0;
@@ -92,6 +94,8 @@ inline OpFlops op_flops(int L) {
 struct BlockArgs {
   const uint32_t* fac;
   const double* coef;
+  const double* coef2;  // NEXT-3: target coefficients (packed like coef) or nullptr
+  const double* T;      // NEXT-3: t per point [n_points][L] (real limbs) when coef2 != nullptr
   const int32_t* blk;
   const double* X;
   const double* PTg;
@@ -248,8 +252,13 @@ PHC_DEV typename Prec<L>::C cls_load(const double2* base, int NE, int e, int c) 
 // partner, giving g_{H+t} = P_{H+t-1} S_{H-t} d_{H+t} and g_{H-t+1} = P_{H-t} S_{H+t-1}
 // d_{H-t+1}, before both chains advance.  4K-3 complex products, critical path K
 // products (two independent chains) instead of 2K-2 for a backward-then-forward sweep.
+//
+// Homotopy (NEXT-3): when hom, the coefficient is the blend
+// c(t) = (1 - t) c_start + t c_target (reading H1), formed here before it is folded into P_0.
 template <int L, int K, int LAYOUT>
-PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double* pt, double* rows, int lane) {
+PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double* pt, double* rows, int lane,
+                                     bool hom, const typename Prec<L>::real& omt,
+                                     const typename Prec<L>::real& tt) {
   using P = Prec<L>;
   using C = typename P::C;
   constexpr int H = K / 2;
@@ -287,6 +296,7 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   C Pk[H];  // P_0 .. P_{H-1}
   C Sk[H];  // S_1 .. S_{H-1} at Sk[1..H-1]
   C p = cload<L>(a.coef + ((size_t)b * kWarp + lane) * 2 * L);  // running P
+  if (hom) p = P::add(P::mul_real(p, omt), P::mul_real(cload<L>(a.coef2 + ((size_t)b * kWarp + lane) * 2 * L), tt));
   C q;                                                           // running S
   // phase 1
   auto phase1 = [&](int t, uint32_t w1, uint32_t w2) {  // w1 = word_at(t), w2 = word_at(K - t + 1)
@@ -392,6 +402,12 @@ block_kernel(const BlockArgs a) {
   const int64_t p = blockIdx.x / units_per_point;
   const int unit = (int)(blockIdx.x % units_per_point);
   if (p >= a.n_points) return;
+  const bool hom = a.coef2 != nullptr;
+  typename P::real tt = P::one().re, omt = P::one().re;
+  if (hom) {
+    tt = P::rload(a.T + p * L);
+    omt = P::one_minus(tt);
+  }
 
   double* pt;
   double* rows_all;
@@ -450,7 +466,7 @@ block_kernel(const BlockArgs a) {
     C fsum = P::zero();
     const int b_step = mA ? 1 : kBlockWarps;
     for (int b = a.blk[i] + (mA ? 0 : warp); b < a.blk[i + 1]; b += b_step) {
-      C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane);
+      C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane, hom, omt, tt);
       fsum = P::add(fsum, y);
     }
     __syncwarp();
@@ -604,6 +620,7 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
   if (R > 255) return;
   std::vector<uint32_t> fac((size_t)nb * K * kWarp);
   std::vector<double> coef((size_t)nb * kWarp * 2 * L, 0.0);
+  std::vector<int64_t> slot_term((size_t)nb * kWarp, -1);
   for (int64_t b = 0; b < nb; ++b) {
     std::vector<std::vector<std::pair<int, int>>> terms;
     for (int64_t t : bterms[b]) {
@@ -631,6 +648,7 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
             (uint32_t)terms[l][j].first | ((uint32_t)terms[l][j].second << 16) | ((uint32_t)rep[l][j] << 24);
       }
       const int64_t t = bterms[b][l];
+      slot_term[(size_t)b * kWarp + l] = t;
       for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
     }
   }
@@ -656,6 +674,7 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
   plan->fac.swap(fac);
   plan->coeff.swap(coef);
   plan->blk.swap(blk);
+  plan->slot_term.swap(slot_term);
   // operation counts per point (useful work: real terms and factors only)
   int64_t cm = (int64_t)s.n_var * std::max(0, E - 1);
   for (int64_t t = 0; t < s.n_terms; ++t) {
@@ -680,6 +699,17 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
     plan->exec_flops_per_point = fl;
   }
   plan->usable = true;
+}
+
+// NEXT-3: a coefficient table in term order ([n_terms][2][L]) packed like plan.coeff.
+inline std::vector<double> pack_block_coeff(const HostBlockPlan& plan, const std::vector<double>& coeff, int L) {
+  std::vector<double> out(plan.coeff.size(), 0.0);
+  for (size_t q = 0; q < plan.slot_term.size(); ++q) {
+    const int64_t t = plan.slot_term[q];
+    if (t < 0) continue;
+    for (int c = 0; c < 2 * L; ++c) out[q * 2 * L + c] = coeff[(size_t)t * 2 * L + c];
+  }
+  return out;
 }
 
 inline int upload_block_tables(const HostBlockPlan& plan, BlockTables* bt) {
@@ -707,6 +737,7 @@ int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_poin
     b.F = a.F + p0 * a.n_eq * 2 * L;
     b.J = a.J + p0 * (int64_t)a.n_eq * a.n_var * 2 * L;
     if (LAYOUT == 0) b.PTg = a.PTg + p0 * (int64_t)(a.n_var + 1) * 2 * a.E * 2 * L;
+    if (a.T) b.T = a.T + p0 * L;
     b.n_points = np;
     if (LAYOUT == 0) {
       // programmatic dependent launch after block_power_table_kernel (same stream)
@@ -762,10 +793,12 @@ int launch_block_pts(const HostBlockPlan& plan, const BlockArgs& a, int64_t np, 
 // Runs the fused path for n_points points resident on the current device.
 template <int L>
 int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, int64_t n_points, const double* x,
-              double* f, double* jac, cudaStream_t st) {
+              const double* T, double* f, double* jac, cudaStream_t st) {
   BlockArgs a;
   a.fac = bt.fac;
   a.coef = bt.coeff;
+  a.coef2 = T ? bt.coeff2 : nullptr;
+  a.T = T;
   a.blk = bt.blk;
   a.X = x;
   a.PTg = nullptr;
@@ -807,6 +840,7 @@ int run_block(const HostBlockPlan& plan, BlockTables& bt, int n_eq, int n_var, i
     b.F = f + p0 * n_eq * 2 * L;
     b.J = jac + p0 * (int64_t)n_eq * n_var * 2 * L;
     b.PTg = bt.PT;
+    if (T) b.T = T + p0 * L;
     b.n_points = np;
     int rc = launch_block_pts<L, 0>(plan, b, np, st);
     if (rc) return rc;

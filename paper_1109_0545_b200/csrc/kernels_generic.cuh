@@ -44,7 +44,8 @@ __global__ void power_table_kernel(const double* __restrict__ X, int n_var, int 
   }
 }
 
-// Per-term kernel (rows a3-a6), one thread per (point, term).
+// Per-term kernel (rows a3-a6), one thread per (point, term).  With coeff2 != nullptr the
+// coefficient is the homotopy blend at the point's t (NEXT-3).
 // For a term c * prod_{j=1..k} u_j with u_j = x_{i_j}^{a_j}, d_j = a_j x_{i_j}^{a_j - 1}:
 //   suffix  s_q = u_{k-q+1} ... u_k              (q = 1..k-1; the paper's phi)
 //   prefix  r_m = c u_1 ... u_m                  (m = 0..k;   the paper's psi with the
@@ -56,7 +57,8 @@ __global__ void power_table_kernel(const double* __restrict__ X, int n_var, int 
 // Packed factor word: bits 0-15 variable, bits 16-23 exponent.
 template <int L, int MAXK>
 __global__ void term_kernel(const int64_t* __restrict__ term_ptr, const uint32_t* __restrict__ fac,
-                            const double* __restrict__ coeff, const double* __restrict__ PT, int n_var, int E,
+                            const double* __restrict__ coeff, const double* __restrict__ coeff2,
+                            const double* __restrict__ T, const double* __restrict__ PT, int n_var, int E,
                             int64_t n_terms, int64_t n_factors, int64_t n_points, double* __restrict__ Y,
                             double* __restrict__ G) {
   using P = Prec<L>;
@@ -68,6 +70,10 @@ __global__ void term_kernel(const int64_t* __restrict__ term_ptr, const uint32_t
   const int64_t f0 = term_ptr[t];
   const int k = (int)(term_ptr[t + 1] - f0);
   C r = cload<L>(coeff + t * 2 * L);
+  if (coeff2) {  // NEXT-3 homotopy: c(t) = (1 - t) c_start + t c_target (reading H1)
+    const typename P::real tt = P::rload(T + p * L);
+    r = P::add(P::mul_real(r, P::one_minus(tt)), P::mul_real(cload<L>(coeff2 + t * 2 * L), tt));
+  }
   auto U = [&](uint32_t w) { return cload<L>(pt + ((int64_t)(w & 0xffffu) * 2 * E + ((w >> 16) & 0xffu) - 1) * 2 * L); };
   auto Dd = [&](uint32_t w) { return cload<L>(pt + ((int64_t)(w & 0xffffu) * 2 * E + E + ((w >> 16) & 0xffu) - 1) * 2 * L); };
   C s[MAXK];

@@ -72,6 +72,7 @@ struct DeviceState {
   int64_t* term_ptr = nullptr;
   uint32_t* fac = nullptr;
   double* coeff = nullptr;
+  double* coeff2 = nullptr;  // NEXT-3 homotopy target coefficients (term order)
   int64_t* poly_ptr = nullptr;
   int64_t* jptr = nullptr;
   int64_t* jidx = nullptr;
@@ -92,12 +93,13 @@ struct DeviceState {
   double* xs = nullptr;
   double* fs = nullptr;
   double* js = nullptr;
+  double* ts = nullptr;  // t per point (homotopy shards)
   int64_t stage_cap = 0;
   ~DeviceState() {
     DeviceGuard g(dev);
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
-                    (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)bt.fac, (void*)bt.coeff,
-                    (void*)bt.blk, (void*)bt.PT})
+                    (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
+                    (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (done) cudaEventDestroy(done);
@@ -116,6 +118,7 @@ struct phc_system {
   std::vector<int64_t> poly_ptr, term_ptr;
   std::vector<uint32_t> fac;
   std::vector<double> coeff;
+  std::vector<double> coeff2;  // NEXT-3: homotopy target coefficients (empty: not a homotopy)
   std::vector<int64_t> jptr, jidx;
   phc::HostBlockPlan plan;  // warp-per-block layout (kernels_block.cuh)
   std::mutex mu;
@@ -173,6 +176,21 @@ int upload(void* dst, const void* src, size_t bytes) {
   return PHC_OK;
 }
 
+// NEXT-3: the target coefficients on one device (term order for the generic path, packed for
+// the block path).
+int upload_target(const phc_system* s, DeviceState* d) {
+  DeviceGuard g(d->dev);
+  int rc;
+  if (!d->coeff2 && (rc = dalloc(&d->coeff2, s->coeff2.size()))) return rc;
+  if ((rc = upload(d->coeff2, s->coeff2.data(), s->coeff2.size() * 8))) return rc;
+  if (s->plan.usable) {
+    const std::vector<double> packed = phc::pack_block_coeff(s->plan, s->coeff2, s->L);
+    if (!d->bt.coeff2 && (rc = dalloc(&d->bt.coeff2, std::max<size_t>(1, packed.size())))) return rc;
+    if ((rc = upload(d->bt.coeff2, packed.data(), packed.size() * 8))) return rc;
+  }
+  return PHC_OK;
+}
+
 int get_device_state(phc_system* s, int dev, DeviceState** out) {
   std::lock_guard<std::mutex> lk(s->mu);
   auto it = s->devs.find(dev);
@@ -202,6 +220,7 @@ int get_device_state(phc_system* s, int dev, DeviceState** out) {
     if ((rc = phc::upload_block_tables(s->plan, &d->bt))) return fail(rc, "block table upload failed");
     d->have_block = true;
   }
+  if (!s->coeff2.empty() && (rc = upload_target(s, d.get()))) return rc;
   *out = d.get();
   s->devs[dev] = std::move(d);
   return PHC_OK;
@@ -230,16 +249,16 @@ int ensure_scratch(const phc_system* s, DeviceState* d, int64_t want_points) {
 }
 
 template <int L, int MAXK>
-void launch_term(const phc_system* s, DeviceState* d, int64_t np, cudaStream_t st) {
+void launch_term(const phc_system* s, DeviceState* d, int64_t np, const double* T, cudaStream_t st) {
   dim3 grid((unsigned)((s->n_terms + 127) / 128), (unsigned)np);
   ProfScope ps(s, d->dev, 1, st);
-  phc::term_kernel<L, MAXK><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, d->PT, s->n_var, s->E, s->n_terms,
-                                                  s->n_factors, np, d->Y, d->G);
+  phc::term_kernel<L, MAXK><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, T ? d->coeff2 : nullptr, T, d->PT,
+                                                  s->n_var, s->E, s->n_terms, s->n_factors, np, d->Y, d->G);
 }
 
 template <int L>
-int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
-                cudaStream_t st) {
+int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
+                double* jac, cudaStream_t st) {
   int rc = ensure_scratch(s, d, n_points);
   if (rc) return rc;
   const int64_t cd = 2 * L;
@@ -251,14 +270,15 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
     phc::power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * s->n_var * cd, s->n_var, s->E,
                                                                               np, d->PT);
     }
+    const double* Tc = T ? T + p0 * L : nullptr;
     if (s->kmax <= 8)
-      launch_term<L, 8>(s, d, np, st);
+      launch_term<L, 8>(s, d, np, Tc, st);
     else if (s->kmax <= 16)
-      launch_term<L, 16>(s, d, np, st);
+      launch_term<L, 16>(s, d, np, Tc, st);
     else if (s->kmax <= 32)
-      launch_term<L, 32>(s, d, np, st);
+      launch_term<L, 32>(s, d, np, Tc, st);
     else
-      launch_term<L, PHC_MAX_K>(s, d, np, st);
+      launch_term<L, PHC_MAX_K>(s, d, np, Tc, st);
     const int64_t ne = (int64_t)s->n_eq * s->n_var + s->n_eq;
     dim3 grid((unsigned)((ne + 127) / 128), (unsigned)np);
     ProfScope ps(s, d->dev, 2, st);
@@ -270,18 +290,19 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
   return PHC_OK;
 }
 
-// Evaluate n_points points resident on device d, on stream st.
-int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
-                  cudaStream_t st) {
+// Evaluate n_points points resident on device d, on stream st.  T (t per point, device d)
+// selects the homotopy coefficients (NEXT-3); nullptr evaluates the system's own coefficients.
+int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
+                  double* jac, cudaStream_t st) {
   if (n_points <= 0) return PHC_OK;
   if (d->have_block) {
     ProfScope ps(s, d->dev, 3, st);
-    int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, f, jac, st)
-                       : phc::run_block<4>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, f, jac, st);
+    int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, T, f, jac, st)
+                       : phc::run_block<4>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, T, f, jac, st);
     if (rc) return fail(PHC_ECUDA, "block kernel launch failed: %s", cudaGetErrorString(cudaGetLastError()));
     return PHC_OK;
   }
-  return s->L == 2 ? run_generic<2>(s, d, n_points, x, f, jac, st) : run_generic<4>(s, d, n_points, x, f, jac, st);
+  return s->L == 2 ? run_generic<2>(s, d, n_points, x, T, f, jac, st) : run_generic<4>(s, d, n_points, x, T, f, jac, st);
 }
 
 int ensure_stage(const phc_system* s, DeviceState* d, int64_t np) {
@@ -291,10 +312,12 @@ int ensure_stage(const phc_system* s, DeviceState* d, int64_t np) {
   if (d->xs) cudaFree(d->xs);
   if (d->fs) cudaFree(d->fs);
   if (d->js) cudaFree(d->js);
-  d->xs = d->fs = d->js = nullptr;
+  if (d->ts) cudaFree(d->ts);
+  d->xs = d->fs = d->js = d->ts = nullptr;
   d->stage_cap = 0;
   const int64_t cd = 2 * s->L;
   int rc;
+  if ((rc = dalloc(&d->ts, (size_t)(np * s->L)))) return rc;
   if ((rc = dalloc(&d->xs, (size_t)(np * s->n_var * cd)))) return rc;
   if ((rc = dalloc(&d->fs, (size_t)(np * s->n_eq * cd)))) return rc;
   if ((rc = dalloc(&d->js, (size_t)(np * (int64_t)s->n_eq * s->n_var * cd)))) return rc;
@@ -418,8 +441,9 @@ void phc_system_destroy(phc_system* s) {
   delete s;
 }
 
-int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double* x, double* f, double* jac,
-                            const int32_t* devices, int32_t n_devices, void* stream) {
+// Shared body of the batch calls: T = t per point [n_points][L] (homotopy) or nullptr.
+static int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* f,
+                           double* jac, const int32_t* devices, int32_t n_devices, void* stream) {
   g_err.clear();
   phc_system* s = const_cast<phc_system*>(cs);
   if (!s) return fail(PHC_EINVAL, "NULL system");
@@ -444,7 +468,7 @@ int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double
     DeviceState* d;
     int rc = get_device_state(s, s->home, &d);
     if (rc) return rc;
-    return run_on_device(s, d, n_points, x, f, jac, st);
+    return run_on_device(s, d, n_points, x, T, f, jac, st);
   }
   // sharded: contiguous equal ranges [g P / G, (g+1) P / G)
   cudaEvent_t start;
@@ -460,7 +484,7 @@ int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double
     DeviceState* d;
     if ((rc = get_device_state(s, dv, &d))) break;
     if (dv == s->home) {
-      rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, f + p0 * s->n_eq * cd,
+      rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
                          jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st);
       continue;
     }
@@ -477,7 +501,11 @@ int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double
       rc = fail(PHC_ECUDA, "scatter copy failed");
       break;
     }
-    if ((rc = run_on_device(s, d, np, d->xs, d->fs, d->js, d->stream))) break;
+    if (T && cudaMemcpyPeerAsync(d->ts, dv, T + p0 * s->L, s->home, np * s->L * 8, d->stream) != cudaSuccess) {
+      rc = fail(PHC_ECUDA, "scatter copy (t) failed");
+      break;
+    }
+    if ((rc = run_on_device(s, d, np, d->xs, T ? d->ts : nullptr, d->fs, d->js, d->stream))) break;
     if (cudaMemcpyPeerAsync(f + p0 * s->n_eq * cd, s->home, d->fs, dv, np * s->n_eq * cd * 8, d->stream) != cudaSuccess ||
         cudaMemcpyPeerAsync(jac + p0 * (int64_t)s->n_eq * s->n_var * cd, s->home, d->js, dv,
                             np * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream) != cudaSuccess) {
@@ -497,8 +525,22 @@ int phc_eval_jacobian_batch(const phc_system* cs, int64_t n_points, const double
   return rc;
 }
 
-int phc_newton_step_batch(const phc_system* cs, int64_t n_points, const double* x, double* x_new, double* residual,
-                          int32_t* status, void* stream) {
+int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double* x, double* f, double* jac,
+                            const int32_t* devices, int32_t n_devices, void* stream) {
+  return eval_batch_impl(s, n_points, x, nullptr, f, jac, devices, n_devices, stream);
+}
+
+int phc_eval_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t, double* f,
+                            double* jac, const int32_t* devices, int32_t n_devices, void* stream) {
+  g_err.clear();
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (s->coeff2.empty()) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
+  return eval_batch_impl(s, n_points, x, t, f, jac, devices, n_devices, stream);
+}
+
+static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* x_new,
+                       double* residual, int32_t* status, void* stream) {
   g_err.clear();
   phc_system* s = const_cast<phc_system*>(cs);
   if (!s) return fail(PHC_EINVAL, "NULL system");
@@ -533,7 +575,7 @@ int phc_newton_step_batch(const phc_system* cs, int64_t n_points, const double* 
   const int threads = n <= 48 ? 128 : 256;
   for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
     const int64_t np = std::min(chunk, n_points - p0);
-    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, d->nF, d->nJ, st))) return rc;
+    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, T ? T + p0 * L : nullptr, d->nF, d->nJ, st))) return rc;
     phc::NewtonArgs a;
     a.X = x + p0 * n * cd;
     a.F = d->nF;
@@ -563,6 +605,86 @@ int phc_newton_step_batch(const phc_system* cs, int64_t n_points, const double* 
     CUDA_TRY(cudaGetLastError());
   }
   return PHC_OK;
+}
+
+int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x, double* x_new, double* residual,
+                          int32_t* status, void* stream) {
+  return newton_impl(s, n_points, x, nullptr, x_new, residual, status, stream);
+}
+
+int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t,
+                                   double* x_new, double* residual, int32_t* status, void* stream) {
+  g_err.clear();
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (s->coeff2.empty()) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
+  return newton_impl(s, n_points, x, t, x_new, residual, status, stream);
+}
+
+int phc_system_set_target(phc_system* s, const double* coeff_target) {
+  g_err.clear();
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (s->n_terms > 0 && !coeff_target) return fail(PHC_EINVAL, "NULL coeff_target");
+  const size_t nc = (size_t)s->n_terms * 2 * s->L;
+  for (size_t q = 0; q < nc; ++q)
+    if (!std::isfinite(coeff_target[q])) return fail(PHC_EINVAL, "target coefficient limb %zu is not finite", q);
+  {
+    DeviceGuard g(s->home);
+    cudaDeviceSynchronize();  // no evaluation may be reading the previous target
+  }
+  s->coeff2.assign(coeff_target, coeff_target + nc);
+  if (nc == 0) s->coeff2.assign(1, 0.0);  // a homotopy without terms: keep the flag
+  std::lock_guard<std::mutex> lk(s->mu);
+  for (auto& kv : s->devs) {
+    int rc = upload_target(s, kv.second.get());
+    if (rc) return rc;
+  }
+  return PHC_OK;
+}
+
+int phc_homotopy_old_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_terms,
+                            const int64_t* poly_ptr, const int64_t* term_ptr, const int32_t* var_idx,
+                            const int32_t* exponent, const double* coeff_start, const double* coeff_target,
+                            int32_t device) {
+  g_err.clear();
+  if (!out) return fail(PHC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_eq < 1 || n_var < 1 || n_terms < 0 || !poly_ptr || !term_ptr) return fail(PHC_EINVAL, "malformed input");
+  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 or 4");
+  if (n_terms > 0 && (!coeff_start || !coeff_target)) return fail(PHC_EINVAL, "NULL coefficients");
+  if (n_terms > 0 && term_ptr[n_terms] > 0 && (!var_idx || !exponent)) return fail(PHC_EINVAL, "NULL var_idx/exponent");
+  if (poly_ptr[0] != 0 || poly_ptr[n_eq] != n_terms || term_ptr[0] != 0)
+    return fail(PHC_EINVAL, "poly_ptr/term_ptr must start at 0 and poly_ptr end at n_terms");
+  for (int i = 0; i < n_eq; ++i)
+    if (poly_ptr[i + 1] < poly_ptr[i]) return fail(PHC_EINVAL, "poly_ptr not monotone at %d", i);
+  for (int64_t t = 0; t < n_terms; ++t)
+    if (term_ptr[t + 1] < term_ptr[t]) return fail(PHC_EINVAL, "term_ptr not monotone at %lld", (long long)t);
+  // each term c x^a of h = (1 - t) c_s x^a + t c_f x^a becomes c_s x^a, -c_s t x^a, c_f t x^a,
+  // with t the variable n_var ("t treated as just another variable")
+  const int cd = 2 * limbs;
+  std::vector<int64_t> pp(1, 0), tp(1, 0);
+  std::vector<int32_t> vi, ex;
+  std::vector<double> cf;
+  for (int i = 0; i < n_eq; ++i) {
+    for (int64_t t = poly_ptr[i]; t < poly_ptr[i + 1]; ++t) {
+      for (int copy = 0; copy < 3; ++copy) {
+        for (int64_t q = term_ptr[t]; q < term_ptr[t + 1]; ++q) {
+          vi.push_back(var_idx ? var_idx[q] : 0);
+          ex.push_back(exponent ? exponent[q] : 0);
+        }
+        if (copy > 0) {
+          vi.push_back(n_var);
+          ex.push_back(1);
+        }
+        tp.push_back((int64_t)vi.size());
+        const double* c = (copy == 2 ? coeff_target : coeff_start) + t * cd;
+        for (int j = 0; j < cd; ++j) cf.push_back(copy == 1 ? -c[j] : c[j]);
+      }
+    }
+    pp.push_back((int64_t)tp.size() - 1);
+  }
+  return phc_system_create(out, n_eq, n_var + 1, limbs, (int64_t)tp.size() - 1, pp.data(), tp.data(), vi.data(),
+                           ex.data(), cf.data(), device);
 }
 
 int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* jac, void* stream) {

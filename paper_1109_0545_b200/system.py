@@ -16,7 +16,10 @@ class System:
     """A system handle: ``System(arrays, device=0)`` with ``arrays`` having the attributes
     n_eq, n_var, limbs, poly_ptr, term_ptr, var_idx, exponent, coeff (include/phc.h layout)."""
 
-    def __init__(self, arrays, device: int = 0):
+    def __init__(self, arrays, device: int = 0, coeff_target=None, old_homotopy: bool = False):
+        """``coeff_target`` [n_terms][2][L] attaches homotopy target coefficients (NEXT-3,
+        phc_system_set_target).  ``old_homotopy=True`` instead builds the paper's "old"
+        t-as-variable system (phc_homotopy_old_create): n_var + 1 variables, t last."""
         self.n_eq = int(arrays.n_eq)
         self.n_var = int(arrays.n_var)
         self.limbs = int(arrays.limbs)
@@ -28,8 +31,25 @@ class System:
         cf = np.ascontiguousarray(arrays.coeff, dtype=np.float64)
         self.n_terms = int(tp.shape[0] - 1)
         self._h = None
+        self.homotopy = False
+        if old_homotopy:
+            ct = np.ascontiguousarray(coeff_target, dtype=np.float64)
+            self._h = _lib.phc_homotopy_old_create(self.n_eq, self.n_var, self.limbs, self.n_terms, _ptr(pp),
+                                                   _ptr(tp), _ptr(vi), _ptr(ex), _ptr(cf), _ptr(ct), self.device)
+            self.n_var += 1
+            self.n_terms *= 3
+            return
         self._h = _lib.phc_system_create(self.n_eq, self.n_var, self.limbs, self.n_terms, _ptr(pp), _ptr(tp),
                                          _ptr(vi), _ptr(ex), _ptr(cf), self.device)
+        if coeff_target is not None:
+            self.set_target(coeff_target)
+
+    def set_target(self, coeff_target):
+        ct = np.ascontiguousarray(coeff_target, dtype=np.float64)
+        if ct.shape != (self.n_terms, 2, self.limbs):
+            raise ValueError(f"coeff_target must have shape {(self.n_terms, 2, self.limbs)}")
+        _lib.phc_system_set_target(self._h, _ptr(ct))
+        self.homotopy = True
 
     def close(self):
         if self._h is not None:
@@ -104,6 +124,45 @@ class System:
         status = torch.empty(P, dtype=torch.int32, device=X.device)
         st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
         _lib.phc_newton_step_batch(self._h, P, _ptr(X), _ptr(X_new), _ptr(res), _ptr(status), ctypes.c_void_p(st))
+        return X_new, res, status
+
+    def eval_homotopy_batch(self, X, T, F=None, J=None, devices=None, stream=None):
+        """h(., t_p) at X [P, n_var, 2, L] with T [P, L] (real t limbs), both on the home
+        device -> (F, J) as eval_batch (NEXT-3)."""
+        import torch
+
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        self._check(T, (P, L))
+        if F is None:
+            F = torch.empty((P, self.n_eq, 2, L), dtype=torch.float64, device=X.device)
+        if J is None:
+            J = torch.empty((P, self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=X.device)
+        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        if devices:
+            dv = (ctypes.c_int32 * len(devices))(*devices)
+            nd = len(devices)
+        else:
+            dv, nd = None, 0
+        _lib.phc_eval_homotopy_batch(self._h, P, _ptr(X), _ptr(T), _ptr(F), _ptr(J), dv, nd, ctypes.c_void_p(st))
+        return F, J
+
+    def newton_step_homotopy(self, X, T, X_new=None, stream=None):
+        """One Newton iteration on h(., t_p) = 0 per point: X [P, n, 2, L], T [P, L]."""
+        import torch
+
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        self._check(T, (P, L))
+        if X_new is None:
+            X_new = torch.empty_like(X)
+        res = torch.empty(P, dtype=torch.float64, device=X.device)
+        status = torch.empty(P, dtype=torch.int32, device=X.device)
+        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        _lib.phc_newton_step_homotopy_batch(self._h, P, _ptr(X), _ptr(T), _ptr(X_new), _ptr(res), _ptr(status),
+                                            ctypes.c_void_p(st))
         return X_new, res, status
 
     def eval_batch_host(self, X, F=None, J=None, devices=None):
