@@ -115,6 +115,23 @@ int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x
                           int32_t* status, void* stream);
 
 /* ---------------------------------------------------------------------------------------
+ * NEXT-2: common-support systems and the paper's two-stage evaluation
+ * (Alg. 2: "V := Monomial_Evaluation", then "Y := Coefficient_Product", PAPER.md P:269-284,
+ * P:329-333; Table 1's "system of 40 variables with a common support of 200 monomials",
+ * P:355-358).  Every polynomial uses the same n_mono monomials:
+ *     f_i(x) = sum_{j < n_mono} coeff[i][j] * x^{a_j}.
+ *   mono_ptr [n_mono+1]  CSR over factors of monomial j (mono_ptr[0] = 0, non-decreasing)
+ *   var_idx, exponent    as in phc_system_create (strictly increasing indices, a >= 1)
+ *   coeff    [n_eq][n_mono][2][limbs]  dense coefficient matrix C (HOST pointer, copied)
+ * The handle works with phc_eval_jacobian[_batch][_host] and phc_newton_step_batch (same
+ * layouts and semantics).  Each monomial and its partials are evaluated once per point,
+ * then [F | J] = C [V | D] (D: the partials, sparse).  Homotopy coefficients are not
+ * supported on these handles (PHC_EUNSUPPORTED). */
+int phc_system_create_common(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_mono,
+                             const int64_t* mono_ptr, const int32_t* var_idx, const int32_t* exponent,
+                             const double* coeff, int32_t device);
+
+/* ---------------------------------------------------------------------------------------
  * NEXT-3: homotopy coefficients.  PAPER.md §7 P:647-649 (Table 6,
  * P:651-668): the "new" evaluator handles the continuation parameter t through the
  * coefficients, the "old" one treats t "as just another variable".  With start

@@ -19,6 +19,7 @@ from ._lib import (  # noqa: F401
     phc_newton_step_homotopy_batch,
     phc_eval_homotopy_batch,
     phc_system_set_target,
+    phc_system_create_common,
     phc_homotopy_old_create,
     phc_profile_enable,
     phc_profile_read,

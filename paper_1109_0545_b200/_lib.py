@@ -28,6 +28,7 @@ EXPORTED = (
     "phc_eval_jacobian_batch_host",
     "phc_newton_step_batch",
     "phc_system_set_target",
+    "phc_system_create_common",
     "phc_eval_homotopy_batch",
     "phc_newton_step_homotopy_batch",
     "phc_homotopy_old_create",
@@ -66,6 +67,8 @@ def _load():
     lib.phc_eval_jacobian_batch_host.restype = ctypes.c_int
     lib.phc_newton_step_batch.argtypes = [P, i64, P, P, P, P, P]
     lib.phc_newton_step_batch.restype = ctypes.c_int
+    lib.phc_system_create_common.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, i32]
+    lib.phc_system_create_common.restype = ctypes.c_int
     lib.phc_system_set_target.argtypes = [P, P]
     lib.phc_system_set_target.restype = ctypes.c_int
     lib.phc_eval_homotopy_batch.argtypes = [P, i64, P, P, P, P, P, i32, P]
@@ -125,6 +128,13 @@ def phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices):
 
 def phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream):
     return check(lib.phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream))
+
+
+def phc_system_create_common(n_eq, n_var, limbs, n_mono, mono_ptr, var_idx, exponent, coeff, device):
+    h = ctypes.c_void_p()
+    check(lib.phc_system_create_common(ctypes.byref(h), n_eq, n_var, limbs, n_mono, mono_ptr, var_idx, exponent,
+                                       coeff, device))
+    return h
 
 
 def phc_system_set_target(h, coeff_target):

@@ -18,6 +18,7 @@
 #include "kernels_generic.cuh"
 #include "kernels_block.cuh"
 #include "kernels_newton.cuh"
+#include "kernels_common.cuh"
 
 namespace {
 
@@ -76,6 +77,11 @@ struct DeviceState {
   int64_t* poly_ptr = nullptr;
   int64_t* jptr = nullptr;
   int64_t* jidx = nullptr;
+  // common-support tables (NEXT-2): column lists and C transposed
+  int64_t* cl_ptr = nullptr;
+  int32_t* cl_j = nullptr;
+  int64_t* cl_q = nullptr;
+  double* cT = nullptr;
   // block path tables
   phc::BlockTables bt{};
   bool have_block = false;
@@ -99,7 +105,8 @@ struct DeviceState {
     DeviceGuard g(dev);
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
-                    (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2})
+                    (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
+                    (void*)cl_q, (void*)cT})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (done) cudaEventDestroy(done);
@@ -119,6 +126,12 @@ struct phc_system {
   std::vector<uint32_t> fac;
   std::vector<double> coeff;
   std::vector<double> coeff2;  // NEXT-3: homotopy target coefficients (empty: not a homotopy)
+  // NEXT-2 common-support system: "terms" are the M shared monomials (unit coefficients),
+  // C^T [M][n_eq][2][L] and the per-column lists of the coefficient product
+  bool common = false;
+  std::vector<int64_t> cl_ptr, cl_q;
+  std::vector<int32_t> cl_j;
+  std::vector<double> cT;
   std::vector<int64_t> jptr, jidx;
   phc::HostBlockPlan plan;  // warp-per-block layout (kernels_block.cuh)
   std::mutex mu;
@@ -221,6 +234,16 @@ int get_device_state(phc_system* s, int dev, DeviceState** out) {
     d->have_block = true;
   }
   if (!s->coeff2.empty() && (rc = upload_target(s, d.get()))) return rc;
+  if (s->common) {
+    if ((rc = dalloc(&d->cl_ptr, s->cl_ptr.size()))) return rc;
+    if ((rc = dalloc(&d->cl_j, s->cl_j.size()))) return rc;
+    if ((rc = dalloc(&d->cl_q, s->cl_q.size()))) return rc;
+    if ((rc = dalloc(&d->cT, s->cT.size()))) return rc;
+    if ((rc = upload(d->cl_ptr, s->cl_ptr.data(), s->cl_ptr.size() * 8))) return rc;
+    if ((rc = upload(d->cl_j, s->cl_j.data(), s->cl_j.size() * 4))) return rc;
+    if ((rc = upload(d->cl_q, s->cl_q.data(), s->cl_q.size() * 8))) return rc;
+    if ((rc = upload(d->cT, s->cT.data(), s->cT.size() * 8))) return rc;
+  }
   *out = d.get();
   s->devs[dev] = std::move(d);
   return PHC_OK;
@@ -290,11 +313,51 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
   return PHC_OK;
 }
 
+// NEXT-2 two-stage path: power table, monomial stage V (the term kernel with unit
+// coefficients), coefficient product Y = C [V | D].
+template <int L>
+int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
+               cudaStream_t st) {
+  int rc = ensure_scratch(s, d, n_points);
+  if (rc) return rc;
+  const int64_t cd = 2 * L;
+  constexpr int TI = L == 2 ? 8 : 4;
+  for (int64_t p0 = 0; p0 < n_points; p0 += d->chunk_cap) {
+    const int64_t np = std::min(d->chunk_cap, n_points - p0);
+    const int64_t nth = np * (s->n_var + 1);
+    {
+      ProfScope ps(s, d->dev, 0, st);
+      phc::power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * s->n_var * cd, s->n_var,
+                                                                                s->E, np, d->PT);
+    }
+    if (s->kmax <= 8)
+      launch_term<L, 8>(s, d, np, nullptr, st);
+    else if (s->kmax <= 16)
+      launch_term<L, 16>(s, d, np, nullptr, st);
+    else if (s->kmax <= 32)
+      launch_term<L, 32>(s, d, np, nullptr, st);
+    else
+      launch_term<L, PHC_MAX_K>(s, d, np, nullptr, st);
+    const int64_t tiles = (s->n_eq + TI - 1) / TI;
+    const int64_t nthr = np * (s->n_var + 1) * tiles;
+    ProfScope ps(s, d->dev, 2, st);
+    phc::coef_product_kernel<L, TI><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(
+        d->cl_ptr, d->cl_j, d->cl_q, d->cT, d->Y, d->G, s->n_eq, s->n_var, s->n_terms, s->n_factors, np,
+        f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+    CUDA_TRY(cudaGetLastError());
+  }
+  return PHC_OK;
+}
+
 // Evaluate n_points points resident on device d, on stream st.  T (t per point, device d)
 // selects the homotopy coefficients (NEXT-3); nullptr evaluates the system's own coefficients.
 int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
                   double* jac, cudaStream_t st) {
   if (n_points <= 0) return PHC_OK;
+  if (s->common) {
+    if (T) return fail(PHC_EUNSUPPORTED, "homotopy coefficients are not supported on common-support systems");
+    return s->L == 2 ? run_common<2>(s, d, n_points, x, f, jac, st) : run_common<4>(s, d, n_points, x, f, jac, st);
+  }
   if (d->have_block) {
     ProfScope ps(s, d->dev, 3, st);
     int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, T, f, jac, st)
@@ -420,6 +483,86 @@ int phc_system_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t lim
   int rc = get_device_state(s.get(), device, &d);
   if (rc) return rc;
   *out = s.release();
+  return PHC_OK;
+}
+
+int phc_system_create_common(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_mono,
+                             const int64_t* mono_ptr, const int32_t* var_idx, const int32_t* exponent,
+                             const double* coeff, int32_t device) {
+  g_err.clear();
+  if (!out) return fail(PHC_EINVAL, "out is NULL");
+  *out = nullptr;
+  if (n_eq < 1 || n_var < 1) return fail(PHC_EINVAL, "n_eq and n_var must be >= 1 (got %d, %d)", n_eq, n_var);
+  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 (DD) or 4 (QD), got %d", limbs);
+  if (n_mono < 1) return fail(PHC_EINVAL, "n_mono must be >= 1");
+  if (n_mono > INT32_MAX) return fail(PHC_EUNSUPPORTED, "n_mono too large");
+  if (!mono_ptr || !coeff) return fail(PHC_EINVAL, "NULL array");
+  const size_t nc = (size_t)n_eq * n_mono * 2 * limbs;
+  for (size_t q = 0; q < nc; ++q)
+    if (!std::isfinite(coeff[q])) return fail(PHC_EINVAL, "coefficient limb %zu is not finite", q);
+  // the monomials as a one-polynomial system with unit coefficients: validation, packing and
+  // the monomial stage are those of an ordinary system (phc_system_create)
+  std::vector<int64_t> pp(n_eq + 1, 0);
+  pp[0] = 0;
+  for (int i = 1; i <= n_eq; ++i) pp[i] = n_mono;  // polynomial 0 owns every monomial
+  std::vector<double> ones((size_t)n_mono * 2 * limbs, 0.0);
+  for (int64_t j = 0; j < n_mono; ++j) ones[(size_t)j * 2 * limbs] = 1.0;
+  phc_system* s = nullptr;
+  int rc = phc_system_create(&s, n_eq, n_var, limbs, n_mono, pp.data(), mono_ptr, var_idx, exponent, ones.data(),
+                             device);
+  if (rc) return rc;
+  s->common = true;
+  s->plan = phc::HostBlockPlan();  // the fused per-polynomial path does not apply
+  {
+    std::lock_guard<std::mutex> lk(s->mu);
+    for (auto& kv : s->devs) kv.second->have_block = false;
+  }
+  // C^T [M][n_eq][2][L]
+  const int cd = 2 * limbs;
+  s->cT.resize(nc);
+  for (int i = 0; i < n_eq; ++i)
+    for (int64_t j = 0; j < n_mono; ++j)
+      for (int c = 0; c < cd; ++c) s->cT[((size_t)j * n_eq + i) * cd + c] = coeff[((size_t)i * n_mono + j) * cd + c];
+  // column lists: c = 0 every monomial (F), c = v + 1 the factor slots on variable v (J)
+  std::vector<std::vector<std::pair<int32_t, int64_t>>> cols(n_var + 1);
+  for (int64_t j = 0; j < n_mono; ++j) {
+    cols[0].push_back({(int32_t)j, -1});
+    for (int64_t q = mono_ptr[j]; q < mono_ptr[j + 1]; ++q) cols[var_idx[q] + 1].push_back({(int32_t)j, q});
+  }
+  s->cl_ptr.assign(1, 0);
+  for (auto& c : cols) {
+    for (auto& e : c) {
+      s->cl_j.push_back(e.first);
+      s->cl_q.push_back(e.second);
+    }
+    s->cl_ptr.push_back((int64_t)s->cl_j.size());
+  }
+  // counts: monomial stage (4k - 3 CM per monomial, power table) + coefficient product
+  int64_t nz_vars = 0;
+  for (int v = 0; v < n_var; ++v) nz_vars += cols[v + 1].empty() ? 0 : 1;
+  s->nnz = (int64_t)n_eq * nz_vars;
+  const int64_t cma = (int64_t)n_eq * (n_mono + s->n_factors);
+  s->cm_per_point += cma;
+  s->ca_per_point = cma;
+  DeviceState* d;
+  if ((rc = get_device_state(s, s->home, &d))) {
+    phc_system_destroy(s);
+    return rc;
+  }
+  // the home replica was made before the common tables existed: add them now
+  {
+    DeviceGuard g(s->home);
+    if ((rc = dalloc(&d->cl_ptr, s->cl_ptr.size())) || (rc = dalloc(&d->cl_j, s->cl_j.size())) ||
+        (rc = dalloc(&d->cl_q, s->cl_q.size())) || (rc = dalloc(&d->cT, s->cT.size())) ||
+        (rc = upload(d->cl_ptr, s->cl_ptr.data(), s->cl_ptr.size() * 8)) ||
+        (rc = upload(d->cl_j, s->cl_j.data(), s->cl_j.size() * 4)) ||
+        (rc = upload(d->cl_q, s->cl_q.data(), s->cl_q.size() * 8)) ||
+        (rc = upload(d->cT, s->cT.data(), s->cT.size() * 8))) {
+      phc_system_destroy(s);
+      return rc;
+    }
+  }
+  *out = s;
   return PHC_OK;
 }
 
@@ -624,6 +767,7 @@ int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const 
 int phc_system_set_target(phc_system* s, const double* coeff_target) {
   g_err.clear();
   if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (s->common) return fail(PHC_EUNSUPPORTED, "homotopy coefficients are not supported on common-support systems");
   if (s->n_terms > 0 && !coeff_target) return fail(PHC_EINVAL, "NULL coeff_target");
   const size_t nc = (size_t)s->n_terms * 2 * s->L;
   for (size_t q = 0; q < nc; ++q)
@@ -763,9 +907,14 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
   out[4] = s->nnz;
   out[5] = s->plan.usable ? s->plan.cm_per_point : s->cm_per_point;
   out[6] = s->ca_per_point;
-  out[7] = s->plan.usable ? s->plan.launches : 3;
+  out[7] = s->plan.usable ? s->plan.launches : 3;  // generic and common paths: 3 kernels
   if (s->plan.usable) {
     out[8] = s->plan.exec_flops_per_point;
+  } else if (s->common) {
+    const phc::OpFlops f = phc::op_flops(s->L);
+    const int64_t mono_cm = s->cm_per_point - s->ca_per_point;  // monomial stage + power table products
+    out[8] = mono_cm * f.cm + (int64_t)s->n_var * std::max(0, s->E - 1) * f.ci + s->ca_per_point * (f.cm_lazy + f.ca_lazy) +
+             (int64_t)s->n_eq * (s->n_var + 1) * f.norm;
   } else {
     const phc::OpFlops f = phc::op_flops(s->L);
     out[8] = s->cm_per_point * f.cm + s->ca_per_point * f.ca + (int64_t)s->n_var * std::max(0, s->E - 1) * f.ci;

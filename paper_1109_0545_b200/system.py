@@ -24,14 +24,21 @@ class System:
         self.n_var = int(arrays.n_var)
         self.limbs = int(arrays.limbs)
         self.device = int(device)
-        pp = np.ascontiguousarray(arrays.poly_ptr, dtype=np.int64)
-        tp = np.ascontiguousarray(arrays.term_ptr, dtype=np.int64)
+        pp = np.ascontiguousarray(getattr(arrays, "poly_ptr", np.zeros(1)), dtype=np.int64)
+        tp = np.ascontiguousarray(getattr(arrays, "term_ptr", getattr(arrays, "mono_ptr", None)), dtype=np.int64)
         vi = np.ascontiguousarray(arrays.var_idx, dtype=np.int32)
         ex = np.ascontiguousarray(arrays.exponent, dtype=np.int32)
         cf = np.ascontiguousarray(arrays.coeff, dtype=np.float64)
         self.n_terms = int(tp.shape[0] - 1)
         self._h = None
         self.homotopy = False
+        if hasattr(arrays, "mono_ptr"):
+            # NEXT-2 common-support system: arrays.coeff is the dense [n_eq][n_mono][2][L] matrix
+            mp = np.ascontiguousarray(arrays.mono_ptr, dtype=np.int64)
+            self.n_terms = int(mp.shape[0] - 1)
+            self._h = _lib.phc_system_create_common(self.n_eq, self.n_var, self.limbs, self.n_terms, _ptr(mp),
+                                                    _ptr(vi), _ptr(ex), _ptr(cf), self.device)
+            return
         if old_homotopy:
             ct = np.ascontiguousarray(coeff_target, dtype=np.float64)
             self._h = _lib.phc_homotopy_old_create(self.n_eq, self.n_var, self.limbs, self.n_terms, _ptr(pp),

@@ -20,4 +20,9 @@ from .systems import (  # noqa: F401
     homotopy_target,
     real_limbs,
     random_t,
+    CommonArrays,
+    common_support_system,
+    expand_common,
+    COMMON_CONFIGS,
+    common_config,
 )

@@ -320,3 +320,73 @@ def random_t(P, limbs, seed) -> np.ndarray:
         u >>= (((bits + 31) // 32) * 32 - bits)
         vals.append(Fraction(u, 1 << bits))
     return real_limbs(vals, limbs)
+
+
+# ---------------------------------------------------------------------------
+# Common-support systems (NEXT-2; Table 1)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class CommonArrays:
+    """A common-support system in the layout of phc_system_create_common: M monomials
+    (CSR ``mono_ptr``/``var_idx``/``exponent``) shared by all n_eq polynomials, dense
+    coefficients ``coeff`` [n_eq][M][2][L]."""
+
+    n_eq: int
+    n_var: int
+    limbs: int
+    mono_ptr: np.ndarray
+    var_idx: np.ndarray
+    exponent: np.ndarray
+    coeff: np.ndarray
+
+    @property
+    def n_mono(self) -> int:
+        return int(self.mono_ptr.shape[0] - 1)
+
+
+def common_support_system(n, M, kmin, kmax, amax, limbs, seed, points=1, workers=None):
+    """Table 1 shaped system (reading N2-1): n variables and equations, M shared
+    monomials; monomial j has k_j ~ U{kmin..kmax} distinct sorted variables with exponents
+    ~ U{1..amax}; unit-circle coefficients C[i][j] and points.  Returns (CommonArrays, X)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    mono_ptr, vi, ex = [0], [], []
+    for _ in range(M):
+        k = int(rng.integers(kmin, kmax + 1))
+        vs = sorted(rng.choice(n, k, replace=False).tolist())
+        es = rng.integers(1, amax + 1, k).tolist()
+        vi += vs
+        ex += es
+        mono_ptr.append(len(vi))
+    thetas_c = rng.uniform(0.0, 2.0 * math.pi, size=(n, M))
+    thetas_x = rng.uniform(0.0, 2.0 * math.pi, size=(points, n))
+    coeff = unit_circle_limbs(thetas_c, limbs, workers)
+    X = unit_circle_limbs(thetas_x, limbs, workers)
+    return CommonArrays(n, n, limbs, np.asarray(mono_ptr, np.int64), np.asarray(vi, np.int32),
+                        np.asarray(ex, np.int32), np.ascontiguousarray(coeff)), X
+
+
+# NEXT-2 configs: the Table 1 shape (P:355-358) in complex QD (the precision of the paper's
+# tracking runs, P:606) and DD, single point and batch
+COMMON_CONFIGS = {
+    "common": dict(n=40, M=200, kmin=10, kmax=30, amax=3, limbs=4, points=1),
+    "common_dd": dict(n=40, M=200, kmin=10, kmax=30, amax=3, limbs=2, points=1),
+    "common_batch": dict(n=40, M=200, kmin=10, kmax=30, amax=3, limbs=2, points=8192),
+}
+
+
+def common_config(name: str, seed: int = 1, points: int | None = None, workers=None):
+    c = COMMON_CONFIGS[name]
+    P = c["points"] if points is None else points
+    return common_support_system(c["n"], c["M"], c["kmin"], c["kmax"], c["amax"], c["limbs"], seed, P, workers)
+
+
+def expand_common(cs: CommonArrays) -> SystemArrays:
+    """The same polynomials as an ordinary system (term (i, j) = C[i][j] x^{a_j}), for the
+    oracle and for the per-term path."""
+    monos = []
+    for j in range(cs.n_mono):
+        a, b = int(cs.mono_ptr[j]), int(cs.mono_ptr[j + 1])
+        monos.append(list(zip(cs.var_idx[a:b].tolist(), cs.exponent[a:b].tolist())))
+    polys = [[list(m) for m in monos] for _ in range(cs.n_eq)]
+    return system_from_terms(cs.n_eq, cs.n_var, cs.limbs, polys, cs.coeff.reshape(-1, 2, cs.limbs))

@@ -60,3 +60,35 @@ def test_no_fallback_without_library(tmp_path, monkeypatch):
     monkeypatch.setattr(os.path, "exists", lambda p: False)
     with pytest.raises(ImportError):
         spec.loader.exec_module(mod)
+
+
+@pytest.mark.parametrize("mut,code", [
+    (lambda c: setattr(c, "limbs", 3), -4),
+    (lambda c: setattr(c, "mono_ptr", np.zeros(1, np.int64)), -1),            # no monomials
+    (lambda c: c.coeff.__setitem__((1, 2, 0, 0), np.inf), -1),                # non-finite coefficient
+    (lambda c: c.var_idx.__setitem__(0, 40), -1),                             # variable out of range
+])
+def test_common_validation_errors(mut, code):
+    """phc_system_create_common (NEXT-2) validates before touching a device."""
+    import paper_1109_0545_b200 as phc
+    from synthetic import common_support_system
+    c, _ = common_support_system(8, 12, 2, 5, 3, 2, seed=1)
+    c.coeff = c.coeff.copy()
+    c.var_idx = c.var_idx.copy()
+    mut(c)
+    with pytest.raises(phc.PhcError) as ei:
+        phc.System(c)
+    assert ei.value.code == code, str(ei.value)
+
+
+def test_expand_common_structure():
+    """The expansion used by the oracle keeps every (polynomial, monomial) pair in order."""
+    from synthetic import common_support_system, expand_common
+    c, _ = common_support_system(6, 9, 1, 4, 2, 4, seed=3)
+    e = expand_common(c)
+    assert e.n_terms == 6 * 9
+    for i in range(6):
+        for j, (t, fac) in enumerate(e.terms(i)):
+            a, b = int(c.mono_ptr[j]), int(c.mono_ptr[j + 1])
+            assert fac == list(zip(c.var_idx[a:b].tolist(), c.exponent[a:b].tolist()))
+            assert np.array_equal(e.coeff[t], c.coeff[i, j])
