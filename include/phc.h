@@ -170,6 +170,56 @@ int phc_homotopy_old_create(phc_system** out, int32_t n_eq, int32_t n_var, int32
                             const int32_t* exponent, const double* coeff_start, const double* coeff_target,
                             int32_t device);
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-4: predictor and path tracker (Alg. 1, the
+ * quadratic predictor of §5), many paths side by side on the home device.
+ * --------------------------------------------------------------------------------------- */
+
+/* Predictor (§5, "interpolate points ... by a parabola ... value of this parabola at the
+ * point (t + current step size)").  For each path p and coordinate i independently, x_out[p][i]
+ * = the value at t_new[p] of the polynomial of degree h - 1, h = min(n_hist[p], order + 1),
+ * through (t_hist[p][s], x_hist[p][s][i]), s < h (slot 0 the newest point): order 0 = constant,
+ * 1 = secant, 2 = quadratic (Newton divided differences).  All pointers are device pointers:
+ *   n_hist [n_paths] int32 in 1..3;  t_hist [n_paths][3][limbs] real limbs (distinct t);
+ *   x_hist [n_paths][3][n_var][2][limbs];  t_new [n_paths][limbs];  x_out [n_paths][n_var][2][limbs].
+ * No system handle is needed.  Asynchronous on `stream`. */
+int phc_predict_batch(int32_t limbs, int32_t n_var, int64_t n_paths, int32_t order, const int32_t* n_hist,
+                      const double* t_hist, const double* x_hist, const double* t_new, double* x_out, void* stream);
+
+/* Tracker controls (the paper states none; defaults in DESIGN.md reading T1 follow SPEC's
+ * tracker / corrector decisions). */
+typedef struct phc_track_params {
+  double step_init;   /* lambda_0 */
+  double step_min;    /* stop (fail) when lambda < step_min */
+  double step_max;    /* lambda <= step_max <= 1 */
+  double expand;      /* lambda := min(lambda * expand, step_max) after each accepted step (>= 1) */
+  double contract;    /* lambda := lambda * contract after a rejected step (0 < contract < 1) */
+  double tol;         /* corrector tolerance eps on max_i |h_i| (Alg. 2) */
+  int32_t max_newton; /* Max_It of each corrector call (Alg. 2) */
+  int32_t max_steps;  /* predictor-corrector steps per path before it is declared failed */
+  int32_t end_newton; /* extra Newton iterations at t = 1 on the paths that arrived */
+  int32_t predictor;  /* 0 constant, 1 secant, 2 quadratic (§5) */
+} phc_track_params;
+
+/* Track n_paths solution paths of the homotopy h (phc_system_set_target) from t = 0 to t = 1
+ * (Alg. 1): per path, predict (t_try = min(t + lambda, 1), z_guess from the last accepted
+ * points), correct with Newton on h(., t_try) (phc_newton_step_homotopy_batch), accept when
+ * the residual reaches tol within max_newton iterations (history updated only on success),
+ * otherwise step back; step-size control as in phc_track_params.  All active paths advance
+ * together (one batched corrector call per Newton iteration over the active paths only).
+ *   x          [n_paths][n_var][2][limbs] DEVICE pointer: start solutions in, end points out
+ *              (the last accepted point of every path, refined by end_newton iterations for
+ *              the paths that reached t = 1)
+ *   status     [n_paths] HOST int32 out: 1 reached t = 1, 2 failed (step below step_min or
+ *              max_steps exhausted)
+ *   path_stats [n_paths][5] HOST double out or NULL: accepted steps, corrector calls,
+ *              Newton iterations, min and mean accepted step size (Tables 2-3 columns)
+ *   t_end      [n_paths][limbs] DEVICE out or NULL: t of the returned points
+ * Synchronous (returns when every path has stopped).  PHC_EINVAL without a target or with
+ * inconsistent parameters. */
+int phc_track_paths(const phc_system* s, int64_t n_paths, double* x, const phc_track_params* params,
+                    int32_t* status, double* path_stats, double* t_end, void* stream);
+
 /* Static facts about the system, as built: counts used by the benchmark's model.
  * out[0] = n_terms, out[1] = n_factors, out[2] = max k, out[3] = max exponent D,
  * out[4] = nnz(J) (structurally nonzero entries), out[5] = complex multiplies per point

@@ -19,3 +19,4 @@ from .naive import (  # noqa: F401
 from .compare import rel_errors, exact_equal_limbs  # noqa: F401
 from .newton import newton_step, solve_exact  # noqa: F401
 from .homotopy import evaluate_homotopy_rows, evaluate_homotopy_dt  # noqa: F401
+from .predictor import lagrange_value, predict_point  # noqa: F401

@@ -20,6 +20,9 @@ from ._lib import (  # noqa: F401
     phc_eval_homotopy_batch,
     phc_system_set_target,
     phc_system_create_common,
+    phc_predict_batch,
+    phc_track_paths,
+    TrackParams,
     phc_homotopy_old_create,
     phc_profile_enable,
     phc_profile_read,
@@ -28,4 +31,4 @@ from ._lib import (  # noqa: F401
     phc_system_stats,
     phc_version,
 )
-from .system import System  # noqa: F401
+from .system import System, predict_batch  # noqa: F401

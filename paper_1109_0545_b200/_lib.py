@@ -29,6 +29,8 @@ EXPORTED = (
     "phc_newton_step_batch",
     "phc_system_set_target",
     "phc_system_create_common",
+    "phc_predict_batch",
+    "phc_track_paths",
     "phc_eval_homotopy_batch",
     "phc_newton_step_homotopy_batch",
     "phc_homotopy_old_create",
@@ -39,6 +41,14 @@ EXPORTED = (
     "phc_last_error",
     "phc_version",
 )
+
+
+class TrackParams(ctypes.Structure):
+    """phc_track_params (include/phc.h); defaults: DESIGN.md reading T1."""
+    _fields_ = [("step_init", ctypes.c_double), ("step_min", ctypes.c_double), ("step_max", ctypes.c_double),
+                ("expand", ctypes.c_double), ("contract", ctypes.c_double), ("tol", ctypes.c_double),
+                ("max_newton", ctypes.c_int32), ("max_steps", ctypes.c_int32), ("end_newton", ctypes.c_int32),
+                ("predictor", ctypes.c_int32)]
 
 
 class PhcError(RuntimeError):
@@ -69,6 +79,10 @@ def _load():
     lib.phc_newton_step_batch.restype = ctypes.c_int
     lib.phc_system_create_common.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, i32]
     lib.phc_system_create_common.restype = ctypes.c_int
+    lib.phc_predict_batch.argtypes = [i32, i32, i64, i32, P, P, P, P, P, P]
+    lib.phc_predict_batch.restype = ctypes.c_int
+    lib.phc_track_paths.argtypes = [P, i64, P, ctypes.POINTER(TrackParams), P, P, P, P]
+    lib.phc_track_paths.restype = ctypes.c_int
     lib.phc_system_set_target.argtypes = [P, P]
     lib.phc_system_set_target.restype = ctypes.c_int
     lib.phc_eval_homotopy_batch.argtypes = [P, i64, P, P, P, P, P, i32, P]
@@ -135,6 +149,14 @@ def phc_system_create_common(n_eq, n_var, limbs, n_mono, mono_ptr, var_idx, expo
     check(lib.phc_system_create_common(ctypes.byref(h), n_eq, n_var, limbs, n_mono, mono_ptr, var_idx, exponent,
                                        coeff, device))
     return h
+
+
+def phc_predict_batch(limbs, n_var, n_paths, order, n_hist, t_hist, x_hist, t_new, x_out, stream):
+    return check(lib.phc_predict_batch(limbs, n_var, n_paths, order, n_hist, t_hist, x_hist, t_new, x_out, stream))
+
+
+def phc_track_paths(h, n_paths, x, params, status, path_stats, t_end, stream):
+    return check(lib.phc_track_paths(h, n_paths, x, ctypes.byref(params), status, path_stats, t_end, stream))
 
 
 def phc_system_set_target(h, coeff_target):

@@ -337,6 +337,12 @@ template <> struct Prec<2> {
   PHC_DEV static real rload(const double* p) { return dd_make(p[0], p[1]); }
   PHC_DEV static real one_minus(const real& t) { return dd_add(dd_make(1, 0), dd_neg(t)); }
   PHC_DEV static C mul_real(const C& a, const real& s) { C r; r.re = dd_mul(a.re, s); r.im = dd_mul(a.im, s); return r; }
+  PHC_DEV static real rfrom(double d) { return dd_make(d, 0.0); }
+  PHC_DEV static real radd(const real& a, const real& b) { return dd_add(a, b); }
+  PHC_DEV static real rsub(const real& a, const real& b) { return dd_sub(a, b); }
+  PHC_DEV static real rmul(const real& a, const real& b) { return dd_mul(a, b); }
+  PHC_DEV static real rdiv(const real& a, const real& b) { return dd_div(a, b); }
+  PHC_DEV static void rstore(double* p, const real& a) { p[0] = a.x[0]; p[1] = a.x[1]; }
   // fused complex DD product: each real part is a 2-term dot product accumulated
   // in one error term, with one renormalisation (normwise error ~ u^2 |a||b|).
   PHC_DEV static C mul(const C& a, const C& b) {
@@ -455,6 +461,12 @@ template <> struct Prec<4> {
   PHC_DEV static real rload(const double* p) { qd r; for (int i = 0; i < 4; ++i) r.x[i] = p[i]; return r; }
   PHC_DEV static real one_minus(const real& t) { return qd_add(qd_from_d(1.0), qd_neg(t)); }
   PHC_DEV static C mul_real(const C& a, const real& s) { C r; r.re = qd_mul(a.re, s); r.im = qd_mul(a.im, s); return r; }
+  PHC_DEV static real rfrom(double d) { return qd_from_d(d); }
+  PHC_DEV static real radd(const real& a, const real& b) { return qd_add(a, b); }
+  PHC_DEV static real rsub(const real& a, const real& b) { return qd_sub(a, b); }
+  PHC_DEV static real rmul(const real& a, const real& b) { return qd_mul(a, b); }
+  PHC_DEV static real rdiv(const real& a, const real& b) { return qd_div(a, b); }
+  PHC_DEV static void rstore(double* p, const real& a) { for (int i = 0; i < 4; ++i) p[i] = a.x[i]; }
   // fused complex QD product: each real part is a QD dot product x*y + z*w evaluated in
   // one pass (qd_dot2), instead of two qd_mul and a qd_add (~440 vs ~680 FP64 instructions).
   PHC_DEV static C mul(const C& a, const C& b) {

@@ -172,6 +172,29 @@ class System:
                                             ctypes.c_void_p(st))
         return X_new, res, status
 
+    def track(self, X, stream=None, t_end=False, **params):
+        """Track the paths starting at X [P, n, 2, L] (solutions of h(., 0) = 0, on the home
+        device) to t = 1 (NEXT-4, phc_track_paths).  ``params`` override the phc_track_params
+        defaults (reading T1).  Returns (X_end, status [P] numpy int32: 1 arrived,
+        2 failed, stats [P, 5] numpy: accepted, corrector calls, Newton iterations, min step,
+        mean step[, T_end [P, L]])."""
+        import torch
+
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        prm = default_track_params(L)
+        for k, v in params.items():
+            setattr(prm, k, v)
+        Xe = X.clone()
+        status = np.zeros(P, dtype=np.int32)
+        stats = np.zeros((P, 5))
+        te = torch.empty((P, L), dtype=torch.float64, device=X.device) if t_end else None
+        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        _lib.phc_track_paths(self._h, P, _ptr(Xe), prm, _ptr(status), _ptr(stats),
+                             _ptr(te) if te is not None else None, ctypes.c_void_p(st))
+        return (Xe, status, stats, te) if t_end else (Xe, status, stats)
+
     def eval_batch_host(self, X, F=None, J=None, devices=None):
         """Host arrays (numpy or pinned CPU tensors) in and out; synchronous."""
         L = self.limbs
@@ -187,3 +210,27 @@ class System:
             dv, nd = None, 0
         _lib.phc_eval_jacobian_batch_host(self._h, P, _ptr(X), _ptr(F), _ptr(J), dv, nd)
         return F, J
+
+
+def default_track_params(limbs):
+    """Tracker defaults (reading T1; SPEC tracker/corrector decisions): lambda_0 = 0.01,
+    contraction 0.5, expansion 2 after every success, lambda_max = 0.1, lambda_min = 1e-8
+    (DD) / 1e-12 (QD), corrector tolerance 1e-24 (DD) / 1e-48 (QD) with Max_It = 4, 4 end
+    iterations at t = 1, quadratic predictor."""
+    return _lib.TrackParams(step_init=0.01, step_min=1e-8 if limbs == 2 else 1e-12, step_max=0.1, expand=2.0,
+                            contract=0.5, tol=1e-24 if limbs == 2 else 1e-48, max_newton=4, max_steps=100000,
+                            end_newton=4, predictor=2)
+
+
+def predict_batch(order, n_hist, t_hist, x_hist, t_new, out=None, stream=None):
+    """phc_predict_batch on torch tensors: n_hist [P] int32, t_hist [P, 3, L], x_hist [P, 3, n, 2, L],
+    t_new [P, L] (all on one device) -> x_out [P, n, 2, L]."""
+    import torch
+
+    P, _, n, _, L = x_hist.shape
+    if out is None:
+        out = torch.empty((P, n, 2, L), dtype=torch.float64, device=x_hist.device)
+    st = (stream or torch.cuda.current_stream(x_hist.device)).cuda_stream
+    _lib.phc_predict_batch(L, n, P, order, _ptr(n_hist), _ptr(t_hist), _ptr(x_hist), _ptr(t_new), _ptr(out),
+                           ctypes.c_void_p(st))
+    return out

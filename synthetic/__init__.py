@@ -25,4 +25,5 @@ from .systems import (  # noqa: F401
     expand_common,
     COMMON_CONFIGS,
     common_config,
+    total_degree_homotopy,
 )

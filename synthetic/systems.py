@@ -390,3 +390,39 @@ def expand_common(cs: CommonArrays) -> SystemArrays:
         monos.append(list(zip(cs.var_idx[a:b].tolist(), cs.exponent[a:b].tolist())))
     polys = [[list(m) for m in monos] for _ in range(cs.n_eq)]
     return system_from_terms(cs.n_eq, cs.n_var, cs.limbs, polys, cs.coeff.reshape(-1, 2, cs.limbs))
+
+
+# ---------------------------------------------------------------------------
+# Tracker inputs (NEXT-4): a total-degree homotopy with known start solutions
+# ---------------------------------------------------------------------------
+
+def total_degree_homotopy(n, limbs, seed):
+    """Quadratic target system with a total-degree start system on one shared support.
+
+    Support of every polynomial: all monomials of total degree <= 2 in n variables.  Target
+    coefficients: unit-circle (seeded).  Start coefficients: gamma_i for x_i^2, -gamma_i for
+    the constant, 0 elsewhere (g_i = gamma_i (x_i^2 - 1), gamma_i a seeded unit-circle
+    constant: the "gamma trick" that keeps the paths regular for generic gamma).  Start
+    solutions: the 2^n points of {+1, -1}^n, exact.  Returns (system with start coefficients,
+    coeff_target, X_start [2^n][n][2][L])."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    monos = [[]] + [[(v, 1)] for v in range(n)]
+    for a in range(n):
+        for b in range(a, n):
+            monos.append([(a, 2)] if a == b else [(a, 1), (b, 1)])
+    M = len(monos)
+    th_target = rng.uniform(0.0, 2.0 * math.pi, size=n * M)
+    th_gamma = rng.uniform(0.0, 2.0 * math.pi, size=n)
+    target = unit_circle_limbs(th_target, limbs).reshape(n * M, 2, limbs)
+    gamma = unit_circle_limbs(th_gamma, limbs)
+    start = np.zeros((n * M, 2, limbs))
+    for i in range(n):
+        j_sq = monos.index([(i, 2)])
+        start[i * M + j_sq] = gamma[i]
+        start[i * M + 0] = -gamma[i]
+    s = system_from_terms(n, n, limbs, [[list(m) for m in monos] for _ in range(n)], start)
+    X = np.zeros((2 ** n, n, 2, limbs))
+    for k in range(2 ** n):
+        for v in range(n):
+            X[k, v, 0, 0] = -1.0 if (k >> v) & 1 else 1.0
+    return s, target, X
