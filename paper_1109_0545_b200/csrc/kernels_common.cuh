@@ -64,4 +64,105 @@ __global__ void coef_product_kernel(const int64_t* __restrict__ cl_ptr, const in
   }
 }
 
+// Latency variant of the monomial stage (calls with few points, monomials with k <= 32):
+// one warp per (point, monomial), lane l holding factor l (u_l = x^{a_l}, d_l = a_l x^{a_l-1}
+// from the power table; idle lanes u = 1, d = 0).  The products of all factors but one
+// (the paper's omega_m = psi_{m-1} phi_{k-m}) come from an inclusive prefix scan
+// (psi) and an inclusive suffix scan (phi) over the warp, 5 shuffle steps each, then
+// g_l = psi_{l-1} phi_{l+1} d_l: a dependency path of ~7 products instead of ~2k, for ~2x the
+// products of the sequential chains (reading N2-3).  Writes Y[p][j] = x^{a_j} and
+// G[p][q] = g for the monomial's factor slots q, like term_kernel with unit coefficients.
+template <int L>
+__global__ void monomial_scan_kernel(const int64_t* __restrict__ term_ptr, const uint32_t* __restrict__ fac,
+                                     const double* __restrict__ PT, int n_var, int E, int64_t M, int64_t n_factors,
+                                     int64_t n_points, double* __restrict__ Y, double* __restrict__ G) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  constexpr int cd = 2 * L;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (wid >= n_points * M) return;  // warp-uniform
+  const int64_t p = wid / M, j = wid % M;
+  const int64_t f0 = term_ptr[j];
+  const int k = (int)(term_ptr[j + 1] - f0);
+  const double* pt = PT + p * (int64_t)(n_var + 1) * (2 * E) * cd;
+  C u = P::one(), d = P::zero();
+  if (lane < k) {
+    const uint32_t w = fac[f0 + lane];
+    const int64_t e = (int64_t)(w & 0xffffu) * 2 * E + ((w >> 16) & 0xffu) - 1;
+    u = cload<L>(pt + e * cd);
+    d = cload<L>(pt + (e + E) * cd);
+  }
+  auto shfl = [](const C& v, int delta, bool up) {
+    C r;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      r.re.x[i] = up ? __shfl_up_sync(0xffffffffu, v.re.x[i], delta) : __shfl_down_sync(0xffffffffu, v.re.x[i], delta);
+      r.im.x[i] = up ? __shfl_up_sync(0xffffffffu, v.im.x[i], delta) : __shfl_down_sync(0xffffffffu, v.im.x[i], delta);
+    }
+    return r;
+  };
+  C pre = u, suf = u;  // inclusive prefix / suffix products
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const C a = shfl(pre, off, true), b = shfl(suf, off, false);
+    if (lane >= off) pre = P::mul(a, pre);
+    if (lane + off < 32) suf = P::mul(suf, b);
+  }
+  C before = shfl(pre, 1, true), after = shfl(suf, 1, false);
+  if (lane == 0) before = P::one();
+  if (lane == 31) after = P::one();
+  if (lane < k) cstore<L>(G + (p * n_factors + f0 + lane) * cd, P::mul(P::mul(before, d), after));
+  if (lane == 31) cstore<L>(Y + (p * M + j) * cd, pre);
+}
+
+// Latency variant of the coefficient product for calls with few points: one warp per
+// (point, column c, row i); the 32 lanes stride over the column's list (lane l takes entries
+// l, l + 32, ...) and the partial sums meet in a fixed shuffle tree.  ~32x the parallelism of
+// coef_product_kernel at the cost of the tree (worthwhile only when the grid would otherwise be
+// a fraction of a wave).  Different summation order: the two variants agree within the
+// tolerance, each is deterministic (reading N2-2).
+template <int L>
+__global__ void coef_product_split_kernel(const int64_t* __restrict__ cl_ptr, const int32_t* __restrict__ cl_j,
+                                          const int64_t* __restrict__ cl_q, const double* __restrict__ cT,
+                                          const double* __restrict__ Y, const double* __restrict__ G, int n_eq,
+                                          int n_var, int64_t M, int64_t n_factors, int64_t n_points,
+                                          double* __restrict__ F, double* __restrict__ J) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  constexpr int cd = 2 * L;
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int64_t per_point = (int64_t)(n_var + 1) * n_eq;
+  if (wid >= n_points * per_point) return;  // warp-uniform
+  const int64_t p = wid / per_point;
+  const int r = (int)(wid % per_point);
+  const int c = r / n_eq, i = r % n_eq;
+  const double* Yp = Y + p * M * cd;
+  const double* Gp = G + p * n_factors * cd;
+  C acc = P::zero();
+  for (int64_t e = cl_ptr[c] + lane; e < cl_ptr[c + 1]; e += 32) {
+    const int j = cl_j[e];
+    const C val = (c == 0) ? cload<L>(Yp + (int64_t)j * cd) : cload<L>(Gp + cl_q[e] * cd);
+    acc = P::add_lazy(acc, P::mul_lazy(cload<L>(cT + ((int64_t)j * n_eq + i) * cd), val));
+  }
+#pragma unroll
+  for (int d = 16; d >= 1; d >>= 1) {
+    C o;
+#pragma unroll
+    for (int k = 0; k < L; ++k) {
+      o.re.x[k] = __shfl_down_sync(0xffffffffu, acc.re.x[k], d);
+      o.im.x[k] = __shfl_down_sync(0xffffffffu, acc.im.x[k], d);
+    }
+    acc = P::add_lazy(acc, o);
+  }
+  if (lane == 0) {
+    const C v = P::norm(acc);
+    if (c == 0)
+      cstore<L>(F + (p * n_eq + i) * cd, v);
+    else
+      cstore<L>(J + ((p * n_eq + i) * (int64_t)n_var + (c - 1)) * cd, v);
+  }
+}
+
 }  // namespace phc

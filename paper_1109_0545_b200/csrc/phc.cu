@@ -316,9 +316,16 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
 
 // NEXT-2 two-stage path: power table, monomial stage V (the term kernel with unit
 // coefficients), coefficient product Y = C [V | D].
+// split: the latency variant of the coefficient product, chosen per CALL from the call's total
+// point count (so a sharded call and an unsharded one use the same variant).
+inline bool common_split(const phc_system* s, int64_t call_points) {
+  const int TI = s->L == 2 ? 8 : 4;
+  return call_points * (s->n_var + 1) * ((s->n_eq + TI - 1) / TI) < 148 * 128;
+}
+
 template <int L>
 int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
-               cudaStream_t st) {
+               bool split, cudaStream_t st) {
   int rc = ensure_scratch(s, d, n_points);
   if (rc) return rc;
   const int64_t cd = 2 * L;
@@ -331,7 +338,12 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
       phc::power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x + p0 * s->n_var * cd, s->n_var,
                                                                                 s->E, np, d->PT);
     }
-    if (s->kmax <= 8)
+    if (split && s->kmax <= 32) {
+      ProfScope ps1(s, d->dev, 1, st);
+      const int64_t nwarps = np * s->n_terms;
+      phc::monomial_scan_kernel<L><<<(unsigned)((nwarps * 32 + 127) / 128), 128, 0, st>>>(
+          d->term_ptr, d->fac, d->PT, s->n_var, s->E, s->n_terms, s->n_factors, np, d->Y, d->G);
+    } else if (s->kmax <= 8)
       launch_term<L, 8>(s, d, np, nullptr, st);
     else if (s->kmax <= 16)
       launch_term<L, 16>(s, d, np, nullptr, st);
@@ -342,9 +354,16 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
     const int64_t tiles = (s->n_eq + TI - 1) / TI;
     const int64_t nthr = np * (s->n_var + 1) * tiles;
     ProfScope ps(s, d->dev, 2, st);
-    phc::coef_product_kernel<L, TI><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(
-        d->cl_ptr, d->cl_j, d->cl_q, d->cT, d->Y, d->G, s->n_eq, s->n_var, s->n_terms, s->n_factors, np,
-        f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+    if (split) {
+      const int64_t nwarps = np * (s->n_var + 1) * s->n_eq;
+      phc::coef_product_split_kernel<L><<<(unsigned)((nwarps * 32 + 255) / 256), 256, 0, st>>>(
+          d->cl_ptr, d->cl_j, d->cl_q, d->cT, d->Y, d->G, s->n_eq, s->n_var, s->n_terms, s->n_factors, np,
+          f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+    } else {
+      phc::coef_product_kernel<L, TI><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(
+          d->cl_ptr, d->cl_j, d->cl_q, d->cT, d->Y, d->G, s->n_eq, s->n_var, s->n_terms, s->n_factors, np,
+          f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+    }
     CUDA_TRY(cudaGetLastError());
   }
   return PHC_OK;
@@ -353,11 +372,13 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
 // Evaluate n_points points resident on device d, on stream st.  T (t per point, device d)
 // selects the homotopy coefficients (NEXT-3); nullptr evaluates the system's own coefficients.
 int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
-                  double* jac, cudaStream_t st) {
+                  double* jac, cudaStream_t st, int64_t call_points = -1) {
   if (n_points <= 0) return PHC_OK;
   if (s->common) {
     if (T) return fail(PHC_EUNSUPPORTED, "homotopy coefficients are not supported on common-support systems");
-    return s->L == 2 ? run_common<2>(s, d, n_points, x, f, jac, st) : run_common<4>(s, d, n_points, x, f, jac, st);
+    const bool split = common_split(s, call_points < 0 ? n_points : call_points);
+    return s->L == 2 ? run_common<2>(s, d, n_points, x, f, jac, split, st)
+                     : run_common<4>(s, d, n_points, x, f, jac, split, st);
   }
   if (d->have_block) {
     ProfScope ps(s, d->dev, 3, st);
@@ -635,7 +656,7 @@ static int eval_batch_impl(const phc_system* cs, int64_t n_points, const double*
     if ((rc = get_device_state(s, dv, &d))) break;
     if (dv == s->home) {
       rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
-                         jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st);
+                         jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st, n_points);
       continue;
     }
     DeviceGuard gd(dv);
@@ -655,7 +676,7 @@ static int eval_batch_impl(const phc_system* cs, int64_t n_points, const double*
       rc = fail(PHC_ECUDA, "scatter copy (t) failed");
       break;
     }
-    if ((rc = run_on_device(s, d, np, d->xs, T ? d->ts : nullptr, d->fs, d->js, d->stream))) break;
+    if ((rc = run_on_device(s, d, np, d->xs, T ? d->ts : nullptr, d->fs, d->js, d->stream, n_points))) break;
     if (cudaMemcpyPeerAsync(f + p0 * s->n_eq * cd, s->home, d->fs, dv, np * s->n_eq * cd * 8, d->stream) != cudaSuccess ||
         cudaMemcpyPeerAsync(jac + p0 * (int64_t)s->n_eq * s->n_var * cd, s->home, d->js, dv,
                             np * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream) != cudaSuccess) {
@@ -725,7 +746,8 @@ static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, 
   const int threads = n <= 48 ? 128 : 256;
   for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
     const int64_t np = std::min(chunk, n_points - p0);
-    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, T ? T + p0 * L : nullptr, d->nF, d->nJ, st))) return rc;
+    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, T ? T + p0 * L : nullptr, d->nF, d->nJ, st, n_points)))
+      return rc;
     phc::NewtonArgs a;
     a.X = x + p0 * n * cd;
     a.F = d->nF;
