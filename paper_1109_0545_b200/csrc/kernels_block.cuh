@@ -255,10 +255,9 @@ PHC_DEV typename Prec<L>::C cls_load(const double2* base, int NE, int e, int c) 
 //
 // Homotopy (NEXT-3): when hom, the coefficient is the blend
 // c(t) = (1 - t) c_start + t c_target (reading H1), formed here before it is folded into P_0.
-template <int L, int K, int LAYOUT>
+template <int L, int K, int LAYOUT, bool HOM>
 PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double* pt, double* rows, int lane,
-                                     bool hom, const typename Prec<L>::real& omt,
-                                     const typename Prec<L>::real& tt) {
+                                     const typename Prec<L>::real& omt, const typename Prec<L>::real& tt) {
   using P = Prec<L>;
   using C = typename P::C;
   constexpr int H = K / 2;
@@ -296,7 +295,8 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   C Pk[H];  // P_0 .. P_{H-1}
   C Sk[H];  // S_1 .. S_{H-1} at Sk[1..H-1]
   C p = cload<L>(a.coef + ((size_t)b * kWarp + lane) * 2 * L);  // running P
-  if (hom) p = P::add(P::mul_real(p, omt), P::mul_real(cload<L>(a.coef2 + ((size_t)b * kWarp + lane) * 2 * L), tt));
+  if constexpr (HOM)
+    p = P::add(P::mul_real(p, omt), P::mul_real(cload<L>(a.coef2 + ((size_t)b * kWarp + lane) * 2 * L), tt));
   C q;                                                           // running S
   // phase 1
   auto phase1 = [&](int t, uint32_t w1, uint32_t w2) {  // w1 = word_at(t), w2 = word_at(K - t + 1)
@@ -387,7 +387,9 @@ PHC_DEV typename Prec<L>::C row_total(const double* rows, int R, int n_var, int 
   return acc;
 }
 
-template <int L, int K, int LAYOUT>
+// HOM: homotopy coefficients (NEXT-3) -- a separate instantiation, so the plain evaluation
+// carries none of the blend's code or registers.
+template <int L, int K, int LAYOUT, bool HOM>
 __global__ void __launch_bounds__(block_warps(L, LAYOUT) * kWarp, 1)
 block_kernel(const BlockArgs a) {
   using P = Prec<L>;
@@ -402,9 +404,8 @@ block_kernel(const BlockArgs a) {
   const int64_t p = blockIdx.x / units_per_point;
   const int unit = (int)(blockIdx.x % units_per_point);
   if (p >= a.n_points) return;
-  const bool hom = a.coef2 != nullptr;
   typename P::real tt = P::one().re, omt = P::one().re;
-  if (hom) {
+  if constexpr (HOM) {
     tt = P::rload(a.T + p * L);
     omt = P::one_minus(tt);
   }
@@ -466,7 +467,7 @@ block_kernel(const BlockArgs a) {
     C fsum = P::zero();
     const int b_step = mA ? 1 : kBlockWarps;
     for (int b = a.blk[i] + (mA ? 0 : warp); b < a.blk[i + 1]; b += b_step) {
-      C y = do_block<L, K, LAYOUT>(a, b, pt, rows, lane, hom, omt, tt);
+      C y = do_block<L, K, LAYOUT, HOM>(a, b, pt, rows, lane, omt, tt);
       fsum = P::add(fsum, y);
     }
     __syncwarp();
@@ -724,7 +725,7 @@ inline int upload_block_tables(const HostBlockPlan& plan, BlockTables* bt) {
 
 template <int L, int K, int LAYOUT>
 int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_points, cudaStream_t st) {
-  auto kern = block_kernel<L, K, LAYOUT>;
+  auto kern = a.coef2 ? block_kernel<L, K, LAYOUT, true> : block_kernel<L, K, LAYOUT, false>;
   if (plan.smem_bytes > 48 * 1024)
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes) != cudaSuccess)
       return -3;
