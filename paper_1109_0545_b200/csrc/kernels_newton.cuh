@@ -147,4 +147,151 @@ __global__ void __launch_bounds__(256) newton_solve_kernel(const NewtonArgs a) {
   if (tid == 0) a.status[p] = 0;
 }
 
+// ---------------------------------------------------------------------------------------
+// Multi-kernel elimination for systems whose augmented matrix does not fit shared memory
+// (e.g. n = 256 QD: 4.2 MB per point): every step k is two launches over all points of the
+// chunk, so the trailing update of one point spreads over many SMs instead of one CTA.
+//   newton_load_kernel      [J | -F] -> Mg, residual, status := 0          (one CTA per point)
+//   newton_pivot_kernel<k>  pivot search in column k, row swap, pivot reciprocal, multipliers
+//                           l_i = M[i][k] / M[k][k] stored in column k    (one CTA per point)
+//   newton_update_kernel<k> M[i][j] -= l_i M[k][j], i > k, j > k          (many CTAs per point)
+//   newton_backsub_kernel   back substitution and z := z + dz              (one CTA per point)
+// Same pivot rule, operations and order per entry as newton_solve_kernel, so the two paths
+// give the same result bitwise for a given matrix.
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(256) newton_load_kernel(const NewtonArgs a) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  __shared__ double red_v[32];
+  const int64_t p = blockIdx.x;
+  if (p >= a.n_points) return;
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
+  double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
+  const double* Fp = a.F + (size_t)p * n * cd;
+  const double* Jp = a.J + (size_t)p * n * n * cd;
+  double rmax = 0.0;
+  for (int e = tid; e < n * cols; e += T) {
+    const int i = e / cols, j = e % cols;
+    if (j < n) {
+      sstore<L>(M + (size_t)e * cd, cload<L>(Jp + ((size_t)i * n + j) * cd));
+    } else {
+      const C f = cload<L>(Fp + (size_t)i * cd);
+      rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
+      sstore<L>(M + (size_t)e * cd, P::neg(f));
+    }
+  }
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if (lane == 0) red_v[wid] = rmax;
+  __syncthreads();
+  if (tid == 0) {
+    double r = 0.0;
+    for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
+    a.resid[p] = r;
+    a.status[p] = 0;
+  }
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) newton_pivot_kernel(const NewtonArgs a, int k) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_piv, s_bad;
+  __shared__ __align__(16) double s_inv[2 * L];
+  const int64_t p = blockIdx.x;
+  if (p >= a.n_points || a.status[p]) return;
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
+  double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
+  double* invd = M + (size_t)n * cols * cd;
+  auto at = [&](int i, int j) { return M + ((size_t)i * cols + j) * cd; };
+  double best = -1.0;
+  int bi = n;
+  for (int i = k + tid; i < n; i += T) {
+    const double v = P::abs2_hi(sload<L>(at(i, k)));
+    if (v > best) { best = v; bi = i; }
+  }
+  for (int o = 16; o; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+  }
+  if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+  __syncthreads();
+  if (tid == 0) {
+    double b = -1.0;
+    int ix = n;
+    for (int w = 0; w < nwarp; ++w)
+      if (red_v[w] > b || (red_v[w] == b && red_i[w] < ix)) { b = red_v[w]; ix = red_i[w]; }
+    s_piv = ix;
+    s_bad = !(b > 0.0);
+    if (s_bad) a.status[p] = 1;
+  }
+  __syncthreads();
+  if (s_bad) return;
+  const int pv = s_piv;
+  if (pv != k)
+    for (int j = k + tid; j < cols; j += T) {
+      const C u = sload<L>(at(k, j)), v = sload<L>(at(pv, j));
+      sstore<L>(at(k, j), v);
+      sstore<L>(at(pv, j), u);
+    }
+  __syncthreads();
+  if (tid == 0) {
+    const C inv = P::recip(sload<L>(at(k, k)));
+    sstore<L>(s_inv, inv);
+    sstore<L>(invd + (size_t)k * cd, inv);
+  }
+  __syncthreads();
+  const C inv = sload<L>(s_inv);
+  for (int i = k + 1 + tid; i < n; i += T) sstore<L>(at(i, k), P::mul(sload<L>(at(i, k)), inv));
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) newton_update_kernel(const NewtonArgs a, int k) {
+  using P = Prec<L>;
+  const int64_t p = blockIdx.y;
+  if (p >= a.n_points || a.status[p]) return;
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  const int ucols = cols - k - 1;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)(n - k - 1) * ucols) return;
+  const int i = k + 1 + (int)(e / ucols), j = k + 1 + (int)(e % ucols);
+  double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
+  auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
+  sstore<L>(at(i, j), P::sub(sload<L>(at(i, j)), P::mul(sload<L>(at(i, k)), sload<L>(at(k, j)))));
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) newton_backsub_kernel(const NewtonArgs a) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  const int64_t p = blockIdx.x;
+  if (p >= a.n_points) return;
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  const int tid = threadIdx.x, T = blockDim.x;
+  if (a.status[p]) {
+    for (int e = tid; e < n; e += T)
+      cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
+    return;
+  }
+  double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
+  double* invd = M + (size_t)n * cols * cd;
+  auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
+  for (int i = n - 1; i >= 0; --i) {
+    if (tid == 0) sstore<L>(at(i, n), P::mul(sload<L>(at(i, n)), sload<L>(invd + (size_t)i * cd)));
+    __syncthreads();
+    const C xi = sload<L>(at(i, n));
+    for (int r = tid; r < i; r += T) sstore<L>(at(r, n), P::sub(sload<L>(at(r, n)), P::mul(sload<L>(at(r, i)), xi)));
+    __syncthreads();
+  }
+  for (int e = tid; e < n; e += T) {
+    const double* xp = a.X + ((size_t)p * n + e) * cd;
+    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), sload<L>(at(e, n))));
+  }
+}
+
 }  // namespace phc

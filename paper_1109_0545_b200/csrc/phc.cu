@@ -412,6 +412,19 @@ int ensure_stage(const phc_system* s, DeviceState* d, int64_t np) {
 
 }  // namespace
 
+// Multi-kernel elimination (kernels_newton.cuh) for matrices beyond shared memory.
+template <int L>
+void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
+  const int n = a.n;
+  phc::newton_load_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
+  for (int k = 0; k < n; ++k) {
+    phc::newton_pivot_kernel<L><<<(unsigned)np, 256, 0, st>>>(a, k);
+    const int64_t work = (int64_t)(n - k - 1) * (n - k);
+    if (work > 0) phc::newton_update_kernel<L><<<dim3((unsigned)((work + 255) / 256), (unsigned)np), 256, 0, st>>>(a, k);
+  }
+  phc::newton_backsub_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
+}
+
 template <class T>
 struct DevBuf {  // RAII device buffer (the tracker's workspace)
   T* p = nullptr;
@@ -764,14 +777,14 @@ static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, 
         if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
         phc::newton_solve_kernel<2, true><<<(unsigned)np, threads, mat, st>>>(a);
       } else {
-        phc::newton_solve_kernel<2, false><<<(unsigned)np, threads, 0, st>>>(a);
+        newton_multi<2>(a, np, st);
       }
     } else {
       if (smem) {
         if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
         phc::newton_solve_kernel<4, true><<<(unsigned)np, threads, mat, st>>>(a);
       } else {
-        phc::newton_solve_kernel<4, false><<<(unsigned)np, threads, 0, st>>>(a);
+        newton_multi<4>(a, np, st);
       }
     }
     CUDA_TRY(cudaGetLastError());

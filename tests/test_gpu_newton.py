@@ -143,3 +143,33 @@ def test_newton_singular_and_in_place(phc):
     h2.newton_step(B, B)
     torch.cuda.synchronize()
     assert torch.equal(out, B)
+
+
+def test_newton_multi_kernel_path_vs_oracle(phc):
+    """n = 64 QD: [J | -F] (266 KB) exceeds shared memory, so the elimination runs as two
+    launches per column over many SMs (kernels_newton.cuh, multi-kernel path)."""
+    from synthetic import random_system
+    s, X = random_system(64, 8, 6, 3, 4, seed=3, points=2)
+    xn, res, status, h = _gpu_step(phc, s, X)
+    assert (status == 0).all()
+    F, Jd = h.eval_batch(torch.from_numpy(X).cuda())
+    for p in (0, 1):
+        Jc = Jd.cpu().numpy()[p][..., 0, 0] + 1j * Jd.cpu().numpy()[p][..., 1, 0]
+        cond = np.linalg.cond(Jc)
+        err = _check_point(s, X[p], xn[p], res[p])
+        assert err <= _tol(4, 64, cond), (p, err, cond)
+
+
+def test_newton_multi_kernel_singular(phc):
+    """Multi-kernel path: a variable absent from the system -> zero pivot column -> status 1,
+    x unchanged; the other point of the batch is unaffected."""
+    from synthetic import random_system
+    s, X = random_system(60, 6, 5, 2, 4, seed=4, points=2)
+    keep = s.var_idx != 59
+    counts = np.add.reduceat(keep.astype(np.int64), s.term_ptr[:-1])
+    counts[np.diff(s.term_ptr) == 0] = 0
+    s.term_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    s.var_idx, s.exponent = s.var_idx[keep].copy(), s.exponent[keep].copy()
+    xn, res, status, h = _gpu_step(phc, s, X)
+    assert (status == 1).all()
+    assert np.array_equal(xn, X)
