@@ -1,0 +1,184 @@
+// Latency path for calls with few points (DESIGN.md §4
+// "latency path"): the same evaluation as the fused block kernel, reorganised so that one
+// point's work spreads over many warps with short dependency chains.
+//
+//  * One warp per TERM (not per block of 32 terms): lane l holds factor l of the term,
+//    u_l = x^{a_l} and d_l = a_l x^{a_l - 1} from the power table (idle lanes u = 1, d = 0).
+//  * The products of all factors but one (the paper's omega_m = psi_{m-1} phi_{k-m},
+//    P:549-561) come from an inclusive prefix scan psi (with the coefficient folded into lane
+//    0, reading C3) and an inclusive suffix scan phi over the lanes: 5 shuffle steps each,
+//    then g_l = psi_{l-1} phi_{l+1} d_l.  Dependency path ~8 products instead of ~k; about
+//    2x the products of the sequential chains (reading N2-3) -- the right trade only when the
+//    GPU would otherwise be mostly idle.
+//  * CTA (point p, polynomial i, split s) takes a fixed contiguous range of the terms of
+//    f_i; warp w of the CTA takes terms w, w + W, ... of the range and adds its g_l into its
+//    own shared-memory row (a term's variables are distinct: no conflicts within the warp);
+//    the CTA sums the W rows in warp order.  With S > 1 splits the S partial rows go to a
+//    global scratch and scan_reduce_kernel sums them in split order.  The order is fixed
+//    per system (W, S do not depend on the call), so results are bitwise reproducible.
+//  * The power table of the point is built in shared memory by each CTA (one thread per
+//    entry, binary powering).
+#pragma once
+#include "arith.cuh"
+
+namespace phc {
+
+struct ScanArgs {
+  const int64_t* poly_ptr;
+  const int64_t* term_ptr;
+  const uint32_t* fac;  // var | exp << 16
+  const double* coeff;
+  const double* coeff2;  // homotopy target (NEXT-3) or nullptr
+  const double* T;       // t per point when coeff2
+  const double* X;
+  double* F;
+  double* J;
+  double* part;  // S > 1: [P][n_eq][S][n_var + 1][2L] partial rows (col n_var = F)
+  int n_eq, n_var, E, S;
+  int64_t n_points;
+};
+
+template <int L>
+PHC_DEV typename Prec<L>::C cpow_scan(const typename Prec<L>::C& x, int e) {
+  using P = Prec<L>;
+  if (e == 0) return P::one();
+  int top = 31 - __clz(e);
+  typename P::C r = x;
+  for (int b = top - 1; b >= 0; --b) {
+    r = P::mul(r, r);
+    if ((e >> b) & 1) r = P::mul(r, x);
+  }
+  return r;
+}
+
+template <int L>
+PHC_DEV typename Prec<L>::C shfl_c(const typename Prec<L>::C& v, int delta, bool up) {
+  typename Prec<L>::C r;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    r.re.x[i] = up ? __shfl_up_sync(0xffffffffu, v.re.x[i], delta) : __shfl_down_sync(0xffffffffu, v.re.x[i], delta);
+    r.im.x[i] = up ? __shfl_up_sync(0xffffffffu, v.im.x[i], delta) : __shfl_down_sync(0xffffffffu, v.im.x[i], delta);
+  }
+  return r;
+}
+
+template <int L>
+__global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  constexpr int cd = 2 * L;
+  extern __shared__ __align__(16) double sm[];
+  const int W = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t cta = blockIdx.x;
+  const int s = (int)(cta % a.S);
+  const int i = (int)((cta / a.S) % a.n_eq);
+  const int64_t p = cta / ((int64_t)a.S * a.n_eq);
+  if (p >= a.n_points) return;
+  const int twoE = 2 * a.E;
+  double* pt = sm;                                         // [(n_var)][2E][cd]
+  double* rows = sm + (size_t)a.n_var * twoE * cd;         // [W][n_var][cd]
+  double* fpart = rows + (size_t)W * a.n_var * cd;         // [W][cd]
+  // power table of point p: U[v][e-1] = x_v^e, Dd[v][e-1] = e x_v^(e-1)
+  for (int idx = threadIdx.x; idx < a.n_var * a.E; idx += blockDim.x) {
+    const int v = idx / a.E, e = idx % a.E + 1;
+    const C x = cload<L>(a.X + (p * a.n_var + v) * cd);
+    const C pm = cpow_scan<L>(x, e - 1);
+    sstore<L>(pt + ((size_t)v * twoE + e - 1) * cd, e == 1 ? x : P::mul(pm, x));
+    sstore<L>(pt + ((size_t)v * twoE + a.E + e - 1) * cd, e == 1 ? pm : P::mul_int(pm, (double)e));
+  }
+  for (int e = threadIdx.x; e < W * a.n_var * cd / 2; e += blockDim.x)
+    reinterpret_cast<double2*>(rows)[e] = make_double2(0.0, 0.0);
+  typename P::real tt = P::one().re, omt = P::one().re;
+  if (a.coeff2) {
+    tt = P::rload(a.T + p * L);
+    omt = P::one_minus(tt);
+  }
+  __syncthreads();
+  const int64_t t0 = a.poly_ptr[i], nt = a.poly_ptr[i + 1] - t0;
+  const int64_t r0 = t0 + nt * s / a.S, r1 = t0 + nt * (s + 1) / a.S;  // this split's terms
+  double* myrow = rows + (size_t)warp * a.n_var * cd;
+  C fsum = P::zero();
+  for (int64_t t = r0 + warp; t < r1; t += W) {
+    const int64_t f0 = a.term_ptr[t];
+    const int k = (int)(a.term_ptr[t + 1] - f0);
+    C c = cload<L>(a.coeff + t * cd);
+    if (a.coeff2) c = P::add(P::mul_real(c, omt), P::mul_real(cload<L>(a.coeff2 + t * cd), tt));
+    C u = P::one(), d = P::zero();
+    int v = -1;
+    if (lane < k) {
+      const uint32_t w = a.fac[f0 + lane];
+      v = (int)(w & 0xffffu);
+      const int e = (int)((w >> 16) & 0xffu);
+      u = sload<L>(pt + ((size_t)v * twoE + e - 1) * cd);
+      d = sload<L>(pt + ((size_t)v * twoE + a.E + e - 1) * cd);
+    }
+    C pre = (lane == 0) ? P::mul(c, u) : u;  // psi with the coefficient folded in
+    C suf = u;                                // phi
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      const C x1 = shfl_c<L>(pre, off, true), x2 = shfl_c<L>(suf, off, false);
+      if (lane >= off) pre = P::mul(x1, pre);
+      if (lane + off < 32) suf = P::mul(suf, x2);
+    }
+    C before = shfl_c<L>(pre, 1, true), after = shfl_c<L>(suf, 1, false);
+    if (lane == 0) before = c;
+    if (lane == 31) after = P::one();
+    if (lane < k) {
+      const C g = P::mul(P::mul(before, d), after);
+      double* acc = myrow + (size_t)v * cd;
+      sstore<L>(acc, P::add(sload<L>(acc), g));
+    }
+    const C y = shfl_c<L>(pre, 31, false);  // only lane 0 reads lane 31's full product
+    if (k == 0) {                           // constant term: value c
+      fsum = P::add(fsum, c);
+    } else {
+      fsum = P::add(fsum, y);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) sstore<L>(fpart + (size_t)warp * cd, fsum);
+  __syncthreads();
+  // CTA totals in warp order; S == 1 writes F and J, S > 1 writes the partial row
+  const bool direct = a.S == 1;
+  for (int col = threadIdx.x; col <= a.n_var; col += blockDim.x) {
+    C acc;
+    if (col < a.n_var) {
+      acc = sload<L>(rows + (size_t)col * cd);
+      for (int w = 1; w < W; ++w) acc = P::add(acc, sload<L>(rows + ((size_t)w * a.n_var + col) * cd));
+    } else {
+      acc = sload<L>(fpart);
+      for (int w = 1; w < W; ++w) acc = P::add(acc, sload<L>(fpart + (size_t)w * cd));
+    }
+    if (direct) {
+      if (col < a.n_var)
+        cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)a.n_var + col) * cd, acc);
+      else
+        cstore<L>(a.F + (p * a.n_eq + i) * cd, acc);
+    } else {
+      cstore<L>(a.part + (((p * a.n_eq + i) * a.S + s) * (int64_t)(a.n_var + 1) + col) * cd, acc);
+    }
+  }
+}
+
+// Sum of the S partial rows in split order (S > 1).
+template <int L>
+__global__ void scan_reduce_kernel(const ScanArgs a) {
+  using P = Prec<L>;
+  constexpr int cd = 2 * L;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t per_point = (int64_t)a.n_eq * (a.n_var + 1);
+  if (gid >= a.n_points * per_point) return;
+  const int64_t p = gid / per_point;
+  const int i = (int)((gid % per_point) / (a.n_var + 1));
+  const int col = (int)(gid % (a.n_var + 1));
+  const double* src = a.part + (((p * a.n_eq + i) * a.S) * (int64_t)(a.n_var + 1) + col) * cd;
+  typename P::C acc = cload<L>(src);
+  for (int s = 1; s < a.S; ++s) acc = P::add(acc, cload<L>(src + (size_t)s * (a.n_var + 1) * cd));
+  if (col < a.n_var)
+    cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)a.n_var + col) * cd, acc);
+  else
+    cstore<L>(a.F + (p * a.n_eq + i) * cd, acc);
+}
+
+}  // namespace phc

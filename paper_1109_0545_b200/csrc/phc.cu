@@ -20,6 +20,7 @@
 #include "kernels_newton.cuh"
 #include "kernels_common.cuh"
 #include "kernels_track.cuh"
+#include "kernels_scan.cuh"
 
 namespace {
 
@@ -96,6 +97,9 @@ struct DeviceState {
   double* nJ = nullptr;
   double* nM = nullptr;
   int64_t n_cap = 0;
+  // latency (warp-scan) path: partial rows of the S splits
+  double* part = nullptr;
+  int64_t part_cap = 0;
   // staging buffers for remote shards
   double* xs = nullptr;
   double* fs = nullptr;
@@ -107,7 +111,7 @@ struct DeviceState {
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
                     (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
-                    (void*)cl_q, (void*)cT})
+                    (void*)cl_q, (void*)cT, (void*)part})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (done) cudaEventDestroy(done);
@@ -130,6 +134,10 @@ struct phc_system {
   // NEXT-2 common-support system: "terms" are the M shared monomials (unit coefficients),
   // C^T [M][n_eq][2][L] and the per-column lists of the coefficient product
   bool common = false;
+  // latency path (kernels_scan.cuh): eligible when k <= 32 and the CTA's table + rows fit
+  bool scan_ok = false;
+  int scan_S = 1, scan_W = 8;
+  size_t scan_smem = 0;
   std::vector<int64_t> cl_ptr, cl_q;
   std::vector<int32_t> cl_j;
   std::vector<double> cT;
@@ -314,6 +322,56 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
   return PHC_OK;
 }
 
+// Latency path (kernels_scan.cuh) for calls with few points: one warp per term.
+constexpr int64_t kScanMaxTerms = 148 * 32;  // call_points * n_terms at or below: latency path
+
+template <int L>
+int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
+             double* jac, cudaStream_t st) {
+  const int64_t cd = 2 * L;
+  phc::ScanArgs a;
+  a.poly_ptr = d->poly_ptr;
+  a.term_ptr = d->term_ptr;
+  a.fac = d->fac;
+  a.coeff = d->coeff;
+  a.coeff2 = T ? d->coeff2 : nullptr;
+  a.T = T;
+  a.X = x;
+  a.F = f;
+  a.J = jac;
+  a.n_eq = s->n_eq;
+  a.n_var = s->n_var;
+  a.E = s->E;
+  a.S = s->scan_S;
+  a.n_points = n_points;
+  a.part = nullptr;
+  if (s->scan_S > 1) {
+    const int64_t need = n_points * s->n_eq * s->scan_S * (int64_t)(s->n_var + 1) * cd;
+    if (need > d->part_cap) {
+      cudaStreamSynchronize(st);
+      if (d->part) cudaFree(d->part);
+      d->part = nullptr;
+      d->part_cap = 0;
+      int rc = dalloc(&d->part, (size_t)need);
+      if (rc) return rc;
+      d->part_cap = need;
+    }
+    a.part = d->part;
+  }
+  ProfScope ps(s, d->dev, 3, st);
+  auto kern = phc::poly_scan_kernel<L>;
+  if (s->scan_smem > 48 * 1024)
+    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->scan_smem));
+  const int64_t ctas = n_points * s->n_eq * s->scan_S;
+  kern<<<(unsigned)ctas, s->scan_W * 32, s->scan_smem, st>>>(a);
+  if (s->scan_S > 1) {
+    const int64_t nth = n_points * s->n_eq * (int64_t)(s->n_var + 1);
+    phc::scan_reduce_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(a);
+  }
+  CUDA_TRY(cudaGetLastError());
+  return PHC_OK;
+}
+
 // NEXT-2 two-stage path: power table, monomial stage V (the term kernel with unit
 // coefficients), coefficient product Y = C [V | D].
 // split: the latency variant of the coefficient product, chosen per CALL from the call's total
@@ -380,6 +438,8 @@ int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const d
     return s->L == 2 ? run_common<2>(s, d, n_points, x, f, jac, split, st)
                      : run_common<4>(s, d, n_points, x, f, jac, split, st);
   }
+  if (s->scan_ok && (call_points < 0 ? n_points : call_points) * s->n_terms <= kScanMaxTerms)
+    return s->L == 2 ? run_scan<2>(s, d, n_points, x, T, f, jac, st) : run_scan<4>(s, d, n_points, x, T, f, jac, st);
   if (d->have_block) {
     ProfScope ps(s, d->dev, 3, st);
     int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, T, f, jac, st)
@@ -519,6 +579,15 @@ int phc_system_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t lim
   s->cm_per_point += (int64_t)n_var * std::max(0, s->E - 1);
   s->ca_per_point = n_factors + n_terms;  // one add per contribution into a zero-initialised sum
   phc::plan_blocks(*s, &s->plan);
+  {
+    // latency path eligibility and its fixed split (independent of the call: reproducibility)
+    int64_t max_terms = 0;
+    for (int i = 0; i < n_eq; ++i) max_terms = std::max<int64_t>(max_terms, poly_ptr[i + 1] - poly_ptr[i]);
+    const int W = s->scan_W;
+    s->scan_smem = ((size_t)n_var * 2 * s->E + (size_t)W * n_var + W) * 2 * limbs * sizeof(double);
+    s->scan_ok = kmax <= 32 && s->scan_smem <= (size_t)200 * 1024 && max_terms > 0;
+    s->scan_S = (int)std::max<int64_t>(1, std::min<int64_t>(148 / n_eq, (max_terms + W - 1) / W));
+  }
   s->ca_per_point = s->plan.usable ? s->plan.ca_per_point : s->ca_per_point;
   DeviceState* d;
   int rc = get_device_state(s.get(), device, &d);
