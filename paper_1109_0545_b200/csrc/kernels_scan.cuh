@@ -14,7 +14,8 @@
 //    f_i; warp w of the CTA takes terms w, w + W, ... of the range and adds its g_l into its
 //    own shared-memory row (a term's variables are distinct: no conflicts within the warp);
 //    the CTA sums the W rows in warp order.  With S > 1 splits the S partial rows go to a
-//    global scratch and scan_reduce_kernel sums them in split order.  The order is fixed
+//    global scratch and the last CTA of the polynomial to arrive (atomic counter) sums them
+//    in split order.  The order is fixed
 //    per system (W, S do not depend on the call), so results are bitwise reproducible.
 //  * The power table of the point is built in shared memory by each CTA (one thread per
 //    entry, binary powering).
@@ -34,6 +35,7 @@ struct ScanArgs {
   double* F;
   double* J;
   double* part;  // S > 1: [P][n_eq][S][n_var + 1][2L] partial rows (col n_var = F)
+  int* count;    // S > 1: [P][n_eq] arrival counters (zero between calls)
   int n_eq, n_var, E, S;
   int64_t n_points;
 };
@@ -49,6 +51,48 @@ PHC_DEV typename Prec<L>::C cpow_scan(const typename Prec<L>::C& x, int e) {
     if ((e >> b) & 1) r = P::mul(r, x);
   }
   return r;
+}
+
+// One out-of-line copy of the QD complex product: the per-term code calls it ~13 times, and
+// inlining every call made the kernel 11k instructions, whose instruction-cache misses were the
+// top stall (ncu: no_instruction 4.1 of 9 cycles per issue).  DD products stay inline.
+template <int L>
+__device__ __noinline__ typename Prec<L>::C cmul_ool(const typename Prec<L>::C a, const typename Prec<L>::C b) {
+  return Prec<L>::mul(a, b);
+}
+// two independent products in one call (the psi and phi scans advance together: ILP)
+template <int L>
+struct CPair {
+  typename Prec<L>::C a, b;
+};
+template <int L>
+__device__ __noinline__ CPair<L> cmul2_ool(const typename Prec<L>::C a1, const typename Prec<L>::C b1,
+                                           const typename Prec<L>::C a2, const typename Prec<L>::C b2) {
+  CPair<L> r;
+  r.a = Prec<L>::mul(a1, b1);
+  r.b = Prec<L>::mul(a2, b2);
+  return r;
+}
+template <int L>
+PHC_DEV typename Prec<L>::C smul(const typename Prec<L>::C& a, const typename Prec<L>::C& b) {
+  if constexpr (L == 4) return cmul_ool<L>(a, b);
+  else return Prec<L>::mul(a, b);
+}
+
+// partial rows written by other CTAs: read through L2 (ld.global.cg), never a stale L1 line
+template <int L>
+PHC_DEV typename Prec<L>::C cload_cg(const double* p) {
+  typename Prec<L>::C v;
+  double d[2 * L];
+#pragma unroll
+  for (int q = 0; q < 2 * L; q += 2) {
+    double2 t = __ldcg(reinterpret_cast<const double2*>(p + q));
+    d[q] = t.x;
+    d[q + 1] = t.y;
+  }
+#pragma unroll
+  for (int q = 0; q < L; ++q) { v.re.x[q] = d[q]; v.im.x[q] = d[L + q]; }
+  return v;
 }
 
 template <int L>
@@ -113,19 +157,27 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
       u = sload<L>(pt + ((size_t)v * twoE + e - 1) * cd);
       d = sload<L>(pt + ((size_t)v * twoE + a.E + e - 1) * cd);
     }
-    C pre = (lane == 0) ? P::mul(c, u) : u;  // psi with the coefficient folded in
-    C suf = u;                                // phi
-#pragma unroll
+    // every lane multiplies (by 1 where the scan has no partner): no divergence around the
+    // out-of-line product
+    C pre = smul<L>(lane == 0 ? c : P::one(), u);  // psi with the coefficient folded in
+    C suf = u;                                     // phi
+#pragma unroll 1
     for (int off = 1; off < 32; off <<= 1) {
       const C x1 = shfl_c<L>(pre, off, true), x2 = shfl_c<L>(suf, off, false);
-      if (lane >= off) pre = P::mul(x1, pre);
-      if (lane + off < 32) suf = P::mul(suf, x2);
+      if constexpr (L == 4) {
+        const CPair<L> r = cmul2_ool<L>(lane >= off ? x1 : P::one(), pre, suf, lane + off < 32 ? x2 : P::one());
+        pre = r.a;
+        suf = r.b;
+      } else {
+        pre = P::mul(lane >= off ? x1 : P::one(), pre);
+        suf = P::mul(suf, lane + off < 32 ? x2 : P::one());
+      }
     }
     C before = shfl_c<L>(pre, 1, true), after = shfl_c<L>(suf, 1, false);
     if (lane == 0) before = c;
     if (lane == 31) after = P::one();
+    const C g = smul<L>(smul<L>(before, d), after);
     if (lane < k) {
-      const C g = P::mul(P::mul(before, d), after);
       double* acc = myrow + (size_t)v * cd;
       sstore<L>(acc, P::add(sload<L>(acc), g));
     }
@@ -159,26 +211,25 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
       cstore<L>(a.part + (((p * a.n_eq + i) * a.S + s) * (int64_t)(a.n_var + 1) + col) * cd, acc);
     }
   }
-}
-
-// Sum of the S partial rows in split order (S > 1).
-template <int L>
-__global__ void scan_reduce_kernel(const ScanArgs a) {
-  using P = Prec<L>;
-  constexpr int cd = 2 * L;
-  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t per_point = (int64_t)a.n_eq * (a.n_var + 1);
-  if (gid >= a.n_points * per_point) return;
-  const int64_t p = gid / per_point;
-  const int i = (int)((gid % per_point) / (a.n_var + 1));
-  const int col = (int)(gid % (a.n_var + 1));
-  const double* src = a.part + (((p * a.n_eq + i) * a.S) * (int64_t)(a.n_var + 1) + col) * cd;
-  typename P::C acc = cload<L>(src);
-  for (int s = 1; s < a.S; ++s) acc = P::add(acc, cload<L>(src + (size_t)s * (a.n_var + 1) * cd));
-  if (col < a.n_var)
-    cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)a.n_var + col) * cd, acc);
-  else
-    cstore<L>(a.F + (p * a.n_eq + i) * cd, acc);
+  if (direct) return;
+  // the last CTA of (p, i) to arrive sums the S partial rows in split order
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(a.count + p * a.n_eq + i, 1) == a.S - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  const double* src = a.part + ((p * a.n_eq + i) * a.S) * (int64_t)(a.n_var + 1) * cd;
+  for (int col = threadIdx.x; col <= a.n_var; col += blockDim.x) {
+    C acc = cload_cg<L>(src + (size_t)col * cd);
+    for (int q = 1; q < a.S; ++q) acc = P::add(acc, cload_cg<L>(src + ((size_t)q * (a.n_var + 1) + col) * cd));
+    if (col < a.n_var)
+      cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)a.n_var + col) * cd, acc);
+    else
+      cstore<L>(a.F + (p * a.n_eq + i) * cd, acc);
+  }
+  if (threadIdx.x == 0) a.count[p * a.n_eq + i] = 0;  // ready for the next call
 }
 
 }  // namespace phc

@@ -100,6 +100,8 @@ struct DeviceState {
   // latency (warp-scan) path: partial rows of the S splits
   double* part = nullptr;
   int64_t part_cap = 0;
+  int* count = nullptr;  // arrival counters (zeroed at allocation; each call leaves them zero)
+  int64_t count_cap = 0;
   // staging buffers for remote shards
   double* xs = nullptr;
   double* fs = nullptr;
@@ -111,7 +113,7 @@ struct DeviceState {
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
                     (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
-                    (void*)cl_q, (void*)cT, (void*)part})
+                    (void*)cl_q, (void*)cT, (void*)part, (void*)count})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (done) cudaEventDestroy(done);
@@ -345,6 +347,7 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
   a.S = s->scan_S;
   a.n_points = n_points;
   a.part = nullptr;
+  a.count = nullptr;
   if (s->scan_S > 1) {
     const int64_t need = n_points * s->n_eq * s->scan_S * (int64_t)(s->n_var + 1) * cd;
     if (need > d->part_cap) {
@@ -357,6 +360,18 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
       d->part_cap = need;
     }
     a.part = d->part;
+    const int64_t nc = n_points * s->n_eq;
+    if (nc > d->count_cap) {
+      cudaStreamSynchronize(st);
+      if (d->count) cudaFree(d->count);
+      d->count = nullptr;
+      d->count_cap = 0;
+      int rc = dalloc(&d->count, (size_t)nc);
+      if (rc) return rc;
+      CUDA_TRY(cudaMemset(d->count, 0, nc * sizeof(int)));
+      d->count_cap = nc;
+    }
+    a.count = d->count;
   }
   ProfScope ps(s, d->dev, 3, st);
   auto kern = phc::poly_scan_kernel<L>;
@@ -364,10 +379,6 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
     CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->scan_smem));
   const int64_t ctas = n_points * s->n_eq * s->scan_S;
   kern<<<(unsigned)ctas, s->scan_W * 32, s->scan_smem, st>>>(a);
-  if (s->scan_S > 1) {
-    const int64_t nth = n_points * s->n_eq * (int64_t)(s->n_var + 1);
-    phc::scan_reduce_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(a);
-  }
   CUDA_TRY(cudaGetLastError());
   return PHC_OK;
 }
