@@ -97,6 +97,9 @@ int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double*
 
 /* End-to-end convenience: x, f, jac are HOST pointers (pinned or pageable); copies in,
  * evaluates n_points points on the home device (or sharded as above) and copies out.
+ * On one device the call is a pipeline over chunks of points: the output copies of chunk c
+ * (J dominates the bytes) overlap the evaluation of chunk c+1 (pinned buffers needed for the
+ * overlap); results are bitwise those of phc_eval_jacobian_batch.
  * Synchronous: returns after f and jac are written. */
 int phc_eval_jacobian_batch_host(const phc_system* s, int64_t n_points, const double* x_host, double* f_host,
                                  double* jac_host, const int32_t* devices, int32_t n_devices);

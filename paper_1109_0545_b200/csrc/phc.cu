@@ -69,7 +69,8 @@ int dalloc(T** p, size_t n) {
 // replicated once per device at first use).
 struct DeviceState {
   int dev = -1;
-  cudaStream_t stream = nullptr;  // internal stream for non-home shards
+  cudaStream_t stream = nullptr;   // internal stream for non-home shards
+  cudaStream_t stream2 = nullptr;  // gather stream of the non-home shards
   cudaEvent_t done = nullptr;
   // generic path tables
   int64_t* term_ptr = nullptr;
@@ -116,6 +117,7 @@ struct DeviceState {
                     (void*)cl_q, (void*)cT, (void*)part, (void*)count})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
     if (done) cudaEventDestroy(done);
   }
 };
@@ -151,6 +153,7 @@ struct phc_system {
   double *hx = nullptr, *hf = nullptr, *hj = nullptr;
   int64_t h_cap = 0;
   cudaStream_t hstream = nullptr;
+  cudaStream_t hstream2 = nullptr;  // D2H stream of the pipelined host call
   // kernel timing (phc_profile_*): events on the launch stream, home device only
   bool prof = false;
   struct Rec { int cls; cudaEvent_t a, b; };
@@ -226,6 +229,7 @@ int get_device_state(phc_system* s, int dev, DeviceState** out) {
   std::unique_ptr<DeviceState> d(new DeviceState());
   d->dev = dev;
   CUDA_TRY(cudaStreamCreateWithFlags(&d->stream, cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&d->stream2, cudaStreamNonBlocking));
   CUDA_TRY(cudaEventCreateWithFlags(&d->done, cudaEventDisableTiming));
   int rc;
   if ((rc = dalloc(&d->term_ptr, s->term_ptr.size()))) return rc;
@@ -695,6 +699,7 @@ void phc_system_destroy(phc_system* s) {
     if (s->hf) cudaFree(s->hf);
     if (s->hj) cudaFree(s->hj);
     if (s->hstream) cudaStreamDestroy(s->hstream);
+    if (s->hstream2) cudaStreamDestroy(s->hstream2);
   }
   s->devs.clear();
   {
@@ -769,16 +774,35 @@ static int eval_batch_impl(const phc_system* cs, int64_t n_points, const double*
       rc = fail(PHC_ECUDA, "scatter copy (t) failed");
       break;
     }
-    if ((rc = run_on_device(s, d, np, d->xs, T ? d->ts : nullptr, d->fs, d->js, d->stream, n_points))) break;
-    if (cudaMemcpyPeerAsync(f + p0 * s->n_eq * cd, s->home, d->fs, dv, np * s->n_eq * cd * 8, d->stream) != cudaSuccess ||
-        cudaMemcpyPeerAsync(jac + p0 * (int64_t)s->n_eq * s->n_var * cd, s->home, d->js, dv,
-                            np * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream) != cudaSuccess) {
-      rc = fail(PHC_ECUDA, "gather copy failed");
-      break;
+    // the shard in chunks: evaluation of chunk c on d->stream, its gather to the home device
+    // over NVLink on d->stream2, so the gather overlaps the evaluation of the next chunks
+    // (SURVEY.md §8(e) option 2).  call_points = the call's total: same regime, same bits.
+    const int64_t nch = np >= 8192 ? 4 : 1;
+    for (int64_t c = 0; c < nch && rc == PHC_OK; ++c) {
+      const int64_t q0 = c * np / nch, q1 = (c + 1) * np / nch, nq = q1 - q0;
+      if (nq == 0) continue;
+      if ((rc = run_on_device(s, d, nq, d->xs + q0 * s->n_var * cd, T ? d->ts + q0 * s->L : nullptr,
+                              d->fs + q0 * s->n_eq * cd, d->js + q0 * (int64_t)s->n_eq * s->n_var * cd, d->stream,
+                              n_points)))
+        break;
+      cudaEvent_t ce;
+      cudaEventCreateWithFlags(&ce, cudaEventDisableTiming);
+      cudaEventRecord(ce, d->stream);
+      cudaStreamWaitEvent(d->stream2, ce, 0);
+      cudaEventDestroy(ce);
+      if (cudaMemcpyPeerAsync(f + (p0 + q0) * s->n_eq * cd, s->home, d->fs + q0 * s->n_eq * cd, dv,
+                              nq * s->n_eq * cd * 8, d->stream2) != cudaSuccess ||
+          cudaMemcpyPeerAsync(jac + (p0 + q0) * (int64_t)s->n_eq * s->n_var * cd, s->home,
+                              d->js + q0 * (int64_t)s->n_eq * s->n_var * cd, dv,
+                              nq * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream2) != cudaSuccess) {
+        rc = fail(PHC_ECUDA, "gather copy failed");
+        break;
+      }
     }
+    if (rc) break;
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    cudaEventRecord(e, d->stream);
+    cudaEventRecord(e, d->stream2);
     dones.push_back(e);
   }
   for (cudaEvent_t e : dones) {
@@ -1137,13 +1161,52 @@ int phc_eval_jacobian_batch_host(const phc_system* cs, int64_t n_points, const d
     if ((rc = dalloc(&s->hj, (size_t)(n_points * (int64_t)s->n_eq * s->n_var * cd)))) return rc;
     s->h_cap = n_points;
   }
-  CUDA_TRY(cudaMemcpyAsync(s->hx, x_host, n_points * s->n_var * cd * 8, cudaMemcpyHostToDevice, s->hstream));
-  int rc = phc_eval_jacobian_batch(s, n_points, s->hx, s->hf, s->hj, devices, n_devices, s->hstream);
+  const bool single = !devices || n_devices <= 0 || (n_devices == 1 && devices[0] == s->home);
+  if (!single) {
+    CUDA_TRY(cudaMemcpyAsync(s->hx, x_host, n_points * s->n_var * cd * 8, cudaMemcpyHostToDevice, s->hstream));
+    int rc = phc_eval_jacobian_batch(s, n_points, s->hx, s->hf, s->hj, devices, n_devices, s->hstream);
+    if (rc) return rc;
+    CUDA_TRY(cudaMemcpyAsync(f_host, s->hf, n_points * s->n_eq * cd * 8, cudaMemcpyDeviceToHost, s->hstream));
+    CUDA_TRY(cudaMemcpyAsync(jac_host, s->hj, n_points * (int64_t)s->n_eq * s->n_var * cd * 8,
+                             cudaMemcpyDeviceToHost, s->hstream));
+    CUDA_TRY(cudaStreamSynchronize(s->hstream));
+    return PHC_OK;
+  }
+  // one device: a pipeline over chunks of points -- H2D and evaluation of chunk c on
+  // hstream, its D2H on a second stream, so the output copies (the bulk of the bytes: J)
+  // overlap the evaluation of the following chunks.  Every chunk is evaluated with the
+  // call's total point count as its regime (run_on_device call_points), so the results are
+  // bitwise those of the unchunked call.
+  if (!s->hstream2) CUDA_TRY(cudaStreamCreateWithFlags(&s->hstream2, cudaStreamNonBlocking));
+  DeviceState* d;
+  int rc = get_device_state(s, s->home, &d);
   if (rc) return rc;
-  CUDA_TRY(cudaMemcpyAsync(f_host, s->hf, n_points * s->n_eq * cd * 8, cudaMemcpyDeviceToHost, s->hstream));
-  CUDA_TRY(cudaMemcpyAsync(jac_host, s->hj, n_points * (int64_t)s->n_eq * s->n_var * cd * 8, cudaMemcpyDeviceToHost,
-                           s->hstream));
-  CUDA_TRY(cudaStreamSynchronize(s->hstream));
+  const int64_t chunks = n_points >= 8192 ? 8 : (n_points >= 1024 ? 4 : 1);
+  std::vector<cudaEvent_t> evs;
+  for (int64_t c = 0; c < chunks; ++c) {
+    const int64_t p0 = c * n_points / chunks, p1 = (c + 1) * n_points / chunks, np = p1 - p0;
+    if (np == 0) continue;
+    CUDA_TRY(cudaMemcpyAsync(s->hx + p0 * s->n_var * cd, x_host + p0 * s->n_var * cd, np * s->n_var * cd * 8,
+                             cudaMemcpyHostToDevice, s->hstream));
+    if ((rc = run_on_device(s, d, np, s->hx + p0 * s->n_var * cd, nullptr, s->hf + p0 * s->n_eq * cd,
+                            s->hj + p0 * (int64_t)s->n_eq * s->n_var * cd, s->hstream, n_points)))
+      break;
+    cudaEvent_t e;
+    CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    evs.push_back(e);
+    CUDA_TRY(cudaEventRecord(e, s->hstream));
+    CUDA_TRY(cudaStreamWaitEvent(s->hstream2, e, 0));
+    CUDA_TRY(cudaMemcpyAsync(f_host + p0 * s->n_eq * cd, s->hf + p0 * s->n_eq * cd, np * s->n_eq * cd * 8,
+                             cudaMemcpyDeviceToHost, s->hstream2));
+    CUDA_TRY(cudaMemcpyAsync(jac_host + p0 * (int64_t)s->n_eq * s->n_var * cd,
+                             s->hj + p0 * (int64_t)s->n_eq * s->n_var * cd,
+                             np * (int64_t)s->n_eq * s->n_var * cd * 8, cudaMemcpyDeviceToHost, s->hstream2));
+  }
+  cudaStreamSynchronize(s->hstream);
+  cudaStreamSynchronize(s->hstream2);
+  for (cudaEvent_t e : evs) cudaEventDestroy(e);
+  if (rc) return rc;
+  CUDA_TRY(cudaGetLastError());
   return PHC_OK;
 }
 

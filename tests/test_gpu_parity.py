@@ -244,3 +244,15 @@ def test_latency_path_vs_batch_path(phc, name):
         assert _limb_rel_diff(F[p], f.cpu().numpy()) <= TOL[s.limbs]
         assert _limb_rel_diff(J[p], j.cpu().numpy()) <= TOL[s.limbs]
         assert limbs_normalised(f.cpu().numpy()) and limbs_normalised(j.cpu().numpy())
+
+
+def test_host_pipeline_equals_device_call(phc):
+    """phc_eval_jacobian_batch_host pipelines 8 chunks (output copies overlapping the next
+    chunk's evaluation) at >= 8192 points: bitwise the device call's results."""
+    s, X = config_system("batch", seed=6, points=8200)
+    F, J, h = gpu_eval(phc, s, X)
+    Fh = torch.empty((X.shape[0], s.n_eq, 2, 2), dtype=torch.float64).pin_memory()
+    Jh = torch.empty((X.shape[0], s.n_eq, s.n_var, 2, 2), dtype=torch.float64).pin_memory()
+    Xh = torch.from_numpy(X).pin_memory()
+    h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy())
+    assert np.array_equal(F, Fh.numpy()) and np.array_equal(J, Jh.numpy())
