@@ -29,7 +29,7 @@ struct NewtonArgs {
 };
 
 template <int L, bool SMEM>
-__global__ void __launch_bounds__(256) newton_solve_kernel(const NewtonArgs a) {
+__global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   using P = Prec<L>;
   using C = typename P::C;
   extern __shared__ __align__(16) double nsm[];
