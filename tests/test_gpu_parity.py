@@ -162,11 +162,16 @@ def test_ragged_and_many_points(phc, L):
     coeff = unit_circle_limbs(rng.uniform(0, 6.283, T), L, 1)
     s = system_from_terms(n, n, L, polys, coeff)
     X = unit_circle_limbs(rng.uniform(0, 6.283, (37, n)), L, 1)
-    F, J, _ = gpu_eval(phc, s, X)
+    F, J, h = gpu_eval(phc, s, X)
     for p in (0, 17, 36):
         ar, Fr, Jr = oracle_point(s, X[p], arith="exact")
         ef, ej = compare_point(ar, Fr, Jr, F[p], J[p], L)
         assert ef <= TOL[L] and ej <= TOL[L], (p, ef, ej)
+        # the same point alone takes the latency path (one warp per term)
+        f1, j1 = h.eval(torch.from_numpy(X[p]).cuda())
+        torch.cuda.synchronize()
+        ef, ej = compare_point(ar, Fr, Jr, f1.cpu().numpy(), j1.cpu().numpy(), L)
+        assert ef <= TOL[L] and ej <= TOL[L], (p, "latency", ef, ej)
 
 
 def test_euler_identity_full_batch(phc):
