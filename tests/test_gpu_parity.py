@@ -11,7 +11,7 @@ torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
 from _parity import TOL, compare_point, limbs_normalised, oracle_point  # noqa: E402
-from oracle import ExactArith, evaluate_system  # noqa: E402
+from oracle import ExactArith, evaluate_system, rel_errors  # noqa: E402
 from synthetic import (config_system, limbs_from_values, special_gaussian_system,  # noqa: E402
                        special_linear_system, system_from_terms, random_system, homogeneous_system)
 
@@ -261,3 +261,40 @@ def test_host_pipeline_equals_device_call(phc):
     Xh = torch.from_numpy(X).pin_memory()
     h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy())
     assert np.array_equal(F, Fh.numpy()) and np.array_equal(J, Jh.numpy())
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_compiled_maxima(phc, L):
+    """The compiled limits of include/phc.h: a term with k = PHC_MAX_K = 64 factors (generic
+    path), an exponent of PHC_MAX_EXP = 255, and n_var = PHC_MAX_VARS = 65534 (a sparse
+    system touching the last variable); against the mp512 oracle."""
+    from synthetic.systems import unit_circle_limbs
+    rng = np.random.default_rng(21)
+    n = 64
+    polys = [[[(v, int(rng.integers(1, 4))) for v in range(n)], [(5, 255)]],
+             [[(0, 255), (63, 1)], []],
+             [[(v, 1) for v in range(0, n, 2)]]]
+    T = sum(len(p) for p in polys)
+    coeff = unit_circle_limbs(rng.uniform(0, 6.283, T), L, 1)
+    s = system_from_terms(3, n, L, polys, coeff)
+    X = unit_circle_limbs(rng.uniform(0, 6.283, (1, n)), L, 1)
+    f, j, h = gpu_eval(phc, s, X)
+    assert h.stats["kmax"] == 64 and h.stats["D"] == 255 and h.stats["path"] == 0
+    ar, F, J = oracle_point(s, X[0], arith="mp")
+    ef, ej = compare_point(ar, F, J, f[0], j[0], L)
+    assert ef <= TOL[L] and ej <= TOL[L], (ef, ej)
+    # n_var at the limit, two sparse polynomials
+    nv = 65534
+    polys = [[[(0, 2), (nv - 1, 3)], [(nv // 2, 1)]], [[(nv - 1, 1)], []]]
+    coeff = unit_circle_limbs(rng.uniform(0, 6.283, 4), L, 1)
+    s2 = system_from_terms(2, nv, L, polys, coeff)
+    X2 = np.zeros((1, nv, 2, L))
+    X2[0, :, 0, 0] = 1.0
+    X2[0, [0, nv // 2, nv - 1]] = unit_circle_limbs(rng.uniform(0, 6.283, 3), L, 1)
+    f2, j2, _ = gpu_eval(phc, s2, X2)
+    ar, F2, J2 = oracle_point(s2, X2[0], arith="mp")
+    cols = [0, nv // 2, nv - 1, 1, 77]
+    ef = rel_errors(ar, F2, f2[0])[0]
+    ej = rel_errors(ar, [J2[i][c] for i in range(2) for c in cols], np.stack([j2[0][i, c] for i in range(2) for c in cols]))[0]
+    assert ef <= TOL[L] and ej <= TOL[L], (ef, ej)
+    assert np.count_nonzero(j2[0][..., 0, 0]) == 4
