@@ -148,6 +148,87 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
+// Small systems (n <= 32): one WARP per point, lane i owns row i of [J | -F] (in the warp's
+// slice of shared memory); no block barriers -- the pivot is a warp argmax, every lane
+// computes the pivot reciprocal itself (same inputs, same bits), the row swap is one column
+// per lane.  Same pivot rule, operations and order per entry as newton_solve_kernel, so the
+// two kernels give bitwise identical steps; this one avoids ~5 block barriers per column
+// (the tracker's corrector at n = 8: 26 us -> a few us per call).
+// ---------------------------------------------------------------------------------------
+template <int L>
+__global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  extern __shared__ __align__(16) double wsm[];
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
+  if (p >= a.n_points) return;  // warp-uniform
+  double* M = wsm + (size_t)wib * n * cols * cd;
+  auto at = [&](int i, int j) { return M + ((size_t)i * cols + j) * cd; };
+  const double* Fp = a.F + (size_t)p * n * cd;
+  const double* Jp = a.J + (size_t)p * n * n * cd;
+  double rmax = 0.0;
+  if (lane < n) {
+    for (int j = 0; j < n; ++j) sstore<L>(at(lane, j), cload<L>(Jp + ((size_t)lane * n + j) * cd));
+    const C f = cload<L>(Fp + (size_t)lane * cd);
+    rmax = sqrt(P::abs2_hi(f));
+    sstore<L>(at(lane, n), P::neg(f));
+  }
+  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  if (lane == 0) a.resid[p] = rmax;
+  __syncwarp();
+  C inv_diag = P::zero();  // lane i keeps 1 / U[i][i] for the back substitution
+  for (int k = 0; k < n; ++k) {
+    double best = -1.0;
+    int bi = n;
+    if (lane >= k && lane < n) {
+      best = P::abs2_hi(sload<L>(at(lane, k)));
+      bi = lane;
+    }
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (!(best > 0.0)) {  // zero pivot column: singular, x unchanged
+      for (int e = lane; e < n; e += 32)
+        cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
+      if (lane == 0) a.status[p] = 1;
+      return;
+    }
+    if (bi != k)
+      for (int j = k + lane; j < cols; j += 32) {
+        const C u = sload<L>(at(k, j)), v = sload<L>(at(bi, j));
+        sstore<L>(at(k, j), v);
+        sstore<L>(at(bi, j), u);
+      }
+    __syncwarp();
+    const C inv = P::recip(sload<L>(at(k, k)));
+    if (lane == k) inv_diag = inv;
+    if (lane > k && lane < n) {
+      const C l = P::mul(sload<L>(at(lane, k)), inv);
+      sstore<L>(at(lane, k), l);
+      for (int j = k + 1; j < cols; ++j) sstore<L>(at(lane, j), P::sub(sload<L>(at(lane, j)), P::mul(l, sload<L>(at(k, j)))));
+    }
+    __syncwarp();
+  }
+  // back substitution, column oriented as in newton_solve_kernel
+  for (int i = n - 1; i >= 0; --i) {
+    if (lane == i) sstore<L>(at(i, n), P::mul(sload<L>(at(i, n)), inv_diag));
+    __syncwarp();
+    const C xi = sload<L>(at(i, n));
+    if (lane < i) sstore<L>(at(lane, n), P::sub(sload<L>(at(lane, n)), P::mul(sload<L>(at(lane, i)), xi)));
+    __syncwarp();
+  }
+  if (lane < n) {
+    const double* xp = a.X + ((size_t)p * n + lane) * cd;
+    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), sload<L>(at(lane, n))));
+  }
+  if (lane == 0) a.status[p] = 0;
+}
+
+// ---------------------------------------------------------------------------------------
 // Multi-kernel elimination for systems whose augmented matrix does not fit shared memory
 // (e.g. n = 256 QD: 4.2 MB per point): every step k is two launches over all points of the
 // chunk, so the trailing update of one point spreads over many SMs instead of one CTA.

@@ -877,6 +877,22 @@ static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, 
     a.n = n;
     a.n_points = np;
     ProfScope ps(s, d->dev, 2, st);
+    // small systems: one warp per point (bitwise the same step as the CTA kernel)
+    const size_t per_warp = (size_t)n * (n + 1) * cd * sizeof(double);
+    if (n <= 32 && (n <= 16 || n_points < 4096)) {
+      const int wpc = per_warp * 4 <= (size_t)160 * 1024 ? 4 : (per_warp * 2 <= (size_t)160 * 1024 ? 2 : 1);
+      const size_t sm = per_warp * wpc;
+      const unsigned grid = (unsigned)((np + wpc - 1) / wpc);
+      if (L == 2) {
+        if (sm > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        phc::newton_warp_kernel<2><<<grid, wpc * 32, sm, st>>>(a);
+      } else {
+        if (sm > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        phc::newton_warp_kernel<4><<<grid, wpc * 32, sm, st>>>(a);
+      }
+      CUDA_TRY(cudaGetLastError());
+      continue;
+    }
     if (L == 2) {
       if (smem) {
         if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
@@ -1023,9 +1039,9 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   DevBuf<int32_t> n_hist, idx_d, clip_d, acc_d, nst_d;
   if ((rc = dalloc(&t_hist.p, (size_t)(P * 3 * L))) || (rc = dalloc(&x_hist.p, (size_t)(P * 3 * n * cd))) ||
       (rc = dalloc(&lam_d.p, (size_t)P)) || (rc = dalloc(&tc.p, (size_t)(P * L))) ||
-      (rc = dalloc(&xc.p, (size_t)(P * n * cd))) || (rc = dalloc(&res_d.p, (size_t)P)) ||
+      (rc = dalloc(&xc.p, (size_t)(P * n * cd))) || (rc = dalloc(&res_d.p, (size_t)P * q.max_newton)) ||
       (rc = dalloc(&n_hist.p, (size_t)P)) || (rc = dalloc(&idx_d.p, (size_t)P)) || (rc = dalloc(&clip_d.p, (size_t)P)) ||
-      (rc = dalloc(&acc_d.p, (size_t)P)) || (rc = dalloc(&nst_d.p, (size_t)P)))
+      (rc = dalloc(&acc_d.p, (size_t)P)) || (rc = dalloc(&nst_d.p, (size_t)P * q.max_newton)))
     return rc;
   auto grid = [](int64_t nth) { return (unsigned)((nth + 127) / 128); };
   if (L == 2)
@@ -1034,8 +1050,8 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
     phc::track_init_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
   CUDA_TRY(cudaGetLastError());
   // host-side per-path control state (Alg. 1 step_size_control / stop_criterion)
-  std::vector<double> lam((size_t)P, q.step_init), res((size_t)P);
-  std::vector<int32_t> stat((size_t)P, 0), idx, clip((size_t)P), acc((size_t)P), nst((size_t)P);
+  std::vector<double> lam((size_t)P, q.step_init), res((size_t)P * q.max_newton);
+  std::vector<int32_t> stat((size_t)P, 0), idx, clip((size_t)P), acc((size_t)P), nst((size_t)P * q.max_newton);
   std::vector<int64_t> steps((size_t)P, 0), succ((size_t)P, 0), iters((size_t)P, 0);
   std::vector<double> min_step((size_t)P, 1e300), sum_step((size_t)P, 0.0);
   while (true) {
@@ -1055,24 +1071,26 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
                                                            q.predictor, tc.p, xc.p, clip_d.p);
     CUDA_TRY(cudaGetLastError());
     CUDA_TRY(cudaMemcpyAsync(clip.data(), clip_d.p, A * 4, cudaMemcpyDeviceToHost, st));
-    // correct: Alg. 2 on h(., t_try) until the residual passes tol or max_newton iterations
+    // correct: Alg. 2 on h(., t_try).  All max_newton iterations are enqueued back to back
+    // (one host synchronisation per tracker step instead of one per iteration); iteration k
+    // records its residual and status in row k.  A path is corrected at the first iteration
+    // whose residual passes tol (Alg. 2 applies that iteration's update too); the iterations
+    // after it only refine the point further (documented deviation, reading T1).
+    for (int k = 0; k < q.max_newton; ++k)
+      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p + (size_t)k * A, nst_d.p + (size_t)k * A, st))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(res.data(), res_d.p, (size_t)q.max_newton * A * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(nst.data(), nst_d.p, (size_t)q.max_newton * A * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<char> conv((size_t)A, 0), bad((size_t)A, 0);
-    for (int k = 0; k < q.max_newton; ++k) {
-      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p, nst_d.p, st))) return rc;
-      CUDA_TRY(cudaMemcpyAsync(res.data(), res_d.p, A * 8, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaMemcpyAsync(nst.data(), nst_d.p, A * 4, cudaMemcpyDeviceToHost, st));
-      CUDA_TRY(cudaStreamSynchronize(st));
-      bool all = true;
-      for (int64_t a = 0; a < A; ++a) {
-        if (conv[a] || bad[a]) continue;
+    for (int64_t a = 0; a < A; ++a) {
+      for (int k = 0; k < q.max_newton && !conv[a] && !bad[a]; ++k) {
         iters[idx[a]]++;
-        if (nst[a] != 0 || !std::isfinite(res[a]))
+        const double r = res[(size_t)k * A + a];
+        if (nst[(size_t)k * A + a] != 0 || !std::isfinite(r))
           bad[a] = 1;
-        else if (res[a] <= q.tol)
-          conv[a] = 1;  // Alg. 2 applies this iteration's update too: xc holds it
-        all = all && (conv[a] || bad[a]);
+        else if (r <= q.tol)
+          conv[a] = 1;
       }
-      if (all) break;
     }
     // step-size control, step back, stop criterion (Alg. 1; SPEC tracker defaults)
     for (int64_t a = 0; a < A; ++a) {

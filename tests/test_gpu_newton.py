@@ -173,3 +173,18 @@ def test_newton_multi_kernel_singular(phc):
     xn, res, status, h = _gpu_step(phc, s, X)
     assert (status == 1).all()
     assert np.array_equal(xn, X)
+
+
+@pytest.mark.parametrize("name", ["c2", "batch"])
+def test_warp_and_cta_eliminations_agree_bitwise(phc, name):
+    """16 < n <= 32: below 4,096 points the elimination runs one warp per point, from 4,096 on
+    one CTA per point; both perform the same operations in the same order, so the steps are
+    bitwise equal (4,096 vs 4,095 points: the evaluation takes the batch kernel in both)."""
+    s, X = config_system(name, seed=4, points=4096)
+    h = phc.System(s)
+    Xd = torch.from_numpy(X).cuda()
+    Xa, ra, sa = h.newton_step(Xd)          # 4,096 points: CTA kernel
+    Xb, rb, sb = h.newton_step(Xd[:4095])   # 4,095 points: warp kernel
+    torch.cuda.synchronize()
+    assert (sa == 0).all() and (sb == 0).all()
+    assert torch.equal(Xa[:4095], Xb) and torch.equal(ra[:4095], rb)
