@@ -33,6 +33,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "arith.cuh"
@@ -498,6 +500,21 @@ block_kernel(const BlockArgs a) {
 // ---------------------------------------------------------------------------
 // host side: plan (blocks, edge colouring, packing), upload, launch
 // ---------------------------------------------------------------------------
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device) and size: the
+// attribute call costs microseconds, and the tracker's corrector launches thousands of times.
+inline cudaError_t ensure_smem(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& v = done[{func, dev}];
+  if (v >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) v = bytes;
+  return e;
+}
+
 inline int compiled_K(int kmax) {
   static const int ks[] = {2, 4, 8, 12, 16, 20, 24, 32};
   for (int k : ks)
@@ -653,9 +670,14 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
     }
   }
-  // mode A (a warp owns whole polynomials) when every polynomial is one block; mode B (a CTA
-  // owns a polynomial, its warps split the blocks) otherwise, with one warp per block up to 8
-  plan->mode = max_blocks_per_poly >= 2 ? 1 : 0;
+  // mode A (a warp owns whole polynomials, the CTA's power table serves up to 4 nw of them)
+  // or mode B (a CTA owns a polynomial, its warps split the blocks, one warp per block up to
+  // 8).  Calls with few points take the latency path (kernels_scan.cuh), so this kernel
+  // serves batches and large systems.  Mode B pays the power table once per polynomial:
+  // worth it for long polynomials (>= 4 blocks) or heavy terms (K >= 12: c3 x 4,096 points
+  // 7.1 -> 6.8 us/eval), not for light multi-block ones (a total-degree tracker system with
+  // k <= 2: 141 -> 85 us per 1,024 points in mode A).
+  plan->mode = (max_blocks_per_poly >= 4 || (max_blocks_per_poly >= 2 && K >= 12)) ? 1 : 0;
   const int nw = plan->mode == 1 ? std::min(max_blocks_per_poly, 8) : block_warps(L, layout);
   plan->nw = nw;
   if (layout == 2) {
@@ -727,7 +749,7 @@ template <int L, int K, int LAYOUT>
 int launch_block_k(const HostBlockPlan& plan, const BlockArgs& a, int64_t n_points, cudaStream_t st) {
   auto kern = a.coef2 ? block_kernel<L, K, LAYOUT, true> : block_kernel<L, K, LAYOUT, false>;
   if (plan.smem_bytes > 48 * 1024)
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)plan.smem_bytes) != cudaSuccess)
+    if (ensure_smem((const void*)kern, plan.smem_bytes) != cudaSuccess)
       return -3;
   const int64_t units = a.mode == 0 ? (a.n_eq + a.polys_per_cta - 1) / a.polys_per_cta : a.n_eq;
   const int64_t max_grid = (int64_t)1 << 30;

@@ -380,7 +380,7 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
   ProfScope ps(s, d->dev, 3, st);
   auto kern = phc::poly_scan_kernel<L>;
   if (s->scan_smem > 48 * 1024)
-    CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s->scan_smem));
+    CUDA_TRY(phc::ensure_smem((const void*)kern, s->scan_smem));
   const int64_t ctas = n_points * s->n_eq * s->scan_S;
   kern<<<(unsigned)ctas, s->scan_W * 32, s->scan_smem, st>>>(a);
   CUDA_TRY(cudaGetLastError());
@@ -884,10 +884,10 @@ static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, 
       const size_t sm = per_warp * wpc;
       const unsigned grid = (unsigned)((np + wpc - 1) / wpc);
       if (L == 2) {
-        if (sm > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_warp_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (sm > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_warp_kernel<2>, sm));
         phc::newton_warp_kernel<2><<<grid, wpc * 32, sm, st>>>(a);
       } else {
-        if (sm > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_warp_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+        if (sm > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_warp_kernel<4>, sm));
         phc::newton_warp_kernel<4><<<grid, wpc * 32, sm, st>>>(a);
       }
       CUDA_TRY(cudaGetLastError());
@@ -895,14 +895,14 @@ static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, 
     }
     if (L == 2) {
       if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
+        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2, true>, mat));
         phc::newton_solve_kernel<2, true><<<(unsigned)np, threads, mat, st>>>(a);
       } else {
         newton_multi<2>(a, np, st);
       }
     } else {
       if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(cudaFuncSetAttribute(phc::newton_solve_kernel<4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)mat));
+        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4, true>, mat));
         phc::newton_solve_kernel<4, true><<<(unsigned)np, threads, mat, st>>>(a);
       } else {
         newton_multi<4>(a, np, st);
