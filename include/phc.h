@@ -32,8 +32,12 @@
  * handle concurrently on different streams (calls on one stream are fine).
  *
  * Determinism.  For a given system and point the results are bitwise reproducible:
- * every sum is taken in a fixed order, independent of the launch configuration,
- * of n_points and of the device list of a batch call.
+ * every sum is taken in a fixed order, independent of the launch configuration and of
+ * the device list or chunking of a batch call.  Two regimes exist per system (DESIGN.md
+ * reading N2-2): calls whose total point count times the number of terms is at most
+ * 148 * 32 take the latency path (one warp per term), larger calls the batch kernels;
+ * the regime is chosen from the call's total point count, each regime is deterministic,
+ * and the two agree within the DD/QD tolerance (not bitwise).
  */
 #ifndef PHC_H
 #define PHC_H
