@@ -132,8 +132,9 @@ int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x
  *   coeff    [n_eq][n_mono][2][limbs]  dense coefficient matrix C (HOST pointer, copied)
  * The handle works with phc_eval_jacobian[_batch][_host] and phc_newton_step_batch (same
  * layouts and semantics).  Each monomial and its partials are evaluated once per point,
- * then [F | J] = C [V | D] (D: the partials, sparse).  Homotopy coefficients are not
- * supported on these handles (PHC_EUNSUPPORTED). */
+ * then [F | J] = C [V | D] (D: the partials, sparse).  phc_system_set_target attaches a
+ * dense target matrix [n_eq][n_mono][2][limbs]; the homotopy calls then blend
+ * C(t) = (1 - t) C + t C_target entry by entry inside the coefficient product. */
 int phc_system_create_common(phc_system** out, int32_t n_eq, int32_t n_var, int32_t limbs, int64_t n_mono,
                              const int64_t* mono_ptr, const int32_t* var_idx, const int32_t* exponent,
                              const double* coeff, int32_t device);
@@ -148,7 +149,8 @@ int phc_system_create_common(phc_system** out, int32_t n_eq, int32_t n_var, int3
  * --------------------------------------------------------------------------------------- */
 
 /* Attach target coefficients coeff_target [n_terms][2][limbs] (HOST pointer, deep-copied,
- * same term order as coeff) and upload them to every device the handle uses.  Calling it
+ * same term order as coeff; for a common-support handle the dense [n_eq][n_mono][2][limbs]
+ * matrix) and upload them to every device the handle uses.  Calling it
  * again replaces them (the home device is synchronised first).  PHC_EINVAL on NULL or
  * non-finite limbs.  The plain eval calls keep evaluating the start coefficients. */
 int phc_system_set_target(phc_system* s, const double* coeff_target);

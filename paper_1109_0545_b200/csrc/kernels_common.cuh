@@ -26,6 +26,7 @@ namespace phc {
 template <int L, int TI>
 __global__ void coef_product_kernel(const int64_t* __restrict__ cl_ptr, const int32_t* __restrict__ cl_j,
                                     const int64_t* __restrict__ cl_q, const double* __restrict__ cT,
+                                    const double* __restrict__ cT2, const double* __restrict__ T,
                                     const double* __restrict__ Y, const double* __restrict__ G, int n_eq, int n_var,
                                     int64_t M, int64_t n_factors, int64_t n_points, double* __restrict__ F,
                                     double* __restrict__ J) {
@@ -43,6 +44,11 @@ __global__ void coef_product_kernel(const int64_t* __restrict__ cl_ptr, const in
   C acc[TI];
 #pragma unroll
   for (int u = 0; u < TI; ++u) acc[u] = P::zero();
+  typename P::real tt = P::one().re, omt = P::one().re;
+  if (cT2) {
+    tt = P::rload(T + p * L);
+    omt = P::one_minus(tt);
+  }
   const double* Yp = Y + p * M * cd;
   const double* Gp = G + p * n_factors * cd;
   for (int64_t e = cl_ptr[c]; e < cl_ptr[c + 1]; ++e) {
@@ -51,7 +57,12 @@ __global__ void coef_product_kernel(const int64_t* __restrict__ cl_ptr, const in
     const double* crow = cT + ((int64_t)j * n_eq + i0) * cd;
 #pragma unroll
     for (int u = 0; u < TI; ++u)
-      if (i0 + u < n_eq) acc[u] = P::add_lazy(acc[u], P::mul_lazy(cload<L>(crow + u * cd), val));
+      if (i0 + u < n_eq) {
+        C c = cload<L>(crow + u * cd);
+        if (cT2)  // homotopy (NEXT-3): c(t) = (1 - t) c_s + t c_f
+          c = P::add(P::mul_real(c, omt), P::mul_real(cload<L>(cT2 + ((int64_t)j * n_eq + i0 + u) * cd), tt));
+        acc[u] = P::add_lazy(acc[u], P::mul_lazy(c, val));
+      }
   }
 #pragma unroll
   for (int u = 0; u < TI; ++u) {
@@ -125,6 +136,7 @@ __global__ void monomial_scan_kernel(const int64_t* __restrict__ term_ptr, const
 template <int L>
 __global__ void coef_product_split_kernel(const int64_t* __restrict__ cl_ptr, const int32_t* __restrict__ cl_j,
                                           const int64_t* __restrict__ cl_q, const double* __restrict__ cT,
+                                          const double* __restrict__ cT2, const double* __restrict__ T,
                                           const double* __restrict__ Y, const double* __restrict__ G, int n_eq,
                                           int n_var, int64_t M, int64_t n_factors, int64_t n_points,
                                           double* __restrict__ F, double* __restrict__ J) {
@@ -141,10 +153,17 @@ __global__ void coef_product_split_kernel(const int64_t* __restrict__ cl_ptr, co
   const double* Yp = Y + p * M * cd;
   const double* Gp = G + p * n_factors * cd;
   C acc = P::zero();
+  typename P::real tt = P::one().re, omt = P::one().re;
+  if (cT2) {
+    tt = P::rload(T + p * L);
+    omt = P::one_minus(tt);
+  }
   for (int64_t e = cl_ptr[c] + lane; e < cl_ptr[c + 1]; e += 32) {
     const int j = cl_j[e];
     const C val = (c == 0) ? cload<L>(Yp + (int64_t)j * cd) : cload<L>(Gp + cl_q[e] * cd);
-    acc = P::add_lazy(acc, P::mul_lazy(cload<L>(cT + ((int64_t)j * n_eq + i) * cd), val));
+    C cf = cload<L>(cT + ((int64_t)j * n_eq + i) * cd);
+    if (cT2) cf = P::add(P::mul_real(cf, omt), P::mul_real(cload<L>(cT2 + ((int64_t)j * n_eq + i) * cd), tt));
+    acc = P::add_lazy(acc, P::mul_lazy(cf, val));
   }
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {

@@ -85,6 +85,7 @@ struct DeviceState {
   int32_t* cl_j = nullptr;
   int64_t* cl_q = nullptr;
   double* cT = nullptr;
+  double* cT2 = nullptr;  // homotopy target of a common-support system
   // block path tables
   phc::BlockTables bt{};
   bool have_block = false;
@@ -114,7 +115,7 @@ struct DeviceState {
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
                     (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
-                    (void*)cl_q, (void*)cT, (void*)part, (void*)count})
+                    (void*)cl_q, (void*)cT, (void*)part, (void*)count, (void*)cT2})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (stream2) cudaStreamDestroy(stream2);
@@ -138,6 +139,8 @@ struct phc_system {
   // NEXT-2 common-support system: "terms" are the M shared monomials (unit coefficients),
   // C^T [M][n_eq][2][L] and the per-column lists of the coefficient product
   bool common = false;
+  bool has_target = false;    // NEXT-3 target attached (coeff2, or cT2 for common systems)
+  std::vector<double> cT2;    // common systems: target C^T [M][n_eq][2][L]
   // latency path (kernels_scan.cuh): eligible when k <= 32 and the CTA's table + rows fit
   bool scan_ok = false;
   int scan_S = 1, scan_W = 8;
@@ -208,6 +211,10 @@ int upload(void* dst, const void* src, size_t bytes) {
 int upload_target(const phc_system* s, DeviceState* d) {
   DeviceGuard g(d->dev);
   int rc;
+  if (s->common) {
+    if (!d->cT2 && (rc = dalloc(&d->cT2, s->cT2.size()))) return rc;
+    return upload(d->cT2, s->cT2.data(), s->cT2.size() * 8);
+  }
   if (!d->coeff2 && (rc = dalloc(&d->coeff2, s->coeff2.size()))) return rc;
   if ((rc = upload(d->coeff2, s->coeff2.data(), s->coeff2.size() * 8))) return rc;
   if (s->plan.usable) {
@@ -248,7 +255,7 @@ int get_device_state(phc_system* s, int dev, DeviceState** out) {
     if ((rc = phc::upload_block_tables(s->plan, &d->bt))) return fail(rc, "block table upload failed");
     d->have_block = true;
   }
-  if (!s->coeff2.empty() && (rc = upload_target(s, d.get()))) return rc;
+  if (s->has_target && (rc = upload_target(s, d.get()))) return rc;
   if (s->common) {
     if ((rc = dalloc(&d->cl_ptr, s->cl_ptr.size()))) return rc;
     if ((rc = dalloc(&d->cl_j, s->cl_j.size()))) return rc;
@@ -397,8 +404,8 @@ inline bool common_split(const phc_system* s, int64_t call_points) {
 }
 
 template <int L>
-int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, double* f, double* jac,
-               bool split, cudaStream_t st) {
+int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
+               double* jac, bool split, cudaStream_t st) {
   int rc = ensure_scratch(s, d, n_points);
   if (rc) return rc;
   const int64_t cd = 2 * L;
@@ -430,12 +437,12 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
     if (split) {
       const int64_t nwarps = np * (s->n_var + 1) * s->n_eq;
       phc::coef_product_split_kernel<L><<<(unsigned)((nwarps * 32 + 255) / 256), 256, 0, st>>>(
-          d->cl_ptr, d->cl_j, d->cl_q, d->cT, d->Y, d->G, s->n_eq, s->n_var, s->n_terms, s->n_factors, np,
-          f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+          d->cl_ptr, d->cl_j, d->cl_q, d->cT, T ? d->cT2 : nullptr, T ? T + p0 * L : nullptr, d->Y, d->G, s->n_eq,
+          s->n_var, s->n_terms, s->n_factors, np, f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
     } else {
       phc::coef_product_kernel<L, TI><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(
-          d->cl_ptr, d->cl_j, d->cl_q, d->cT, d->Y, d->G, s->n_eq, s->n_var, s->n_terms, s->n_factors, np,
-          f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+          d->cl_ptr, d->cl_j, d->cl_q, d->cT, T ? d->cT2 : nullptr, T ? T + p0 * L : nullptr, d->Y, d->G, s->n_eq,
+          s->n_var, s->n_terms, s->n_factors, np, f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
     }
     CUDA_TRY(cudaGetLastError());
   }
@@ -448,10 +455,9 @@ int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const d
                   double* jac, cudaStream_t st, int64_t call_points = -1) {
   if (n_points <= 0) return PHC_OK;
   if (s->common) {
-    if (T) return fail(PHC_EUNSUPPORTED, "homotopy coefficients are not supported on common-support systems");
     const bool split = common_split(s, call_points < 0 ? n_points : call_points);
-    return s->L == 2 ? run_common<2>(s, d, n_points, x, f, jac, split, st)
-                     : run_common<4>(s, d, n_points, x, f, jac, split, st);
+    return s->L == 2 ? run_common<2>(s, d, n_points, x, T, f, jac, split, st)
+                     : run_common<4>(s, d, n_points, x, T, f, jac, split, st);
   }
   if (s->scan_ok && (call_points < 0 ? n_points : call_points) * s->n_terms <= kScanMaxTerms)
     return s->L == 2 ? run_scan<2>(s, d, n_points, x, T, f, jac, st) : run_scan<4>(s, d, n_points, x, T, f, jac, st);
@@ -822,7 +828,7 @@ int phc_eval_homotopy_batch(const phc_system* s, int64_t n_points, const double*
                             double* jac, const int32_t* devices, int32_t n_devices, void* stream) {
   g_err.clear();
   if (!s) return fail(PHC_EINVAL, "NULL system");
-  if (s->coeff2.empty()) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
   if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
   return eval_batch_impl(s, n_points, x, t, f, jac, devices, n_devices, stream);
 }
@@ -922,7 +928,7 @@ int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const 
                                    double* x_new, double* residual, int32_t* status, void* stream) {
   g_err.clear();
   if (!s) return fail(PHC_EINVAL, "NULL system");
-  if (s->coeff2.empty()) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
   if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
   return newton_impl(s, n_points, x, t, x_new, residual, status, stream);
 }
@@ -930,8 +936,29 @@ int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const 
 int phc_system_set_target(phc_system* s, const double* coeff_target) {
   g_err.clear();
   if (!s) return fail(PHC_EINVAL, "NULL system");
-  if (s->common) return fail(PHC_EUNSUPPORTED, "homotopy coefficients are not supported on common-support systems");
   if (s->n_terms > 0 && !coeff_target) return fail(PHC_EINVAL, "NULL coeff_target");
+  if (s->common) {  // dense target matrix [n_eq][n_mono][2][L], stored transposed
+    const int cd = 2 * s->L;
+    const size_t nc = (size_t)s->n_eq * s->n_terms * cd;
+    for (size_t q = 0; q < nc; ++q)
+      if (!std::isfinite(coeff_target[q])) return fail(PHC_EINVAL, "target coefficient limb %zu is not finite", q);
+    {
+      DeviceGuard g(s->home);
+      cudaDeviceSynchronize();
+    }
+    s->cT2.resize(nc);
+    for (int i = 0; i < s->n_eq; ++i)
+      for (int64_t j = 0; j < s->n_terms; ++j)
+        for (int c = 0; c < cd; ++c)
+          s->cT2[((size_t)j * s->n_eq + i) * cd + c] = coeff_target[((size_t)i * s->n_terms + j) * cd + c];
+    s->has_target = true;
+    std::lock_guard<std::mutex> lk(s->mu);
+    for (auto& kv : s->devs) {
+      int rc = upload_target(s, kv.second.get());
+      if (rc) return rc;
+    }
+    return PHC_OK;
+  }
   const size_t nc = (size_t)s->n_terms * 2 * s->L;
   for (size_t q = 0; q < nc; ++q)
     if (!std::isfinite(coeff_target[q])) return fail(PHC_EINVAL, "target coefficient limb %zu is not finite", q);
@@ -940,7 +967,8 @@ int phc_system_set_target(phc_system* s, const double* coeff_target) {
     cudaDeviceSynchronize();  // no evaluation may be reading the previous target
   }
   s->coeff2.assign(coeff_target, coeff_target + nc);
-  if (nc == 0) s->coeff2.assign(1, 0.0);  // a homotopy without terms: keep the flag
+  if (nc == 0) s->coeff2.assign(1, 0.0);
+  s->has_target = true;
   std::lock_guard<std::mutex> lk(s->mu);
   for (auto& kv : s->devs) {
     int rc = upload_target(s, kv.second.get());
@@ -1020,7 +1048,7 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   g_err.clear();
   phc_system* s = const_cast<phc_system*>(cs);
   if (!s || !prm) return fail(PHC_EINVAL, "NULL argument");
-  if (s->coeff2.empty()) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
   if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "tracking needs a square system");
   if (n_paths < 0) return fail(PHC_EINVAL, "n_paths < 0");
   if (n_paths == 0) return PHC_OK;

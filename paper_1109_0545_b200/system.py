@@ -32,12 +32,16 @@ class System:
         self.n_terms = int(tp.shape[0] - 1)
         self._h = None
         self.homotopy = False
+        self.common = False
         if hasattr(arrays, "mono_ptr"):
             # NEXT-2 common-support system: arrays.coeff is the dense [n_eq][n_mono][2][L] matrix
             mp = np.ascontiguousarray(arrays.mono_ptr, dtype=np.int64)
             self.n_terms = int(mp.shape[0] - 1)
             self._h = _lib.phc_system_create_common(self.n_eq, self.n_var, self.limbs, self.n_terms, _ptr(mp),
                                                     _ptr(vi), _ptr(ex), _ptr(cf), self.device)
+            self.common = True
+            if coeff_target is not None:
+                self.set_target(coeff_target)
             return
         if old_homotopy:
             ct = np.ascontiguousarray(coeff_target, dtype=np.float64)
@@ -53,8 +57,9 @@ class System:
 
     def set_target(self, coeff_target):
         ct = np.ascontiguousarray(coeff_target, dtype=np.float64)
-        if ct.shape != (self.n_terms, 2, self.limbs):
-            raise ValueError(f"coeff_target must have shape {(self.n_terms, 2, self.limbs)}")
+        want = (self.n_eq, self.n_terms, 2, self.limbs) if self.common else (self.n_terms, 2, self.limbs)
+        if ct.shape != want:
+            raise ValueError(f"coeff_target must have shape {want}")
         _lib.phc_system_set_target(self._h, _ptr(ct))
         self.homotopy = True
 

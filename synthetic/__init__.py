@@ -26,4 +26,5 @@ from .systems import (  # noqa: F401
     COMMON_CONFIGS,
     common_config,
     total_degree_homotopy,
+    as_common,
 )

@@ -426,3 +426,26 @@ def total_degree_homotopy(n, limbs, seed):
         for v in range(n):
             X[k, v, 0, 0] = -1.0 if (k >> v) & 1 else 1.0
     return s, target, X
+
+
+def as_common(system, coeff_target=None):
+    """A system whose polynomials all list the same terms in the same order, as a
+    common-support system (CommonArrays) plus, if given, its target coefficients as the dense
+    [n_eq][M][2][L] matrix.  Raises ValueError otherwise.  Host bookkeeping only."""
+    terms0 = [fac for _, fac in system.terms(0)]
+    M = len(terms0)
+    for i in range(1, system.n_eq):
+        if [fac for _, fac in system.terms(i)] != terms0:
+            raise ValueError("polynomials do not share one support")
+    mono_ptr, vi, ex = [0], [], []
+    for fac in terms0:
+        for v, a in fac:
+            vi.append(v)
+            ex.append(a)
+        mono_ptr.append(len(vi))
+    L = system.limbs
+    c = CommonArrays(system.n_eq, system.n_var, L, np.asarray(mono_ptr, np.int64), np.asarray(vi, np.int32),
+                     np.asarray(ex, np.int32), np.ascontiguousarray(system.coeff.reshape(system.n_eq, M, 2, L)))
+    if coeff_target is None:
+        return c
+    return c, np.ascontiguousarray(np.asarray(coeff_target).reshape(system.n_eq, M, 2, L))

@@ -102,3 +102,49 @@ def test_newton_on_common_system_converges(phc):
         assert int(st[0]) == 0
         res.append(float(r[0]))
     assert res[0] > 1e-5 and res[-1] < 1e-28, res
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_common_homotopy_vs_oracle_and_endpoints(phc, L):
+    """Homotopy coefficients on a common-support handle: h(x, t) with the dense start and
+    target matrices blended per entry, against the homotopy oracle on the expanded system;
+    t = 0 / 1 bitwise the plain start / target evaluations."""
+    from oracle.homotopy import evaluate_homotopy_rows
+    from synthetic import random_t, real_limbs
+    c, X = common_support_system(9, 14, 1, 5, 3, L, seed=7, points=3)
+    from synthetic.systems import unit_circle_limbs
+    ct = unit_circle_limbs(np.random.default_rng(3).uniform(0, 6.283, (9, 14)), L, 1)
+    h = phc.System(c, coeff_target=ct)
+    T = random_t(3, L, seed=8)
+    F, J = h.eval_homotopy_batch(torch.from_numpy(X).cuda(), torch.from_numpy(T).cuda())
+    torch.cuda.synchronize()
+    e = expand_common(c)
+    for p in range(3):
+        ar, Fr, Jr = evaluate_homotopy_rows(e, ct.reshape(-1, 2, L), X[p], T[p], arith="exact" if L == 2 else "mp")
+        ef, ej = compare_point(ar, Fr, Jr, F[p].cpu().numpy(), J[p].cpu().numpy(), L)
+        assert ef <= TOL[L] and ej <= TOL[L], (p, ef, ej)
+    T01 = torch.from_numpy(real_limbs([0, 1, 0], L)).cuda()
+    F01, J01 = h.eval_homotopy_batch(torch.from_numpy(X).cuda(), T01)
+    Fs, Js = phc.System(c).eval_batch(torch.from_numpy(X).cuda())
+    c2 = type(c)(c.n_eq, c.n_var, L, c.mono_ptr, c.var_idx, c.exponent, ct)
+    Ft, Jt = phc.System(c2).eval_batch(torch.from_numpy(X).cuda())
+    torch.cuda.synchronize()
+    assert torch.equal(F01[0], Fs[0]) and torch.equal(J01[0], Js[0])
+    assert torch.equal(F01[1], Ft[1]) and torch.equal(J01[1], Jt[1])
+
+
+def test_track_on_common_support_handle(phc):
+    """The total-degree homotopy shares one support across its polynomials: tracked through a
+    common-support handle (two-stage evaluation) the 8 paths reach the same end points as
+    through the per-term handle (within the tolerance)."""
+    from synthetic import as_common, total_degree_homotopy
+    s, cf, X0 = total_degree_homotopy(3, 2, seed=7)
+    c, cft = as_common(s, cf)
+    X = torch.from_numpy(X0).cuda()
+    Xa, sa, _ = phc.System(s, coeff_target=cf).track(X)
+    Xb, sb, _ = phc.System(c, coeff_target=cft).track(X)
+    assert (sa == 1).all() and (sb == 1).all()
+    za = Xa.cpu().numpy()
+    zb = Xb.cpu().numpy()
+    d = np.abs((za[..., 0] + za[..., 1]) - (zb[..., 0] + zb[..., 1])).max()
+    assert d <= 1e-25, d
