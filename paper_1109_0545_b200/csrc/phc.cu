@@ -507,6 +507,21 @@ void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
 }
 
 template <class T>
+struct HostBuf {  // RAII pinned host buffer (the tracker's per-step exchange arrays)
+  T* p = nullptr;
+  int alloc(size_t n) {
+    if (cudaMallocHost((void**)&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return fail(PHC_ENOMEM, "cudaMallocHost(%zu bytes) failed", n * sizeof(T));
+    }
+    return PHC_OK;
+  }
+  T& operator[](size_t i) { return p[i]; }
+  ~HostBuf() { if (p) cudaFreeHost(p); }
+};
+
+template <class T>
 struct DevBuf {  // RAII device buffer (the tracker's workspace)
   T* p = nullptr;
   ~DevBuf() { if (p) cudaFree(p); }
@@ -1077,19 +1092,24 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   else
     phc::track_init_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
   CUDA_TRY(cudaGetLastError());
-  // host-side per-path control state (Alg. 1 step_size_control / stop_criterion)
-  std::vector<double> lam((size_t)P, q.step_init), res((size_t)P * q.max_newton);
-  std::vector<int32_t> stat((size_t)P, 0), idx, clip((size_t)P), acc((size_t)P), nst((size_t)P * q.max_newton);
+  // host-side per-path control state (Alg. 1 step_size_control / stop_criterion); the arrays
+  // exchanged with the device every step live in pinned memory (truly asynchronous copies)
+  HostBuf<double> lam, res;
+  HostBuf<int32_t> idx, clip, acc, nst;
+  if ((rc = lam.alloc(P)) || (rc = res.alloc((size_t)P * q.max_newton)) || (rc = idx.alloc(P)) ||
+      (rc = clip.alloc(P)) || (rc = acc.alloc(P)) || (rc = nst.alloc((size_t)P * q.max_newton)))
+    return rc;
+  for (int64_t p = 0; p < P; ++p) lam[p] = q.step_init;
+  std::vector<int32_t> stat((size_t)P, 0);
   std::vector<int64_t> steps((size_t)P, 0), succ((size_t)P, 0), iters((size_t)P, 0);
   std::vector<double> min_step((size_t)P, 1e300), sum_step((size_t)P, 0.0);
   while (true) {
-    idx.clear();
+    int64_t A = 0;
     for (int64_t p = 0; p < P; ++p)
-      if (stat[p] == 0) idx.push_back((int32_t)p);
-    const int64_t A = (int64_t)idx.size();
+      if (stat[p] == 0) idx[A++] = (int32_t)p;
     if (A == 0) break;
-    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.data(), A * 4, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(lam_d.p, lam.data(), P * 8, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(lam_d.p, lam.p, P * 8, cudaMemcpyHostToDevice, st));
     // predict: t_try = min(t + lambda, 1), z_guess by the secant / quadratic predictor (§5)
     if (L == 2)
       phc::predict_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
@@ -1098,7 +1118,7 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
       phc::predict_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
                                                            q.predictor, tc.p, xc.p, clip_d.p);
     CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(clip.data(), clip_d.p, A * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(clip.p, clip_d.p, A * 4, cudaMemcpyDeviceToHost, st));
     // correct: Alg. 2 on h(., t_try).  All max_newton iterations are enqueued back to back
     // (one host synchronisation per tracker step instead of one per iteration); iteration k
     // records its residual and status in row k.  A path is corrected at the first iteration
@@ -1106,8 +1126,8 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
     // after it only refine the point further (documented deviation, reading T1).
     for (int k = 0; k < q.max_newton; ++k)
       if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p + (size_t)k * A, nst_d.p + (size_t)k * A, st))) return rc;
-    CUDA_TRY(cudaMemcpyAsync(res.data(), res_d.p, (size_t)q.max_newton * A * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(nst.data(), nst_d.p, (size_t)q.max_newton * A * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(res.p, res_d.p, (size_t)q.max_newton * A * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(nst.p, nst_d.p, (size_t)q.max_newton * A * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
     std::vector<char> conv((size_t)A, 0), bad((size_t)A, 0);
     for (int64_t a = 0; a < A; ++a) {
@@ -1138,7 +1158,7 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
       }
       if (stat[p] == 0 && steps[p] >= q.max_steps) stat[p] = 2;
     }
-    CUDA_TRY(cudaMemcpyAsync(acc_d.p, acc.data(), A * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(acc_d.p, acc.p, A * 4, cudaMemcpyHostToDevice, st));
     if (L == 2)
       phc::accept_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
     else
@@ -1151,12 +1171,11 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
     phc::track_finish_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, t_hist.p, x_hist.p, x, t_end);
   CUDA_TRY(cudaGetLastError());
   // end refinement at t = 1 of the paths that arrived (Newton on the target system)
-  idx.clear();
+  int64_t A = 0;
   for (int64_t p = 0; p < P; ++p)
-    if (stat[p] == 1) idx.push_back((int32_t)p);
-  const int64_t A = (int64_t)idx.size();
+    if (stat[p] == 1) idx[A++] = (int32_t)p;
   if (q.end_newton > 0 && A > 0) {
-    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.data(), A * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
     std::vector<double> ones((size_t)A * L, 0.0);
     for (int64_t a = 0; a < A; ++a) ones[(size_t)a * L] = 1.0;
     CUDA_TRY(cudaMemcpyAsync(tc.p, ones.data(), A * L * 8, cudaMemcpyHostToDevice, st));
