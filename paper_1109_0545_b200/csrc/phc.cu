@@ -139,6 +139,7 @@ struct phc_system {
   // NEXT-2 common-support system: "terms" are the M shared monomials (unit coefficients),
   // C^T [M][n_eq][2][L] and the per-column lists of the coefficient product
   bool common = false;
+  bool fused_gather = true;   // remote shards write F, J into home memory over NVLink (else staged copies)
   bool has_target = false;    // NEXT-3 target attached (coeff2, or cT2 for common systems)
   std::vector<double> cT2;    // common systems: target C^T [M][n_eq][2][L]
   // latency path (kernels_scan.cuh): eligible when k <= 32 and the CTA's table + rows fit
@@ -783,7 +784,27 @@ static int eval_batch_impl(const phc_system* cs, int64_t n_points, const double*
     cudaDeviceCanAccessPeer(&can, dv, s->home);
     if (can) {
       cudaError_t pe = cudaDeviceEnablePeerAccess(s->home, 0);
-      if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (pe != cudaSuccess) {
+        cudaGetLastError();
+        can = 0;
+      }
+    }
+    if (can && s->fused_gather) {
+      // fused scatter/compute/gather (SURVEY.md §8(e) option 1): with peer access the
+      // kernels of device dv read their points and t from the home device and store F and J
+      // straight into the caller's home-device buffers over NVLink -- no staging buffers,
+      // no copies; the stores of a point's rows overlap the evaluation of the next points.
+      if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
+      if ((rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
+                              jac + p0 * (int64_t)s->n_eq * s->n_var * cd, d->stream, n_points)))
+        break;
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      cudaEventRecord(e, d->stream);
+      dones.push_back(e);
+      continue;
     }
     if ((rc = ensure_stage(s, d, np))) break;
     if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
