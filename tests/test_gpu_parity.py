@@ -298,3 +298,23 @@ def test_compiled_maxima(phc, L):
     ej = rel_errors(ar, [J2[i][c] for i in range(2) for c in cols], np.stack([j2[0][i, c] for i in range(2) for c in cols]))[0]
     assert ef <= TOL[L] and ej <= TOL[L], (ef, ej)
     assert np.count_nonzero(j2[0][..., 0, 0]) == 4
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_empty_inputs(phc, L):
+    """Zero points: every batch call is a no-op returning PHC_OK; a system without any term
+    (n_terms = 0): F = 0 and J = 0 exactly, through the latency path and the batch kernels."""
+    s, X = config_system("tiny" if L == 2 else "c3", seed=1, points=1)
+    h = phc.System(s)
+    X0 = torch.empty((0, s.n_var, 2, L), dtype=torch.float64, device="cuda")
+    F0, J0 = h.eval_batch(X0)
+    Xn, r, st = h.newton_step(X0)
+    torch.cuda.synchronize()
+    assert F0.shape[0] == 0 and J0.shape[0] == 0 and Xn.shape[0] == 0
+    empty = system_from_terms(3, 4, L, [[], [], []], np.zeros((0, 2, L)))
+    he = phc.System(empty)
+    Xe = torch.from_numpy(np.ones((5000, 4, 2, L))).cuda()
+    for pts in (1, 5000):
+        F, J = he.eval_batch(Xe[:pts])
+        torch.cuda.synchronize()
+        assert (F == 0).all() and (J == 0).all()
