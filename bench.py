@@ -111,9 +111,18 @@ def model_counts(s, st):
     return cm, ca
 
 
-def exec_flops_per_point(s, st):
+def latency_regime(st, points):
+    """True when a call with `points` points takes the latency path (phc.h: n_points * n_terms
+    <= the bound in phc_system_stats out[13])."""
+    return st["latency_bound"] > 0 and points * st["n_terms"] <= st["latency_bound"]
+
+
+def exec_flops_per_point(s, st, points=None):
     """Executed FP64 flops per point of the kernels' useful work, as counted by the library
-    (phc_system_stats out[8]; per-op costs from arith.cuh, checked against ncu)."""
+    (phc_system_stats out[8], or out[12] for the latency path; per-op costs from arith.cuh,
+    checked against ncu)."""
+    if points is not None and latency_regime(st, points):
+        return int(st["latency_exec_flops_per_point"])
     return int(st["exec_flops_per_point"])
 
 
@@ -301,11 +310,11 @@ def main():
         cm_model, ca_model = model_counts(s, st)
         mf = MODEL_FLOPS[s.limbs]
         model_flops_pp = cm_model * mf["cm"] + ca_model * mf["ca"]
-        exec_pp = exec_flops_per_point(s, st)
+        exec_pp = exec_flops_per_point(s, st, P)
         value = aggregate_value(world, P, args.steps, ms)
         peak = peak_now
         # dominant kernel (largest summed time among the classes)
-        names = ["power_table", "term", "reduce", "fused_block"]
+        names = ["power_table", "term", "reduce", "poly_scan" if latency_regime(st, P) else "fused_block"]
         dom = max(range(4), key=lambda i: kms[i])
         dom_ms = kms[dom] / max(kn[dom], 1)
         # the dominant kernel does (nearly) all of the step's FP64 work: the fused block
@@ -330,7 +339,8 @@ def main():
             "vs_baseline": None,
             "dtype": "f64",
             "data": "synthetic (seeded unit-circle systems and points, BASELINE.json recipe)",
-            "config": dict(config_dict(args.workload, c, P, flush), parallelism=f"dp{world} (points)"),
+            "config": dict(config_dict(args.workload, c, P, flush), parallelism=f"dp{world} (points)",
+                           path="latency (one warp per term)" if latency_regime(st, P) else "batch kernels"),
             "roofline": {
                 "bound": "alu",
                 "kernel": names[dom],

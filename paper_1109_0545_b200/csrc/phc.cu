@@ -1350,6 +1350,26 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
   out[9] = s->plan.usable ? 1 : 0;
   out[10] = s->plan.usable ? s->plan.layout : -1;
   out[11] = s->plan.usable ? s->plan.K : s->kmax;
+  {
+    // latency path (kernels_scan.cuh): per term 1 + 10 + 2 complex products on all 32 lanes
+    // (normalised), k + 1 additions; per CTA the power table (<= 2 log2(E) + 1 products and
+    // one integer scaling per entry), n_eq * S CTAs per point
+    const phc::OpFlops f = phc::op_flops(s->L);
+    int64_t fl = 0;
+    if (s->scan_ok && !s->common) {
+      for (int64_t t = 0; t < s->n_terms; ++t) {
+        const int64_t k = s->term_ptr[t + 1] - s->term_ptr[t];
+        fl += 32 * 13 * (int64_t)f.cm + (k + 1) * f.ca;
+      }
+      int lg = 0;
+      while ((1 << lg) < s->E) ++lg;
+      fl += (int64_t)s->n_eq * s->scan_S * s->n_var * s->E * ((2 * lg + 1) * (int64_t)f.cm + f.ci);
+      fl += (int64_t)s->n_eq * s->scan_S * (s->n_var + 1) * (s->scan_W - 1) * (int64_t)f.ca;
+    }
+    out[12] = fl;
+    out[13] = s->scan_ok && !s->common ? kScanMaxTerms : 0;
+    out[14] = s->common ? 1 : 0;
+  }
   return PHC_OK;
 }
 
