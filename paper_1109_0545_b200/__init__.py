@@ -21,6 +21,7 @@ from ._lib import (  # noqa: F401
     phc_system_set_target,
     phc_system_create_common,
     phc_predict_batch,
+    phc_arith_test,
     phc_track_paths,
     TrackParams,
     phc_homotopy_old_create,

@@ -30,6 +30,7 @@ EXPORTED = (
     "phc_system_set_target",
     "phc_system_create_common",
     "phc_predict_batch",
+    "phc_arith_test",
     "phc_track_paths",
     "phc_eval_homotopy_batch",
     "phc_newton_step_homotopy_batch",
@@ -79,6 +80,8 @@ def _load():
     lib.phc_newton_step_batch.restype = ctypes.c_int
     lib.phc_system_create_common.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, i32]
     lib.phc_system_create_common.restype = ctypes.c_int
+    lib.phc_arith_test.argtypes = [i32, i32, i64, P, P, P, P]
+    lib.phc_arith_test.restype = ctypes.c_int
     lib.phc_predict_batch.argtypes = [i32, i32, i64, i32, P, P, P, P, P, P]
     lib.phc_predict_batch.restype = ctypes.c_int
     lib.phc_track_paths.argtypes = [P, i64, P, ctypes.POINTER(TrackParams), P, P, P, P]
@@ -149,6 +152,10 @@ def phc_system_create_common(n_eq, n_var, limbs, n_mono, mono_ptr, var_idx, expo
     check(lib.phc_system_create_common(ctypes.byref(h), n_eq, n_var, limbs, n_mono, mono_ptr, var_idx, exponent,
                                        coeff, device))
     return h
+
+
+def phc_arith_test(op, limbs, n, a, b, out, stream):
+    return check(lib.phc_arith_test(op, limbs, n, a, b, out, stream))
 
 
 def phc_predict_batch(limbs, n_var, n_paths, order, n_hist, t_hist, x_hist, t_new, x_out, stream):

@@ -21,6 +21,7 @@
 #include "kernels_common.cuh"
 #include "kernels_track.cuh"
 #include "kernels_scan.cuh"
+#include "kernels_selftest.cuh"
 
 namespace {
 
@@ -1217,6 +1218,23 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
       path_stats[p * 5 + 4] = succ[p] ? sum_step[p] / succ[p] : 0.0;
     }
   }
+  return PHC_OK;
+}
+
+int phc_arith_test(int32_t op, int32_t limbs, int64_t n, const double* a, const double* b, double* out, void* stream) {
+  g_err.clear();
+  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 or 4");
+  if (op < 0 || op > 9) return fail(PHC_EINVAL, "unknown op %d", op);
+  if (n < 0) return fail(PHC_EINVAL, "n < 0");
+  if (n == 0) return PHC_OK;
+  if (!a || !b || !out) return fail(PHC_EINVAL, "NULL pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const unsigned grid = (unsigned)((n + 127) / 128);
+  if (limbs == 2)
+    phc::arith_test_kernel<2><<<grid, 128, 0, st>>>(op, n, a, b, out);
+  else
+    phc::arith_test_kernel<4><<<grid, 128, 0, st>>>(op, n, a, b, out);
+  CUDA_TRY(cudaGetLastError());
   return PHC_OK;
 }
 
