@@ -92,3 +92,31 @@ def test_expand_common_structure():
             a, b = int(c.mono_ptr[j]), int(c.mono_ptr[j + 1])
             assert fac == list(zip(c.var_idx[a:b].tolist(), c.exponent[a:b].tolist()))
             assert np.array_equal(e.coeff[t], c.coeff[i, j])
+
+
+def test_next_row_entry_points_validate_without_device():
+    """The NEXT-row entry points reject bad arguments before touching a device."""
+    import ctypes
+    import paper_1109_0545_b200._lib as L
+    lib = L.lib
+    P = ctypes.c_void_p
+    # predictor: bad limbs / order / NULL pointers
+    assert lib.phc_predict_batch(3, 4, 1, 2, None, None, None, None, None, None) == L.PHC_EUNSUPPORTED
+    assert lib.phc_predict_batch(2, 4, 1, 3, None, None, None, None, None, None) == L.PHC_EINVAL
+    assert lib.phc_predict_batch(2, 4, 1, 2, None, None, None, None, None, None) == L.PHC_EINVAL
+    assert lib.phc_predict_batch(2, 4, 0, 2, None, None, None, None, None, None) == L.PHC_OK  # no paths: no-op
+    # arithmetic self-test hook
+    assert lib.phc_arith_test(11, 2, 4, None, None, None, None) == L.PHC_EINVAL
+    assert lib.phc_arith_test(0, 3, 4, None, None, None, None) == L.PHC_EUNSUPPORTED
+    assert lib.phc_arith_test(0, 2, 0, None, None, None, None) == L.PHC_OK
+    # NULL handles
+    prm = L.TrackParams(step_init=0.01, step_min=1e-8, step_max=0.1, expand=2.0, contract=0.5, tol=1e-20,
+                        max_newton=4, max_steps=10, end_newton=0, predictor=2)
+    assert lib.phc_track_paths(None, 1, None, ctypes.byref(prm), None, None, None, None) == L.PHC_EINVAL
+    assert lib.phc_system_set_target(None, None) == L.PHC_EINVAL
+    assert lib.phc_eval_homotopy_batch(None, 1, None, None, None, None, None, 0, None) == L.PHC_EINVAL
+    assert lib.phc_newton_step_homotopy_batch(None, 1, None, None, None, None, None, None) == L.PHC_EINVAL
+    h = P()
+    assert lib.phc_homotopy_old_create(ctypes.byref(h), 0, 1, 2, 0, None, None, None, None, None, None, 0) == L.PHC_EINVAL
+    assert lib.phc_system_create_common(ctypes.byref(h), 2, 2, 2, 0, None, None, None, None, 0) == L.PHC_EINVAL
+    assert "NULL" in L.phc_last_error() or L.phc_last_error() != ""
