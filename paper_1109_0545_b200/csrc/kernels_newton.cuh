@@ -3,10 +3,13 @@
 // partial pivoting on [J | -F] ("the largest number in the current column",
 // P:342-343), back substitution and the update z := z + dz.
 //
-// One CTA per point.  The augmented matrix lives in shared memory when it fits
-// (n (n+1) complex values), otherwise in a global workspace (large systems; correct but
-// one SM per point).  The paper's per-column pivot barrier is a __syncthreads;
-// its row-per-thread assignment becomes a (row, column) grid-stride over the CTA.
+// Three kernels, one result (same pivot rule, same operations per entry, same order):
+//  * newton_solve_kernel: one CTA per point, [J | -F] in shared memory (n (n+1) complex values
+//    up to ~200 KB); the paper's per-column pivot barrier is a __syncthreads, its
+//    row-per-thread assignment a (row, column) grid-stride over the CTA;
+//  * newton_warp_kernel: n <= 32, one warp per point (lane = row), no block barriers;
+//  * the multi-kernel elimination (newton_*_kernel below): matrices beyond shared memory, two
+//    launches per column over all points, the trailing update spread over many SMs.
 #pragma once
 #include <cuda_runtime.h>
 
@@ -28,7 +31,7 @@ struct NewtonArgs {
   int64_t n_points;
 };
 
-template <int L, bool SMEM>
+template <int L>
 __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   using P = Prec<L>;
   using C = typename P::C;
@@ -41,7 +44,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   if (p >= a.n_points) return;
   const int n = a.n, cols = n + 1, cd = 2 * L;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
-  double* M = SMEM ? nsm : a.Mg + (size_t)p * n * cols * cd;
+  double* M = nsm;
   double* invd = M + (size_t)n * cols * cd;  // n pivot reciprocals after the matrix
   auto at = [&](int i, int j) { return M + ((size_t)i * cols + j) * cd; };
   auto ldm = [&](int i, int j) { return sload<L>(at(i, j)); };  // generic: shared or global

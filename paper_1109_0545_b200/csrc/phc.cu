@@ -938,15 +938,15 @@ static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, 
     }
     if (L == 2) {
       if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2, true>, mat));
-        phc::newton_solve_kernel<2, true><<<(unsigned)np, threads, mat, st>>>(a);
+        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2>, mat));
+        phc::newton_solve_kernel<2><<<(unsigned)np, threads, mat, st>>>(a);
       } else {
         newton_multi<2>(a, np, st);
       }
     } else {
       if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4, true>, mat));
-        phc::newton_solve_kernel<4, true><<<(unsigned)np, threads, mat, st>>>(a);
+        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4>, mat));
+        phc::newton_solve_kernel<4><<<(unsigned)np, threads, mat, st>>>(a);
       } else {
         newton_multi<4>(a, np, st);
       }
