@@ -1,0 +1,127 @@
+// NEXT-1 host side: one Newton iteration per point (Alg. 2) -- the
+// evaluation (run_on_device) followed by the elimination kernels of kernels_newton.cuh.
+#include "runtime.h"
+#include "kernels_newton.cuh"
+
+namespace phc_rt {
+
+// Multi-kernel elimination (kernels_newton.cuh) for matrices beyond shared memory.
+template <int L>
+void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
+  const int n = a.n;
+  phc::newton_load_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
+  for (int k = 0; k < n; ++k) {
+    phc::newton_pivot_kernel<L><<<(unsigned)np, 256, 0, st>>>(a, k);
+    const int64_t work = (int64_t)(n - k - 1) * (n - k);
+    if (work > 0) phc::newton_update_kernel<L><<<dim3((unsigned)((work + 255) / 256), (unsigned)np), 256, 0, st>>>(a, k);
+  }
+  phc::newton_backsub_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
+}
+
+int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* x_new,
+                       double* residual, int32_t* status, void* stream) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "Newton needs a square system (n_eq %d != n_var %d)", s->n_eq, s->n_var);
+  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
+  if (n_points == 0) return PHC_OK;
+  if (!x || !x_new || !residual || !status) return fail(PHC_EINVAL, "NULL pointer");
+  if ((((uintptr_t)x) | ((uintptr_t)x_new)) & 31) return fail(PHC_EINVAL, "x/x_new must be 32-byte aligned");
+  DeviceGuard g(s->home);
+  DeviceState* d;
+  int rc = get_device_state(s, s->home, &d);
+  if (rc) return rc;
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = s->n_eq, L = s->L;
+  const int64_t cd = 2 * L;
+  const size_t mat = ((size_t)n * (n + 1) + n) * cd * sizeof(double);  // [J | -F] + pivot reciprocals
+  const bool smem = mat <= (size_t)200 * 1024;
+  const int64_t per_point = (int64_t)n * n * cd * 8 + (smem ? 0 : (int64_t)mat);
+  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)512 << 20) / per_point));
+  if (d->n_cap < chunk) {
+    cudaStreamSynchronize(st);
+    for (double** q : {&d->nF, &d->nJ, &d->nM}) {
+      if (*q) cudaFree(*q);
+      *q = nullptr;
+    }
+    d->n_cap = 0;
+    if ((rc = dalloc(&d->nF, (size_t)(chunk * n * cd)))) return rc;
+    if ((rc = dalloc(&d->nJ, (size_t)(chunk * n * n * cd)))) return rc;
+    if (!smem && (rc = dalloc(&d->nM, (size_t)chunk * mat / sizeof(double)))) return rc;
+    d->n_cap = chunk;
+  }
+  // few points: 512 threads spread one elimination over the whole SM; batches: 128-256 per point
+  const int threads = n_points < 148 ? 512 : (n <= 48 ? 128 : 256);
+  for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
+    const int64_t np = std::min(chunk, n_points - p0);
+    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, T ? T + p0 * L : nullptr, d->nF, d->nJ, st, n_points)))
+      return rc;
+    phc::NewtonArgs a;
+    a.X = x + p0 * n * cd;
+    a.F = d->nF;
+    a.J = d->nJ;
+    a.Xnew = x_new + p0 * n * cd;
+    a.resid = residual + p0;
+    a.status = status + p0;
+    a.Mg = d->nM;
+    a.n = n;
+    a.n_points = np;
+    ProfScope ps(s, d->dev, 2, st);
+    // small systems: one warp per point (bitwise the same step as the CTA kernel)
+    const size_t per_warp = (size_t)n * (n + 1) * cd * sizeof(double);
+    if (n <= 32 && (n <= 16 || n_points < 4096)) {
+      const int wpc = per_warp * 4 <= (size_t)160 * 1024 ? 4 : (per_warp * 2 <= (size_t)160 * 1024 ? 2 : 1);
+      const size_t sm = per_warp * wpc;
+      const unsigned grid = (unsigned)((np + wpc - 1) / wpc);
+      if (L == 2) {
+        if (sm > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_warp_kernel<2>, sm));
+        phc::newton_warp_kernel<2><<<grid, wpc * 32, sm, st>>>(a);
+      } else {
+        if (sm > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_warp_kernel<4>, sm));
+        phc::newton_warp_kernel<4><<<grid, wpc * 32, sm, st>>>(a);
+      }
+      CUDA_TRY(cudaGetLastError());
+      continue;
+    }
+    if (L == 2) {
+      if (smem) {
+        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2>, mat));
+        phc::newton_solve_kernel<2><<<(unsigned)np, threads, mat, st>>>(a);
+      } else {
+        newton_multi<2>(a, np, st);
+      }
+    } else {
+      if (smem) {
+        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4>, mat));
+        phc::newton_solve_kernel<4><<<(unsigned)np, threads, mat, st>>>(a);
+      } else {
+        newton_multi<4>(a, np, st);
+      }
+    }
+    CUDA_TRY(cudaGetLastError());
+  }
+  return PHC_OK;
+}
+
+}  // namespace phc_rt
+
+using namespace phc_rt;
+
+extern "C" {
+
+int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x, double* x_new, double* residual,
+                          int32_t* status, void* stream) {
+  return newton_impl(s, n_points, x, nullptr, x_new, residual, status, stream);
+}
+
+int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t,
+                                   double* x_new, double* residual, int32_t* status, void* stream) {
+  g_err.clear();
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
+  return newton_impl(s, n_points, x, t, x_new, residual, status, stream);
+}
+
+}  // extern "C"

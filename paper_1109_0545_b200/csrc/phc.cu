@@ -14,16 +14,13 @@
 #include <string>
 #include <vector>
 
-#include "../../include/phc.h"
+#include "runtime.h"
 #include "kernels_generic.cuh"
 #include "kernels_block.cuh"
-#include "kernels_newton.cuh"
 #include "kernels_common.cuh"
-#include "kernels_track.cuh"
 #include "kernels_scan.cuh"
-#include "kernels_selftest.cuh"
 
-namespace {
+namespace phc_rt {
 
 thread_local std::string g_err;
 
@@ -37,139 +34,6 @@ int fail(int code, const char* fmt, ...) {
   return code;
 }
 
-#define CUDA_TRY(expr)                                                                         \
-  do {                                                                                         \
-    cudaError_t e_ = (expr);                                                                   \
-    if (e_ != cudaSuccess) return fail(PHC_ECUDA, "%s: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
-  } while (0)
-
-struct DeviceGuard {
-  int prev = -1;
-  explicit DeviceGuard(int dev) {
-    cudaGetDevice(&prev);
-    if (prev != dev) cudaSetDevice(dev);
-  }
-  ~DeviceGuard() {
-    if (prev >= 0) cudaSetDevice(prev);
-  }
-};
-
-template <class T>
-int dalloc(T** p, size_t n) {
-  if (n == 0) n = 1;
-  cudaError_t e = cudaMalloc((void**)p, n * sizeof(T));
-  if (e != cudaSuccess) {
-    *p = nullptr;
-    cudaGetLastError();
-    return fail(PHC_ENOMEM, "cudaMalloc(%zu bytes): %s", n * sizeof(T), cudaGetErrorString(e));
-  }
-  return PHC_OK;
-}
-
-// Per-device replica of the packed tables plus scratch (tables
-// replicated once per device at first use).
-struct DeviceState {
-  int dev = -1;
-  cudaStream_t stream = nullptr;   // internal stream for non-home shards
-  cudaStream_t stream2 = nullptr;  // gather stream of the non-home shards
-  cudaEvent_t done = nullptr;
-  // generic path tables
-  int64_t* term_ptr = nullptr;
-  uint32_t* fac = nullptr;
-  double* coeff = nullptr;
-  double* coeff2 = nullptr;  // NEXT-3 homotopy target coefficients (term order)
-  int64_t* poly_ptr = nullptr;
-  int64_t* jptr = nullptr;
-  int64_t* jidx = nullptr;
-  // common-support tables (NEXT-2): column lists and C transposed
-  int64_t* cl_ptr = nullptr;
-  int32_t* cl_j = nullptr;
-  int64_t* cl_q = nullptr;
-  double* cT = nullptr;
-  double* cT2 = nullptr;  // homotopy target of a common-support system
-  // block path tables
-  phc::BlockTables bt{};
-  bool have_block = false;
-  // scratch
-  double* PT = nullptr;
-  double* Y = nullptr;
-  double* G = nullptr;
-  int64_t chunk_cap = 0;
-  // Newton-step workspace (evaluation outputs and the global elimination matrix)
-  double* nF = nullptr;
-  double* nJ = nullptr;
-  double* nM = nullptr;
-  int64_t n_cap = 0;
-  // latency (warp-scan) path: partial rows of the S splits
-  double* part = nullptr;
-  int64_t part_cap = 0;
-  int* count = nullptr;  // arrival counters (zeroed at allocation; each call leaves them zero)
-  int64_t count_cap = 0;
-  // staging buffers for remote shards
-  double* xs = nullptr;
-  double* fs = nullptr;
-  double* js = nullptr;
-  double* ts = nullptr;  // t per point (homotopy shards)
-  int64_t stage_cap = 0;
-  ~DeviceState() {
-    DeviceGuard g(dev);
-    for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
-                    (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
-                    (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
-                    (void*)cl_q, (void*)cT, (void*)part, (void*)count, (void*)cT2})
-      if (p) cudaFree(p);
-    if (stream) cudaStreamDestroy(stream);
-    if (stream2) cudaStreamDestroy(stream2);
-    if (done) cudaEventDestroy(done);
-  }
-};
-
-}  // namespace
-
-struct phc_system {
-  int32_t n_eq = 0, n_var = 0, L = 0, home = 0;
-  int64_t n_terms = 0, n_factors = 0;
-  int kmax = 0, E = 1;
-  int64_t nnz = 0;
-  int64_t cm_per_point = 0, ca_per_point = 0;
-  // host copies
-  std::vector<int64_t> poly_ptr, term_ptr;
-  std::vector<uint32_t> fac;
-  std::vector<double> coeff;
-  std::vector<double> coeff2;  // NEXT-3: homotopy target coefficients (empty: not a homotopy)
-  // NEXT-2 common-support system: "terms" are the M shared monomials (unit coefficients),
-  // C^T [M][n_eq][2][L] and the per-column lists of the coefficient product
-  bool common = false;
-  bool fused_gather = true;   // remote shards write F, J into home memory over NVLink (else staged copies)
-  bool has_target = false;    // NEXT-3 target attached (coeff2, or cT2 for common systems)
-  std::vector<double> cT2;    // common systems: target C^T [M][n_eq][2][L]
-  // latency path (kernels_scan.cuh): eligible when k <= 32 and the CTA's table + rows fit
-  bool scan_ok = false;
-  int scan_S = 1, scan_W = 8;
-  size_t scan_smem = 0;
-  std::vector<int64_t> cl_ptr, cl_q;
-  std::vector<int32_t> cl_j;
-  std::vector<double> cT;
-  std::vector<int64_t> jptr, jidx;
-  phc::HostBlockPlan plan;  // warp-per-block layout (kernels_block.cuh)
-  std::mutex mu;
-  std::map<int, std::unique_ptr<DeviceState>> devs;
-  // host-API staging on the home device
-  double *hx = nullptr, *hf = nullptr, *hj = nullptr;
-  int64_t h_cap = 0;
-  cudaStream_t hstream = nullptr;
-  cudaStream_t hstream2 = nullptr;  // D2H stream of the pipelined host call
-  // kernel timing (phc_profile_*): events on the launch stream, home device only
-  bool prof = false;
-  struct Rec { int cls; cudaEvent_t a, b; };
-  std::vector<Rec> recs;
-  std::vector<cudaEvent_t> pool;
-  double prof_ms[4] = {0, 0, 0, 0};
-  int64_t prof_n[4] = {0, 0, 0, 0};
-};
-
-namespace {
-
 cudaEvent_t pool_event(phc_system* s) {
   if (!s->pool.empty()) {
     cudaEvent_t e = s->pool.back();
@@ -180,27 +44,6 @@ cudaEvent_t pool_event(phc_system* s) {
   cudaEventCreate(&e);
   return e;
 }
-
-// Brackets one kernel launch with events on its stream when profiling is on.
-struct ProfScope {
-  phc_system* s;
-  int cls;
-  cudaStream_t st;
-  cudaEvent_t a = nullptr;
-  ProfScope(const phc_system* cs, int dev, int cls_, cudaStream_t st_) : s(const_cast<phc_system*>(cs)), cls(cls_), st(st_) {
-    if (!s->prof || dev != s->home) { s = nullptr; return; }
-    a = pool_event(s);
-    cudaEventRecord(a, st);
-  }
-  ~ProfScope() {
-    if (!s) return;
-    cudaEvent_t b = pool_event(s);
-    cudaEventRecord(b, st);
-    s->recs.push_back({cls, a, b});
-  }
-};
-
-size_t cbytes(const phc_system* s) { return (size_t)2 * s->L * sizeof(double); }
 
 int upload(void* dst, const void* src, size_t bytes) {
   if (bytes == 0) return PHC_OK;
@@ -338,7 +181,6 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
 }
 
 // Latency path (kernels_scan.cuh) for calls with few points: one warp per term.
-constexpr int64_t kScanMaxTerms = 148 * 32;  // call_points * n_terms at or below: latency path
 
 template <int L>
 int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
@@ -454,7 +296,7 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
 // Evaluate n_points points resident on device d, on stream st.  T (t per point, device d)
 // selects the homotopy coefficients (NEXT-3); nullptr evaluates the system's own coefficients.
 int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
-                  double* jac, cudaStream_t st, int64_t call_points = -1) {
+                  double* jac, cudaStream_t st, int64_t call_points) {
   if (n_points <= 0) return PHC_OK;
   if (s->common) {
     const bool split = common_split(s, call_points < 0 ? n_points : call_points);
@@ -493,41 +335,132 @@ int ensure_stage(const phc_system* s, DeviceState* d, int64_t np) {
   return PHC_OK;
 }
 
-}  // namespace
-
-// Multi-kernel elimination (kernels_newton.cuh) for matrices beyond shared memory.
-template <int L>
-void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
-  const int n = a.n;
-  phc::newton_load_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
-  for (int k = 0; k < n; ++k) {
-    phc::newton_pivot_kernel<L><<<(unsigned)np, 256, 0, st>>>(a, k);
-    const int64_t work = (int64_t)(n - k - 1) * (n - k);
-    if (work > 0) phc::newton_update_kernel<L><<<dim3((unsigned)((work + 255) / 256), (unsigned)np), 256, 0, st>>>(a, k);
+// Shared body of the batch calls: T = t per point [n_points][L] (homotopy) or nullptr.
+int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* f,
+                           double* jac, const int32_t* devices, int32_t n_devices, void* stream) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
+  if (n_points == 0) return PHC_OK;
+  if (!x || !f || !jac) return fail(PHC_EINVAL, "NULL x/f/jac");
+  if ((((uintptr_t)x) | ((uintptr_t)f) | ((uintptr_t)jac)) & 31) return fail(PHC_EINVAL, "x/f/jac must be 32-byte aligned");
+  std::vector<int> devs;
+  if (!devices || n_devices <= 0)
+    devs.push_back(s->home);
+  else
+    devs.assign(devices, devices + n_devices);
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  for (int dv : devs)
+    if (dv < 0 || dv >= ndev) return fail(PHC_EINVAL, "device %d out of range", dv);
+  cudaStream_t st = (cudaStream_t)stream;
+  DeviceGuard g(s->home);
+  const int64_t cd = 2 * s->L;
+  const int64_t G = (int64_t)devs.size();
+  if (G == 1 && devs[0] == s->home) {
+    DeviceState* d;
+    int rc = get_device_state(s, s->home, &d);
+    if (rc) return rc;
+    return run_on_device(s, d, n_points, x, T, f, jac, st);
   }
-  phc::newton_backsub_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
+  // sharded: contiguous equal ranges [g P / G, (g+1) P / G)
+  cudaEvent_t start;
+  CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(start, st));
+  std::vector<cudaEvent_t> dones;
+  int rc = PHC_OK;
+  for (int64_t gi = 0; gi < G && rc == PHC_OK; ++gi) {
+    const int64_t p0 = gi * n_points / G, p1 = (gi + 1) * n_points / G;
+    const int64_t np = p1 - p0;
+    if (np == 0) continue;
+    const int dv = devs[gi];
+    DeviceState* d;
+    if ((rc = get_device_state(s, dv, &d))) break;
+    if (dv == s->home) {
+      rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
+                         jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st, n_points);
+      continue;
+    }
+    DeviceGuard gd(dv);
+    int can = 0;
+    cudaDeviceCanAccessPeer(&can, dv, s->home);
+    if (can) {
+      cudaError_t pe = cudaDeviceEnablePeerAccess(s->home, 0);
+      if (pe == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+      } else if (pe != cudaSuccess) {
+        cudaGetLastError();
+        can = 0;
+      }
+    }
+    if (can && s->fused_gather) {
+      // fused scatter/compute/gather (SURVEY.md §8(e) option 1): with peer access the
+      // kernels of device dv read their points and t from the home device and store F and J
+      // straight into the caller's home-device buffers over NVLink -- no staging buffers,
+      // no copies; the stores of a point's rows overlap the evaluation of the next points.
+      if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
+      if ((rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
+                              jac + p0 * (int64_t)s->n_eq * s->n_var * cd, d->stream, n_points)))
+        break;
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      cudaEventRecord(e, d->stream);
+      dones.push_back(e);
+      continue;
+    }
+    if ((rc = ensure_stage(s, d, np))) break;
+    if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
+    if (cudaMemcpyPeerAsync(d->xs, dv, x + p0 * s->n_var * cd, s->home, np * s->n_var * cd * 8, d->stream) != cudaSuccess) {
+      rc = fail(PHC_ECUDA, "scatter copy failed");
+      break;
+    }
+    if (T && cudaMemcpyPeerAsync(d->ts, dv, T + p0 * s->L, s->home, np * s->L * 8, d->stream) != cudaSuccess) {
+      rc = fail(PHC_ECUDA, "scatter copy (t) failed");
+      break;
+    }
+    // the shard in chunks: evaluation of chunk c on d->stream, its gather to the home device
+    // over NVLink on d->stream2, so the gather overlaps the evaluation of the next chunks
+    // (SURVEY.md §8(e) option 2).  call_points = the call's total: same regime, same bits.
+    const int64_t nch = np >= 8192 ? 4 : 1;
+    for (int64_t c = 0; c < nch && rc == PHC_OK; ++c) {
+      const int64_t q0 = c * np / nch, q1 = (c + 1) * np / nch, nq = q1 - q0;
+      if (nq == 0) continue;
+      if ((rc = run_on_device(s, d, nq, d->xs + q0 * s->n_var * cd, T ? d->ts + q0 * s->L : nullptr,
+                              d->fs + q0 * s->n_eq * cd, d->js + q0 * (int64_t)s->n_eq * s->n_var * cd, d->stream,
+                              n_points)))
+        break;
+      cudaEvent_t ce;
+      cudaEventCreateWithFlags(&ce, cudaEventDisableTiming);
+      cudaEventRecord(ce, d->stream);
+      cudaStreamWaitEvent(d->stream2, ce, 0);
+      cudaEventDestroy(ce);
+      if (cudaMemcpyPeerAsync(f + (p0 + q0) * s->n_eq * cd, s->home, d->fs + q0 * s->n_eq * cd, dv,
+                              nq * s->n_eq * cd * 8, d->stream2) != cudaSuccess ||
+          cudaMemcpyPeerAsync(jac + (p0 + q0) * (int64_t)s->n_eq * s->n_var * cd, s->home,
+                              d->js + q0 * (int64_t)s->n_eq * s->n_var * cd, dv,
+                              nq * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream2) != cudaSuccess) {
+        rc = fail(PHC_ECUDA, "gather copy failed");
+        break;
+      }
+    }
+    if (rc) break;
+    cudaEvent_t e;
+    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+    cudaEventRecord(e, d->stream2);
+    dones.push_back(e);
+  }
+  for (cudaEvent_t e : dones) {
+    cudaStreamWaitEvent(st, e, 0);
+    cudaEventDestroy(e);
+  }
+  cudaEventDestroy(start);
+  return rc;
 }
 
-template <class T>
-struct HostBuf {  // RAII pinned host buffer (the tracker's per-step exchange arrays)
-  T* p = nullptr;
-  int alloc(size_t n) {
-    if (cudaMallocHost((void**)&p, std::max<size_t>(n, 1) * sizeof(T)) != cudaSuccess) {
-      p = nullptr;
-      cudaGetLastError();
-      return fail(PHC_ENOMEM, "cudaMallocHost(%zu bytes) failed", n * sizeof(T));
-    }
-    return PHC_OK;
-  }
-  T& operator[](size_t i) { return p[i]; }
-  ~HostBuf() { if (p) cudaFreeHost(p); }
-};
+}  // namespace phc_rt
 
-template <class T>
-struct DevBuf {  // RAII device buffer (the tracker's workspace)
-  T* p = nullptr;
-  ~DevBuf() { if (p) cudaFree(p); }
-};
+using namespace phc_rt;
 
 extern "C" {
 
@@ -733,129 +666,6 @@ void phc_system_destroy(phc_system* s) {
   delete s;
 }
 
-// Shared body of the batch calls: T = t per point [n_points][L] (homotopy) or nullptr.
-static int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* f,
-                           double* jac, const int32_t* devices, int32_t n_devices, void* stream) {
-  g_err.clear();
-  phc_system* s = const_cast<phc_system*>(cs);
-  if (!s) return fail(PHC_EINVAL, "NULL system");
-  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
-  if (n_points == 0) return PHC_OK;
-  if (!x || !f || !jac) return fail(PHC_EINVAL, "NULL x/f/jac");
-  if ((((uintptr_t)x) | ((uintptr_t)f) | ((uintptr_t)jac)) & 31) return fail(PHC_EINVAL, "x/f/jac must be 32-byte aligned");
-  std::vector<int> devs;
-  if (!devices || n_devices <= 0)
-    devs.push_back(s->home);
-  else
-    devs.assign(devices, devices + n_devices);
-  int ndev = 0;
-  cudaGetDeviceCount(&ndev);
-  for (int dv : devs)
-    if (dv < 0 || dv >= ndev) return fail(PHC_EINVAL, "device %d out of range", dv);
-  cudaStream_t st = (cudaStream_t)stream;
-  DeviceGuard g(s->home);
-  const int64_t cd = 2 * s->L;
-  const int64_t G = (int64_t)devs.size();
-  if (G == 1 && devs[0] == s->home) {
-    DeviceState* d;
-    int rc = get_device_state(s, s->home, &d);
-    if (rc) return rc;
-    return run_on_device(s, d, n_points, x, T, f, jac, st);
-  }
-  // sharded: contiguous equal ranges [g P / G, (g+1) P / G)
-  cudaEvent_t start;
-  CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
-  CUDA_TRY(cudaEventRecord(start, st));
-  std::vector<cudaEvent_t> dones;
-  int rc = PHC_OK;
-  for (int64_t gi = 0; gi < G && rc == PHC_OK; ++gi) {
-    const int64_t p0 = gi * n_points / G, p1 = (gi + 1) * n_points / G;
-    const int64_t np = p1 - p0;
-    if (np == 0) continue;
-    const int dv = devs[gi];
-    DeviceState* d;
-    if ((rc = get_device_state(s, dv, &d))) break;
-    if (dv == s->home) {
-      rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
-                         jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st, n_points);
-      continue;
-    }
-    DeviceGuard gd(dv);
-    int can = 0;
-    cudaDeviceCanAccessPeer(&can, dv, s->home);
-    if (can) {
-      cudaError_t pe = cudaDeviceEnablePeerAccess(s->home, 0);
-      if (pe == cudaErrorPeerAccessAlreadyEnabled) {
-        cudaGetLastError();
-      } else if (pe != cudaSuccess) {
-        cudaGetLastError();
-        can = 0;
-      }
-    }
-    if (can && s->fused_gather) {
-      // fused scatter/compute/gather (SURVEY.md §8(e) option 1): with peer access the
-      // kernels of device dv read their points and t from the home device and store F and J
-      // straight into the caller's home-device buffers over NVLink -- no staging buffers,
-      // no copies; the stores of a point's rows overlap the evaluation of the next points.
-      if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
-      if ((rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
-                              jac + p0 * (int64_t)s->n_eq * s->n_var * cd, d->stream, n_points)))
-        break;
-      cudaEvent_t e;
-      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-      cudaEventRecord(e, d->stream);
-      dones.push_back(e);
-      continue;
-    }
-    if ((rc = ensure_stage(s, d, np))) break;
-    if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
-    if (cudaMemcpyPeerAsync(d->xs, dv, x + p0 * s->n_var * cd, s->home, np * s->n_var * cd * 8, d->stream) != cudaSuccess) {
-      rc = fail(PHC_ECUDA, "scatter copy failed");
-      break;
-    }
-    if (T && cudaMemcpyPeerAsync(d->ts, dv, T + p0 * s->L, s->home, np * s->L * 8, d->stream) != cudaSuccess) {
-      rc = fail(PHC_ECUDA, "scatter copy (t) failed");
-      break;
-    }
-    // the shard in chunks: evaluation of chunk c on d->stream, its gather to the home device
-    // over NVLink on d->stream2, so the gather overlaps the evaluation of the next chunks
-    // (SURVEY.md §8(e) option 2).  call_points = the call's total: same regime, same bits.
-    const int64_t nch = np >= 8192 ? 4 : 1;
-    for (int64_t c = 0; c < nch && rc == PHC_OK; ++c) {
-      const int64_t q0 = c * np / nch, q1 = (c + 1) * np / nch, nq = q1 - q0;
-      if (nq == 0) continue;
-      if ((rc = run_on_device(s, d, nq, d->xs + q0 * s->n_var * cd, T ? d->ts + q0 * s->L : nullptr,
-                              d->fs + q0 * s->n_eq * cd, d->js + q0 * (int64_t)s->n_eq * s->n_var * cd, d->stream,
-                              n_points)))
-        break;
-      cudaEvent_t ce;
-      cudaEventCreateWithFlags(&ce, cudaEventDisableTiming);
-      cudaEventRecord(ce, d->stream);
-      cudaStreamWaitEvent(d->stream2, ce, 0);
-      cudaEventDestroy(ce);
-      if (cudaMemcpyPeerAsync(f + (p0 + q0) * s->n_eq * cd, s->home, d->fs + q0 * s->n_eq * cd, dv,
-                              nq * s->n_eq * cd * 8, d->stream2) != cudaSuccess ||
-          cudaMemcpyPeerAsync(jac + (p0 + q0) * (int64_t)s->n_eq * s->n_var * cd, s->home,
-                              d->js + q0 * (int64_t)s->n_eq * s->n_var * cd, dv,
-                              nq * (int64_t)s->n_eq * s->n_var * cd * 8, d->stream2) != cudaSuccess) {
-        rc = fail(PHC_ECUDA, "gather copy failed");
-        break;
-      }
-    }
-    if (rc) break;
-    cudaEvent_t e;
-    cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-    cudaEventRecord(e, d->stream2);
-    dones.push_back(e);
-  }
-  for (cudaEvent_t e : dones) {
-    cudaStreamWaitEvent(st, e, 0);
-    cudaEventDestroy(e);
-  }
-  cudaEventDestroy(start);
-  return rc;
-}
-
 int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double* x, double* f, double* jac,
                             const int32_t* devices, int32_t n_devices, void* stream) {
   return eval_batch_impl(s, n_points, x, nullptr, f, jac, devices, n_devices, stream);
@@ -868,106 +678,6 @@ int phc_eval_homotopy_batch(const phc_system* s, int64_t n_points, const double*
   if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
   if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
   return eval_batch_impl(s, n_points, x, t, f, jac, devices, n_devices, stream);
-}
-
-static int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* x_new,
-                       double* residual, int32_t* status, void* stream) {
-  g_err.clear();
-  phc_system* s = const_cast<phc_system*>(cs);
-  if (!s) return fail(PHC_EINVAL, "NULL system");
-  if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "Newton needs a square system (n_eq %d != n_var %d)", s->n_eq, s->n_var);
-  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
-  if (n_points == 0) return PHC_OK;
-  if (!x || !x_new || !residual || !status) return fail(PHC_EINVAL, "NULL pointer");
-  if ((((uintptr_t)x) | ((uintptr_t)x_new)) & 31) return fail(PHC_EINVAL, "x/x_new must be 32-byte aligned");
-  DeviceGuard g(s->home);
-  DeviceState* d;
-  int rc = get_device_state(s, s->home, &d);
-  if (rc) return rc;
-  cudaStream_t st = (cudaStream_t)stream;
-  const int n = s->n_eq, L = s->L;
-  const int64_t cd = 2 * L;
-  const size_t mat = ((size_t)n * (n + 1) + n) * cd * sizeof(double);  // [J | -F] + pivot reciprocals
-  const bool smem = mat <= (size_t)200 * 1024;
-  const int64_t per_point = (int64_t)n * n * cd * 8 + (smem ? 0 : (int64_t)mat);
-  const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)512 << 20) / per_point));
-  if (d->n_cap < chunk) {
-    cudaStreamSynchronize(st);
-    for (double** q : {&d->nF, &d->nJ, &d->nM}) {
-      if (*q) cudaFree(*q);
-      *q = nullptr;
-    }
-    d->n_cap = 0;
-    if ((rc = dalloc(&d->nF, (size_t)(chunk * n * cd)))) return rc;
-    if ((rc = dalloc(&d->nJ, (size_t)(chunk * n * n * cd)))) return rc;
-    if (!smem && (rc = dalloc(&d->nM, (size_t)chunk * mat / sizeof(double)))) return rc;
-    d->n_cap = chunk;
-  }
-  // few points: 512 threads spread one elimination over the whole SM; batches: 128-256 per point
-  const int threads = n_points < 148 ? 512 : (n <= 48 ? 128 : 256);
-  for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
-    const int64_t np = std::min(chunk, n_points - p0);
-    if ((rc = run_on_device(s, d, np, x + p0 * n * cd, T ? T + p0 * L : nullptr, d->nF, d->nJ, st, n_points)))
-      return rc;
-    phc::NewtonArgs a;
-    a.X = x + p0 * n * cd;
-    a.F = d->nF;
-    a.J = d->nJ;
-    a.Xnew = x_new + p0 * n * cd;
-    a.resid = residual + p0;
-    a.status = status + p0;
-    a.Mg = d->nM;
-    a.n = n;
-    a.n_points = np;
-    ProfScope ps(s, d->dev, 2, st);
-    // small systems: one warp per point (bitwise the same step as the CTA kernel)
-    const size_t per_warp = (size_t)n * (n + 1) * cd * sizeof(double);
-    if (n <= 32 && (n <= 16 || n_points < 4096)) {
-      const int wpc = per_warp * 4 <= (size_t)160 * 1024 ? 4 : (per_warp * 2 <= (size_t)160 * 1024 ? 2 : 1);
-      const size_t sm = per_warp * wpc;
-      const unsigned grid = (unsigned)((np + wpc - 1) / wpc);
-      if (L == 2) {
-        if (sm > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_warp_kernel<2>, sm));
-        phc::newton_warp_kernel<2><<<grid, wpc * 32, sm, st>>>(a);
-      } else {
-        if (sm > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_warp_kernel<4>, sm));
-        phc::newton_warp_kernel<4><<<grid, wpc * 32, sm, st>>>(a);
-      }
-      CUDA_TRY(cudaGetLastError());
-      continue;
-    }
-    if (L == 2) {
-      if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2>, mat));
-        phc::newton_solve_kernel<2><<<(unsigned)np, threads, mat, st>>>(a);
-      } else {
-        newton_multi<2>(a, np, st);
-      }
-    } else {
-      if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4>, mat));
-        phc::newton_solve_kernel<4><<<(unsigned)np, threads, mat, st>>>(a);
-      } else {
-        newton_multi<4>(a, np, st);
-      }
-    }
-    CUDA_TRY(cudaGetLastError());
-  }
-  return PHC_OK;
-}
-
-int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x, double* x_new, double* residual,
-                          int32_t* status, void* stream) {
-  return newton_impl(s, n_points, x, nullptr, x_new, residual, status, stream);
-}
-
-int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t,
-                                   double* x_new, double* residual, int32_t* status, void* stream) {
-  g_err.clear();
-  if (!s) return fail(PHC_EINVAL, "NULL system");
-  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
-  if (n_points > 0 && !t) return fail(PHC_EINVAL, "NULL t");
-  return newton_impl(s, n_points, x, t, x_new, residual, status, stream);
 }
 
 int phc_system_set_target(phc_system* s, const double* coeff_target) {
@@ -1057,185 +767,6 @@ int phc_homotopy_old_create(phc_system** out, int32_t n_eq, int32_t n_var, int32
   }
   return phc_system_create(out, n_eq, n_var + 1, limbs, (int64_t)tp.size() - 1, pp.data(), tp.data(), vi.data(),
                            ex.data(), cf.data(), device);
-}
-
-int phc_predict_batch(int32_t limbs, int32_t n_var, int64_t n_paths, int32_t order, const int32_t* n_hist,
-                      const double* t_hist, const double* x_hist, const double* t_new, double* x_out, void* stream) {
-  g_err.clear();
-  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 or 4");
-  if (n_var < 1 || n_paths < 0) return fail(PHC_EINVAL, "n_var >= 1 and n_paths >= 0 required");
-  if (order < 0 || order > 2) return fail(PHC_EINVAL, "order must be 0, 1 or 2");
-  if (n_paths == 0) return PHC_OK;
-  if (!n_hist || !t_hist || !x_hist || !t_new || !x_out) return fail(PHC_EINVAL, "NULL pointer");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int64_t nth = n_paths * n_var;
-  const unsigned grid = (unsigned)((nth + 127) / 128);
-  if (limbs == 2)
-    phc::predict_kernel<2><<<grid, 128, 0, st>>>(n_var, n_paths, nullptr, n_hist, t_hist, x_hist, nullptr, t_new, order,
-                                                 nullptr, x_out, nullptr);
-  else
-    phc::predict_kernel<4><<<grid, 128, 0, st>>>(n_var, n_paths, nullptr, n_hist, t_hist, x_hist, nullptr, t_new, order,
-                                                 nullptr, x_out, nullptr);
-  CUDA_TRY(cudaGetLastError());
-  return PHC_OK;
-}
-
-int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_track_params* prm, int32_t* status,
-                    double* path_stats, double* t_end, void* stream) {
-  g_err.clear();
-  phc_system* s = const_cast<phc_system*>(cs);
-  if (!s || !prm) return fail(PHC_EINVAL, "NULL argument");
-  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
-  if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "tracking needs a square system");
-  if (n_paths < 0) return fail(PHC_EINVAL, "n_paths < 0");
-  if (n_paths == 0) return PHC_OK;
-  if (!x || !status) return fail(PHC_EINVAL, "NULL x/status");
-  const phc_track_params& q = *prm;
-  if (!(q.step_min > 0 && q.step_min <= q.step_init && q.step_init <= q.step_max && q.step_max <= 1.0) ||
-      !(q.contract > 0 && q.contract < 1 && q.expand >= 1) || !(q.tol > 0) || q.max_newton < 1 || q.max_steps < 1 ||
-      q.end_newton < 0 || q.predictor < 0 || q.predictor > 2)
-    return fail(PHC_EINVAL, "invalid tracker parameters");
-  DeviceGuard g(s->home);
-  cudaStream_t st = (cudaStream_t)stream;
-  const int n = s->n_var, L = s->L;
-  const int64_t cd = 2 * L, P = n_paths;
-  int rc;
-  DevBuf<double> t_hist, x_hist, lam_d, tc, xc, res_d;
-  DevBuf<int32_t> n_hist, idx_d, clip_d, acc_d, nst_d;
-  if ((rc = dalloc(&t_hist.p, (size_t)(P * 3 * L))) || (rc = dalloc(&x_hist.p, (size_t)(P * 3 * n * cd))) ||
-      (rc = dalloc(&lam_d.p, (size_t)P)) || (rc = dalloc(&tc.p, (size_t)(P * L))) ||
-      (rc = dalloc(&xc.p, (size_t)(P * n * cd))) || (rc = dalloc(&res_d.p, (size_t)P * q.max_newton)) ||
-      (rc = dalloc(&n_hist.p, (size_t)P)) || (rc = dalloc(&idx_d.p, (size_t)P)) || (rc = dalloc(&clip_d.p, (size_t)P)) ||
-      (rc = dalloc(&acc_d.p, (size_t)P)) || (rc = dalloc(&nst_d.p, (size_t)P * q.max_newton)))
-    return rc;
-  auto grid = [](int64_t nth) { return (unsigned)((nth + 127) / 128); };
-  if (L == 2)
-    phc::track_init_kernel<2><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
-  else
-    phc::track_init_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
-  CUDA_TRY(cudaGetLastError());
-  // host-side per-path control state (Alg. 1 step_size_control / stop_criterion); the arrays
-  // exchanged with the device every step live in pinned memory (truly asynchronous copies)
-  HostBuf<double> lam, res;
-  HostBuf<int32_t> idx, clip, acc, nst;
-  if ((rc = lam.alloc(P)) || (rc = res.alloc((size_t)P * q.max_newton)) || (rc = idx.alloc(P)) ||
-      (rc = clip.alloc(P)) || (rc = acc.alloc(P)) || (rc = nst.alloc((size_t)P * q.max_newton)))
-    return rc;
-  for (int64_t p = 0; p < P; ++p) lam[p] = q.step_init;
-  std::vector<int32_t> stat((size_t)P, 0);
-  std::vector<int64_t> steps((size_t)P, 0), succ((size_t)P, 0), iters((size_t)P, 0);
-  std::vector<double> min_step((size_t)P, 1e300), sum_step((size_t)P, 0.0);
-  while (true) {
-    int64_t A = 0;
-    for (int64_t p = 0; p < P; ++p)
-      if (stat[p] == 0) idx[A++] = (int32_t)p;
-    if (A == 0) break;
-    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(lam_d.p, lam.p, P * 8, cudaMemcpyHostToDevice, st));
-    // predict: t_try = min(t + lambda, 1), z_guess by the secant / quadratic predictor (§5)
-    if (L == 2)
-      phc::predict_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
-                                                           q.predictor, tc.p, xc.p, clip_d.p);
-    else
-      phc::predict_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
-                                                           q.predictor, tc.p, xc.p, clip_d.p);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(clip.p, clip_d.p, A * 4, cudaMemcpyDeviceToHost, st));
-    // correct: Alg. 2 on h(., t_try).  All max_newton iterations are enqueued back to back
-    // (one host synchronisation per tracker step instead of one per iteration); iteration k
-    // records its residual and status in row k.  A path is corrected at the first iteration
-    // whose residual passes tol (Alg. 2 applies that iteration's update too); the iterations
-    // after it only refine the point further (documented deviation, reading T1).
-    for (int k = 0; k < q.max_newton; ++k)
-      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p + (size_t)k * A, nst_d.p + (size_t)k * A, st))) return rc;
-    CUDA_TRY(cudaMemcpyAsync(res.p, res_d.p, (size_t)q.max_newton * A * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(nst.p, nst_d.p, (size_t)q.max_newton * A * 4, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<char> conv((size_t)A, 0), bad((size_t)A, 0);
-    for (int64_t a = 0; a < A; ++a) {
-      for (int k = 0; k < q.max_newton && !conv[a] && !bad[a]; ++k) {
-        iters[idx[a]]++;
-        const double r = res[(size_t)k * A + a];
-        if (nst[(size_t)k * A + a] != 0 || !std::isfinite(r))
-          bad[a] = 1;
-        else if (r <= q.tol)
-          conv[a] = 1;
-      }
-    }
-    // step-size control, step back, stop criterion (Alg. 1; SPEC tracker defaults)
-    for (int64_t a = 0; a < A; ++a) {
-      const int32_t p = idx[a];
-      steps[p]++;
-      const bool ok = conv[a] && !bad[a];
-      acc[a] = ok ? 1 : 0;
-      if (ok) {
-        succ[p]++;
-        min_step[p] = std::min(min_step[p], lam[p]);
-        sum_step[p] += lam[p];
-        if (clip[a]) stat[p] = 1;  // reached t = 1 with a successful correction there
-        lam[p] = std::min(lam[p] * q.expand, q.step_max);
-      } else {
-        lam[p] *= q.contract;
-        if (lam[p] < q.step_min) stat[p] = 2;
-      }
-      if (stat[p] == 0 && steps[p] >= q.max_steps) stat[p] = 2;
-    }
-    CUDA_TRY(cudaMemcpyAsync(acc_d.p, acc.p, A * 4, cudaMemcpyHostToDevice, st));
-    if (L == 2)
-      phc::accept_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
-    else
-      phc::accept_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
-    CUDA_TRY(cudaGetLastError());
-  }
-  if (L == 2)
-    phc::track_finish_kernel<2><<<grid(P * n), 128, 0, st>>>(n, P, t_hist.p, x_hist.p, x, t_end);
-  else
-    phc::track_finish_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, t_hist.p, x_hist.p, x, t_end);
-  CUDA_TRY(cudaGetLastError());
-  // end refinement at t = 1 of the paths that arrived (Newton on the target system)
-  int64_t A = 0;
-  for (int64_t p = 0; p < P; ++p)
-    if (stat[p] == 1) idx[A++] = (int32_t)p;
-  if (q.end_newton > 0 && A > 0) {
-    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
-    std::vector<double> ones((size_t)A * L, 0.0);
-    for (int64_t a = 0; a < A; ++a) ones[(size_t)a * L] = 1.0;
-    CUDA_TRY(cudaMemcpyAsync(tc.p, ones.data(), A * L * 8, cudaMemcpyHostToDevice, st));
-    phc::gather_rows_kernel<<<grid(A * n * cd), 128, 0, st>>>(A, n * cd, idx_d.p, x, xc.p);
-    for (int k = 0; k < q.end_newton; ++k)
-      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p, nst_d.p, st))) return rc;
-    phc::scatter_rows_kernel<<<grid(A * n * cd), 128, 0, st>>>(A, n * cd, idx_d.p, xc.p, x);
-    CUDA_TRY(cudaGetLastError());
-  }
-  CUDA_TRY(cudaStreamSynchronize(st));
-  for (int64_t p = 0; p < P; ++p) {
-    status[p] = stat[p];
-    if (path_stats) {
-      path_stats[p * 5 + 0] = (double)succ[p];
-      path_stats[p * 5 + 1] = (double)steps[p];
-      path_stats[p * 5 + 2] = (double)iters[p];
-      path_stats[p * 5 + 3] = succ[p] ? min_step[p] : 0.0;
-      path_stats[p * 5 + 4] = succ[p] ? sum_step[p] / succ[p] : 0.0;
-    }
-  }
-  return PHC_OK;
-}
-
-int phc_arith_test(int32_t op, int32_t limbs, int64_t n, const double* a, const double* b, double* out, void* stream) {
-  g_err.clear();
-  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 or 4");
-  if (op < 0 || op > 9) return fail(PHC_EINVAL, "unknown op %d", op);
-  if (n < 0) return fail(PHC_EINVAL, "n < 0");
-  if (n == 0) return PHC_OK;
-  if (!a || !b || !out) return fail(PHC_EINVAL, "NULL pointer");
-  cudaStream_t st = (cudaStream_t)stream;
-  const unsigned grid = (unsigned)((n + 127) / 128);
-  if (limbs == 2)
-    phc::arith_test_kernel<2><<<grid, 128, 0, st>>>(op, n, a, b, out);
-  else
-    phc::arith_test_kernel<4><<<grid, 128, 0, st>>>(op, n, a, b, out);
-  CUDA_TRY(cudaGetLastError());
-  return PHC_OK;
 }
 
 int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* jac, void* stream) {
@@ -1392,57 +923,3 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
 }
 
 }  // extern "C"
-
-// ---------------------------------------------------------------------------
-// FP64 peak microbenchmark
-// ---------------------------------------------------------------------------
-namespace {
-__global__ void dfma_chains_kernel(double* out, int iters, double a, double b) {
-  double r[8];
-#pragma unroll
-  for (int c = 0; c < 8; ++c) r[c] = threadIdx.x * 1e-9 + c;
-  for (int i = 0; i < iters; ++i) {
-#pragma unroll
-    for (int c = 0; c < 8; ++c) r[c] = __fma_rn(r[c], a, b);
-  }
-  double s = 0;
-#pragma unroll
-  for (int c = 0; c < 8; ++c) s += r[c];
-  if (s == 12345.678) out[0] = s;
-}
-}  // namespace
-
-extern "C" int phc_fp64_peak(int32_t device, double ms_target, double* tflops) {
-  g_err.clear();
-  if (!tflops) return fail(PHC_EINVAL, "NULL out");
-  DeviceGuard g(device);
-  cudaDeviceProp p;
-  CUDA_TRY(cudaGetDeviceProperties(&p, device));
-  double* d;
-  CUDA_TRY(cudaMalloc(&d, 8));
-  const int blocks = p.multiProcessorCount * 8, threads = 256, iters = 4096;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  for (int w = 0; w < 3; ++w) dfma_chains_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
-  cudaEventRecord(e0);
-  dfma_chains_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float ms1;
-  cudaEventElapsedTime(&ms1, e0, e1);
-  int reps = std::max(1, (int)(ms_target / std::max(ms1, 1e-3f)));
-  cudaEventRecord(e0);
-  for (int r = 0; r < reps; ++r) dfma_chains_kernel<<<blocks, threads>>>(d, iters, 0.999999, 1e-7);
-  cudaEventRecord(e1);
-  cudaEventSynchronize(e1);
-  float ms;
-  cudaEventElapsedTime(&ms, e0, e1);
-  cudaError_t err = cudaGetLastError();
-  cudaFree(d);
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  if (err != cudaSuccess) return fail(PHC_ECUDA, "peak kernel: %s", cudaGetErrorString(err));
-  *tflops = 2.0 * blocks * (double)threads * iters * 8 * reps / (ms * 1e-3) / 1e12;
-  return PHC_OK;
-}

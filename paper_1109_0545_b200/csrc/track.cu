@@ -1,0 +1,173 @@
+// NEXT-4 host side: the predictor entry point and the batched path tracker (Alg. 1,
+// P:191-238; the quadratic predictor of §5), driving the kernels of
+// kernels_track.cuh and the Newton corrector (newton.cu).
+#include "runtime.h"
+#include "kernels_track.cuh"
+
+using namespace phc_rt;
+
+extern "C" {
+
+int phc_predict_batch(int32_t limbs, int32_t n_var, int64_t n_paths, int32_t order, const int32_t* n_hist,
+                      const double* t_hist, const double* x_hist, const double* t_new, double* x_out, void* stream) {
+  g_err.clear();
+  if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 or 4");
+  if (n_var < 1 || n_paths < 0) return fail(PHC_EINVAL, "n_var >= 1 and n_paths >= 0 required");
+  if (order < 0 || order > 2) return fail(PHC_EINVAL, "order must be 0, 1 or 2");
+  if (n_paths == 0) return PHC_OK;
+  if (!n_hist || !t_hist || !x_hist || !t_new || !x_out) return fail(PHC_EINVAL, "NULL pointer");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t nth = n_paths * n_var;
+  const unsigned grid = (unsigned)((nth + 127) / 128);
+  if (limbs == 2)
+    phc::predict_kernel<2><<<grid, 128, 0, st>>>(n_var, n_paths, nullptr, n_hist, t_hist, x_hist, nullptr, t_new, order,
+                                                 nullptr, x_out, nullptr);
+  else
+    phc::predict_kernel<4><<<grid, 128, 0, st>>>(n_var, n_paths, nullptr, n_hist, t_hist, x_hist, nullptr, t_new, order,
+                                                 nullptr, x_out, nullptr);
+  CUDA_TRY(cudaGetLastError());
+  return PHC_OK;
+}
+
+int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_track_params* prm, int32_t* status,
+                    double* path_stats, double* t_end, void* stream) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s || !prm) return fail(PHC_EINVAL, "NULL argument");
+  if (!s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "tracking needs a square system");
+  if (n_paths < 0) return fail(PHC_EINVAL, "n_paths < 0");
+  if (n_paths == 0) return PHC_OK;
+  if (!x || !status) return fail(PHC_EINVAL, "NULL x/status");
+  const phc_track_params& q = *prm;
+  if (!(q.step_min > 0 && q.step_min <= q.step_init && q.step_init <= q.step_max && q.step_max <= 1.0) ||
+      !(q.contract > 0 && q.contract < 1 && q.expand >= 1) || !(q.tol > 0) || q.max_newton < 1 || q.max_steps < 1 ||
+      q.end_newton < 0 || q.predictor < 0 || q.predictor > 2)
+    return fail(PHC_EINVAL, "invalid tracker parameters");
+  DeviceGuard g(s->home);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = s->n_var, L = s->L;
+  const int64_t cd = 2 * L, P = n_paths;
+  int rc;
+  DevBuf<double> t_hist, x_hist, lam_d, tc, xc, res_d;
+  DevBuf<int32_t> n_hist, idx_d, clip_d, acc_d, nst_d;
+  if ((rc = dalloc(&t_hist.p, (size_t)(P * 3 * L))) || (rc = dalloc(&x_hist.p, (size_t)(P * 3 * n * cd))) ||
+      (rc = dalloc(&lam_d.p, (size_t)P)) || (rc = dalloc(&tc.p, (size_t)(P * L))) ||
+      (rc = dalloc(&xc.p, (size_t)(P * n * cd))) || (rc = dalloc(&res_d.p, (size_t)P * q.max_newton)) ||
+      (rc = dalloc(&n_hist.p, (size_t)P)) || (rc = dalloc(&idx_d.p, (size_t)P)) || (rc = dalloc(&clip_d.p, (size_t)P)) ||
+      (rc = dalloc(&acc_d.p, (size_t)P)) || (rc = dalloc(&nst_d.p, (size_t)P * q.max_newton)))
+    return rc;
+  auto grid = [](int64_t nth) { return (unsigned)((nth + 127) / 128); };
+  if (L == 2)
+    phc::track_init_kernel<2><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
+  else
+    phc::track_init_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
+  CUDA_TRY(cudaGetLastError());
+  // host-side per-path control state (Alg. 1 step_size_control / stop_criterion); the arrays
+  // exchanged with the device every step live in pinned memory (truly asynchronous copies)
+  HostBuf<double> lam, res;
+  HostBuf<int32_t> idx, clip, acc, nst;
+  if ((rc = lam.alloc(P)) || (rc = res.alloc((size_t)P * q.max_newton)) || (rc = idx.alloc(P)) ||
+      (rc = clip.alloc(P)) || (rc = acc.alloc(P)) || (rc = nst.alloc((size_t)P * q.max_newton)))
+    return rc;
+  for (int64_t p = 0; p < P; ++p) lam[p] = q.step_init;
+  std::vector<int32_t> stat((size_t)P, 0);
+  std::vector<int64_t> steps((size_t)P, 0), succ((size_t)P, 0), iters((size_t)P, 0);
+  std::vector<double> min_step((size_t)P, 1e300), sum_step((size_t)P, 0.0);
+  while (true) {
+    int64_t A = 0;
+    for (int64_t p = 0; p < P; ++p)
+      if (stat[p] == 0) idx[A++] = (int32_t)p;
+    if (A == 0) break;
+    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(cudaMemcpyAsync(lam_d.p, lam.p, P * 8, cudaMemcpyHostToDevice, st));
+    // predict: t_try = min(t + lambda, 1), z_guess by the secant / quadratic predictor (§5)
+    if (L == 2)
+      phc::predict_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
+                                                           q.predictor, tc.p, xc.p, clip_d.p);
+    else
+      phc::predict_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
+                                                           q.predictor, tc.p, xc.p, clip_d.p);
+    CUDA_TRY(cudaGetLastError());
+    CUDA_TRY(cudaMemcpyAsync(clip.p, clip_d.p, A * 4, cudaMemcpyDeviceToHost, st));
+    // correct: Alg. 2 on h(., t_try).  All max_newton iterations are enqueued back to back
+    // (one host synchronisation per tracker step instead of one per iteration); iteration k
+    // records its residual and status in row k.  A path is corrected at the first iteration
+    // whose residual passes tol (Alg. 2 applies that iteration's update too); the iterations
+    // after it only refine the point further (documented deviation, reading T1).
+    for (int k = 0; k < q.max_newton; ++k)
+      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p + (size_t)k * A, nst_d.p + (size_t)k * A, st))) return rc;
+    CUDA_TRY(cudaMemcpyAsync(res.p, res_d.p, (size_t)q.max_newton * A * 8, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(nst.p, nst_d.p, (size_t)q.max_newton * A * 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<char> conv((size_t)A, 0), bad((size_t)A, 0);
+    for (int64_t a = 0; a < A; ++a) {
+      for (int k = 0; k < q.max_newton && !conv[a] && !bad[a]; ++k) {
+        iters[idx[a]]++;
+        const double r = res[(size_t)k * A + a];
+        if (nst[(size_t)k * A + a] != 0 || !std::isfinite(r))
+          bad[a] = 1;
+        else if (r <= q.tol)
+          conv[a] = 1;
+      }
+    }
+    // step-size control, step back, stop criterion (Alg. 1; SPEC tracker defaults)
+    for (int64_t a = 0; a < A; ++a) {
+      const int32_t p = idx[a];
+      steps[p]++;
+      const bool ok = conv[a] && !bad[a];
+      acc[a] = ok ? 1 : 0;
+      if (ok) {
+        succ[p]++;
+        min_step[p] = std::min(min_step[p], lam[p]);
+        sum_step[p] += lam[p];
+        if (clip[a]) stat[p] = 1;  // reached t = 1 with a successful correction there
+        lam[p] = std::min(lam[p] * q.expand, q.step_max);
+      } else {
+        lam[p] *= q.contract;
+        if (lam[p] < q.step_min) stat[p] = 2;
+      }
+      if (stat[p] == 0 && steps[p] >= q.max_steps) stat[p] = 2;
+    }
+    CUDA_TRY(cudaMemcpyAsync(acc_d.p, acc.p, A * 4, cudaMemcpyHostToDevice, st));
+    if (L == 2)
+      phc::accept_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
+    else
+      phc::accept_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
+    CUDA_TRY(cudaGetLastError());
+  }
+  if (L == 2)
+    phc::track_finish_kernel<2><<<grid(P * n), 128, 0, st>>>(n, P, t_hist.p, x_hist.p, x, t_end);
+  else
+    phc::track_finish_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, t_hist.p, x_hist.p, x, t_end);
+  CUDA_TRY(cudaGetLastError());
+  // end refinement at t = 1 of the paths that arrived (Newton on the target system)
+  int64_t A = 0;
+  for (int64_t p = 0; p < P; ++p)
+    if (stat[p] == 1) idx[A++] = (int32_t)p;
+  if (q.end_newton > 0 && A > 0) {
+    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
+    std::vector<double> ones((size_t)A * L, 0.0);
+    for (int64_t a = 0; a < A; ++a) ones[(size_t)a * L] = 1.0;
+    CUDA_TRY(cudaMemcpyAsync(tc.p, ones.data(), A * L * 8, cudaMemcpyHostToDevice, st));
+    phc::gather_rows_kernel<<<grid(A * n * cd), 128, 0, st>>>(A, n * cd, idx_d.p, x, xc.p);
+    for (int k = 0; k < q.end_newton; ++k)
+      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p, nst_d.p, st))) return rc;
+    phc::scatter_rows_kernel<<<grid(A * n * cd), 128, 0, st>>>(A, n * cd, idx_d.p, xc.p, x);
+    CUDA_TRY(cudaGetLastError());
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  for (int64_t p = 0; p < P; ++p) {
+    status[p] = stat[p];
+    if (path_stats) {
+      path_stats[p * 5 + 0] = (double)succ[p];
+      path_stats[p * 5 + 1] = (double)steps[p];
+      path_stats[p * 5 + 2] = (double)iters[p];
+      path_stats[p * 5 + 3] = succ[p] ? min_step[p] : 0.0;
+      path_stats[p * 5 + 4] = succ[p] ? sum_step[p] / succ[p] : 0.0;
+    }
+  }
+  return PHC_OK;
+}
+
+}  // extern "C"
