@@ -121,6 +121,7 @@ int ensure_scratch(const phc_system* s, DeviceState* d, int64_t want_points) {
   const int64_t per_point = (pt_pp + s->n_terms + s->n_factors) * (int64_t)cbytes(s);
   const int64_t budget = (int64_t)1 << 30;  // 1 GiB of scratch per device
   int64_t cap = std::max<int64_t>(1, std::min<int64_t>(want_points, budget / std::max<int64_t>(per_point, 1)));
+  cap = std::min<int64_t>(cap, 65535);  // the generic kernels put the point on gridDim.y
   if (cap <= d->chunk_cap) return PHC_OK;
   DeviceGuard g(d->dev);
   cudaDeviceSynchronize();

@@ -318,3 +318,22 @@ def test_empty_inputs(phc, L):
         F, J = he.eval_batch(Xe[:pts])
         torch.cuda.synchronize()
         assert (F == 0).all() and (J == 0).all()
+
+
+def test_generic_path_beyond_65535_points(phc):
+    """The generic path (k > 32) puts the point on gridDim.y: calls with more than 65,535
+    points are chunked (point 70,000 checked against the exact oracle)."""
+    from synthetic.systems import unit_circle_limbs
+    rng = np.random.default_rng(9)
+    n = 34
+    polys = [[[(v, 1) for v in range(33)]], [[(0, 2), (33, 1)], []]]
+    coeff = unit_circle_limbs(rng.uniform(0, 6.283, 3), 2, 1)
+    s = system_from_terms(2, n, 2, polys, coeff)
+    P = 70001
+    X = unit_circle_limbs(rng.uniform(0, 6.283, (P, n)), 2, 8)
+    F, J, h = gpu_eval(phc, s, X)
+    assert h.stats["path"] == 0
+    for p in (0, 65535, 70000):
+        ar, Fr, Jr = oracle_point(s, X[p], arith="exact")
+        ef, ej = compare_point(ar, Fr, Jr, F[p], J[p], 2)
+        assert ef <= TOL[2] and ej <= TOL[2], (p, ef, ej)
