@@ -378,15 +378,22 @@ int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, con
     const int dv = devs[gi];
     DeviceState* d;
     if ((rc = get_device_state(s, dv, &d))) break;
-    if (dv == s->home) {
+    // PHC_DEBUG_REMOTE=staged|fused (test hook): shards on the home device take the remote
+    // branches below, so the one-GPU test boxes exercise the scatter / gather bookkeeping
+    const char* dbg = getenv("PHC_DEBUG_REMOTE");
+    const int debug_remote = !dbg ? 0 : (strcmp(dbg, "fused") == 0 ? 2 : (strcmp(dbg, "staged") == 0 ? 1 : 0));
+    if (dv == s->home && !debug_remote) {
       rc = run_on_device(s, d, np, x + p0 * s->n_var * cd, T ? T + p0 * s->L : nullptr, f + p0 * s->n_eq * cd,
                          jac + p0 * (int64_t)s->n_eq * s->n_var * cd, st, n_points);
       continue;
     }
     DeviceGuard gd(dv);
     int can = 0;
-    cudaDeviceCanAccessPeer(&can, dv, s->home);
-    if (can) {
+    if (dv == s->home)
+      can = debug_remote == 2;  // own memory: "peer" pointers are plain device pointers
+    else
+      cudaDeviceCanAccessPeer(&can, dv, s->home);
+    if (can && dv != s->home) {
       cudaError_t pe = cudaDeviceEnablePeerAccess(s->home, 0);
       if (pe == cudaErrorPeerAccessAlreadyEnabled) {
         cudaGetLastError();
@@ -412,6 +419,9 @@ int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, con
     }
     if ((rc = ensure_stage(s, d, np))) break;
     if (cudaStreamWaitEvent(d->stream, start, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
+    // a device listed more than once reuses its staging buffers: the next shard's scatter and
+    // evaluation wait for the previous shard's gathers (recorded on d->done)
+    if (cudaStreamWaitEvent(d->stream, d->done, 0) != cudaSuccess) { rc = fail(PHC_ECUDA, "wait event"); break; }
     if (cudaMemcpyPeerAsync(d->xs, dv, x + p0 * s->n_var * cd, s->home, np * s->n_var * cd * 8, d->stream) != cudaSuccess) {
       rc = fail(PHC_ECUDA, "scatter copy failed");
       break;
@@ -446,6 +456,7 @@ int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, con
       }
     }
     if (rc) break;
+    cudaEventRecord(d->done, d->stream2);
     cudaEvent_t e;
     cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
     cudaEventRecord(e, d->stream2);

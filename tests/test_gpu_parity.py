@@ -337,3 +337,26 @@ def test_generic_path_beyond_65535_points(phc):
         ar, Fr, Jr = oracle_point(s, X[p], arith="exact")
         ef, ej = compare_point(ar, Fr, Jr, F[p], J[p], 2)
         assert ef <= TOL[2] and ej <= TOL[2], (p, ef, ej)
+
+
+@pytest.mark.parametrize("mode", ["staged", "fused"])
+def test_remote_shard_branches_on_one_gpu(phc, mode, monkeypatch):
+    """PHC_DEBUG_REMOTE sends the home device's shards through the remote-device branches of
+    phc_eval_jacobian_batch (staged: peer copies of chunked shards on a second stream, with a
+    device listed several times; fused: kernels storing into the home buffers): bitwise the
+    unsharded results, plain and homotopy."""
+    from synthetic import homotopy_target, random_t
+    s, X = config_system("batch", seed=8, points=3 * 8200)
+    cf = homotopy_target(s, seed=9)
+    T = random_t(X.shape[0], 2, seed=10)
+    h = phc.System(s, coeff_target=cf)
+    Xd, Td = torch.from_numpy(X).cuda(), torch.from_numpy(T).cuda()
+    F1, J1 = h.eval_batch(Xd)
+    H1, K1 = h.eval_homotopy_batch(Xd, Td)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("PHC_DEBUG_REMOTE", mode)
+    F2, J2 = h.eval_batch(Xd, devices=[0, 0, 0])
+    H2, K2 = h.eval_homotopy_batch(Xd, Td, devices=[0, 0, 0])
+    torch.cuda.synchronize()
+    assert torch.equal(F1, F2) and torch.equal(J1, J2)
+    assert torch.equal(H1, H2) and torch.equal(K1, K2)
