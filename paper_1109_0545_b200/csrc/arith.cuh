@@ -19,6 +19,20 @@ namespace phc {
 
 #define PHC_DEV __device__ __forceinline__
 
+// Device-side bounds checks of a debug build (-DPHC_CHECKS=1, __graft_entry__.build_checked):
+// compute-sanitizer is not available on this pool, so indices into the power tables, the
+// row accumulators and the term tables trap when out of range.  No-ops otherwise.
+#if PHC_CHECKS
+#define PHC_CHECK(cond) \
+  do {                  \
+    if (!(cond)) __trap(); \
+  } while (0)
+#else
+#define PHC_CHECK(cond) \
+  do {                  \
+  } while (0)
+#endif
+
 // QD dot product summation shape (1 = balanced trees, 0 = the sequential chains)
 #ifndef PHC_QD_TREE
 #define PHC_QD_TREE 1

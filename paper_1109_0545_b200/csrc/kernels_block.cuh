@@ -272,7 +272,9 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   auto entry = [&](uint32_t word) {
     uint32_t v = word & 0xffffu;
     v = (v == kDummyVar) ? (uint32_t)a.n_var : v;
-    return (int)(v * twoE + ((word >> 16) & 0xffu) - 1);
+    const uint32_t ex = (word >> 16) & 0xffu;
+    PHC_CHECK(v <= (uint32_t)a.n_var && ex >= 1 && ex <= (uint32_t)a.E);
+    return (int)(v * twoE + ex - 1);
   };
   auto ld = [&](int e) -> C {
     if constexpr (LAYOUT == 2) return cls_load<L>(reinterpret_cast<const double2*>(pt), NE, e, cls);
@@ -284,6 +286,7 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   auto rmw = [&](uint32_t word, const C& g) {
     const uint32_t v = word & 0xffffu;
     if (v != kDummyVar) {
+      PHC_CHECK(v < (uint32_t)a.n_var && (LAYOUT == 2 || (word >> 24) < (uint32_t)a.R));
       if constexpr (LAYOUT == 2) {
         double2* rw = reinterpret_cast<double2*>(rows);
         cls_store<L>(rw, a.n_var, (int)v, cls, P::add_lazy(cls_load<L>(rw, a.n_var, (int)v, cls), g));

@@ -53,6 +53,7 @@ __global__ void coef_product_kernel(const int64_t* __restrict__ cl_ptr, const in
   const double* Gp = G + p * n_factors * cd;
   for (int64_t e = cl_ptr[c]; e < cl_ptr[c + 1]; ++e) {
     const int j = cl_j[e];
+    PHC_CHECK(j >= 0 && j < M && (c == 0 || (cl_q[e] >= 0 && cl_q[e] < n_factors)));
     const C val = (c == 0) ? cload<L>(Yp + (int64_t)j * cd) : cload<L>(Gp + cl_q[e] * cd);
     const double* crow = cT + ((int64_t)j * n_eq + i0) * cd;
 #pragma unroll

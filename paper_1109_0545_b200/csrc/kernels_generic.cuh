@@ -74,6 +74,7 @@ __global__ void term_kernel(const int64_t* __restrict__ term_ptr, const uint32_t
     const typename P::real tt = P::rload(T + p * L);
     r = P::add(P::mul_real(r, P::one_minus(tt)), P::mul_real(cload<L>(coeff2 + t * 2 * L), tt));
   }
+  PHC_CHECK(k >= 0 && k <= MAXK);
   auto U = [&](uint32_t w) { return cload<L>(pt + ((int64_t)(w & 0xffffu) * 2 * E + ((w >> 16) & 0xffu) - 1) * 2 * L); };
   auto Dd = [&](uint32_t w) { return cload<L>(pt + ((int64_t)(w & 0xffffu) * 2 * E + E + ((w >> 16) & 0xffu) - 1) * 2 * L); };
   C s[MAXK];

@@ -141,6 +141,7 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
   __syncthreads();
   const int64_t t0 = a.poly_ptr[i], nt = a.poly_ptr[i + 1] - t0;
   const int64_t r0 = t0 + nt * s / a.S, r1 = t0 + nt * (s + 1) / a.S;  // this split's terms
+  PHC_CHECK(nt >= 0 && r0 <= r1);
   double* myrow = rows + (size_t)warp * a.n_var * cd;
   C fsum = P::zero();
   for (int64_t t = r0 + warp; t < r1; t += W) {
@@ -154,6 +155,7 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
       const uint32_t w = a.fac[f0 + lane];
       v = (int)(w & 0xffffu);
       const int e = (int)((w >> 16) & 0xffu);
+      PHC_CHECK(v < a.n_var && e >= 1 && e <= a.E);
       u = sload<L>(pt + ((size_t)v * twoE + e - 1) * cd);
       d = sload<L>(pt + ((size_t)v * twoE + a.E + e - 1) * cd);
     }
