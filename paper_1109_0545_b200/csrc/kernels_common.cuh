@@ -128,6 +128,57 @@ __global__ void monomial_scan_kernel(const int64_t* __restrict__ term_ptr, const
   if (lane == 31) cstore<L>(Y + (p * M + j) * cd, pre);
 }
 
+// Batch variant of the coefficient product over transposed monomial data (Y^T [M][P],
+// G^T [n_factors][P], from term_kernel<..., PTFAST>): threads run over points, so a warp
+// walks one column list with one row tile -- its coefficient loads are warp-uniform
+// broadcasts and its value loads one contiguous line per list entry.  Per output the same
+// operations in the same order as coef_product_kernel (bitwise the same results).
+template <int L, int TI>
+__global__ void coef_product_pt_kernel(const int64_t* __restrict__ cl_ptr, const int32_t* __restrict__ cl_j,
+                                       const int64_t* __restrict__ cl_q, const double* __restrict__ cT,
+                                       const double* __restrict__ cT2, const double* __restrict__ T,
+                                       const double* __restrict__ Yt, const double* __restrict__ Gt, int n_eq,
+                                       int n_var, int64_t n_points, double* __restrict__ F, double* __restrict__ J) {
+  using P = Prec<L>;
+  using C = typename P::C;
+  constexpr int cd = 2 * L;
+  const int tiles = (n_eq + TI - 1) / TI;
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = blockIdx.y / tiles;
+  const int i0 = (blockIdx.y % tiles) * TI;
+  if (p >= n_points) return;
+  C acc[TI];
+#pragma unroll
+  for (int u = 0; u < TI; ++u) acc[u] = P::zero();
+  typename P::real tt = P::one().re, omt = P::one().re;
+  if (cT2) {
+    tt = P::rload(T + p * L);
+    omt = P::one_minus(tt);
+  }
+  for (int64_t e = cl_ptr[c]; e < cl_ptr[c + 1]; ++e) {
+    const int j = cl_j[e];
+    const int64_t row = (c == 0) ? (int64_t)j : cl_q[e];
+    const C val = cload<L>((c == 0 ? Yt : Gt) + (row * n_points + p) * cd);
+    const double* crow = cT + ((int64_t)j * n_eq + i0) * cd;
+#pragma unroll
+    for (int u = 0; u < TI; ++u)
+      if (i0 + u < n_eq) {
+        C cf = cload<L>(crow + u * cd);
+        if (cT2) cf = P::add(P::mul_real(cf, omt), P::mul_real(cload<L>(cT2 + ((int64_t)j * n_eq + i0 + u) * cd), tt));
+        acc[u] = P::add_lazy(acc[u], P::mul_lazy(cf, val));
+      }
+  }
+#pragma unroll
+  for (int u = 0; u < TI; ++u) {
+    if (i0 + u >= n_eq) break;
+    const C v = P::norm(acc[u]);
+    if (c == 0)
+      cstore<L>(F + (p * n_eq + i0 + u) * cd, v);
+    else
+      cstore<L>(J + ((p * n_eq + i0 + u) * (int64_t)n_var + (c - 1)) * cd, v);
+  }
+}
+
 // Latency variant of the coefficient product for calls with few points: one warp per
 // (point, column c, row i); the 32 lanes stride over the column's list (lane l takes entries
 // l, l + 32, ...) and the partial sums meet in a fixed shuffle tree.  ~32x the parallelism of

@@ -55,7 +55,10 @@ __global__ void power_table_kernel(const double* __restrict__ X, int n_var, int 
 //                                                  c * common-factor * omega_m)
 // i.e. 4k-3 complex products per term.
 // Packed factor word: bits 0-15 variable, bits 16-23 exponent.
-template <int L, int MAXK>
+// PTFAST (the common-support batch path): threads run over points (the term tables are
+// warp-uniform loads) and Y, G are stored transposed, [t][p] and [f][p], so the coefficient
+// product reads 32 points' values of one monomial as one contiguous 1 KB (DD) line.
+template <int L, int MAXK, bool PTFAST = false>
 __global__ void term_kernel(const int64_t* __restrict__ term_ptr, const uint32_t* __restrict__ fac,
                             const double* __restrict__ coeff, const double* __restrict__ coeff2,
                             const double* __restrict__ T, const double* __restrict__ PT, int n_var, int E,
@@ -63,8 +66,8 @@ __global__ void term_kernel(const int64_t* __restrict__ term_ptr, const uint32_t
                             double* __restrict__ G) {
   using P = Prec<L>;
   using C = typename P::C;
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t p = blockIdx.y;
+  const int64_t t = PTFAST ? (int64_t)blockIdx.y : (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t p = PTFAST ? (int64_t)blockIdx.x * blockDim.x + threadIdx.x : (int64_t)blockIdx.y;
   if (t >= n_terms || p >= n_points) return;
   const double* pt = PT + p * (int64_t)(n_var + 1) * (2 * E) * (2 * L);
   const int64_t f0 = term_ptr[t];
@@ -82,15 +85,15 @@ __global__ void term_kernel(const int64_t* __restrict__ term_ptr, const uint32_t
     s[1] = U(fac[f0 + k - 1]);
     for (int q = 2; q <= k - 1; ++q) s[q] = P::mul(s[q - 1], U(fac[f0 + k - q]));
   }
-  double* g = G + (p * n_factors + f0) * 2 * L;
   for (int m = 1; m <= k; ++m) {
     const uint32_t w = fac[f0 + m - 1];
     C gm = P::mul(r, Dd(w));
     if (m < k) gm = P::mul(gm, s[k - m]);
-    cstore<L>(g + (m - 1) * 2 * L, gm);
+    const int64_t gi = PTFAST ? (f0 + m - 1) * n_points + p : p * n_factors + f0 + m - 1;
+    cstore<L>(G + gi * 2 * L, gm);
     r = P::mul(r, U(w));
   }
-  cstore<L>(Y + (p * n_terms + t) * 2 * L, r);
+  cstore<L>(Y + (PTFAST ? t * n_points + p : p * n_terms + t) * 2 * L, r);
 }
 
 // Reductions (row a7) and write of Y (row a8): one thread per (point, entry).

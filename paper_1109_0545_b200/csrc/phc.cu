@@ -268,14 +268,24 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
       const int64_t nwarps = np * s->n_terms;
       phc::monomial_scan_kernel<L><<<(unsigned)((nwarps * 32 + 127) / 128), 128, 0, st>>>(
           d->term_ptr, d->fac, d->PT, s->n_var, s->E, s->n_terms, s->n_factors, np, d->Y, d->G);
-    } else if (s->kmax <= 8)
-      launch_term<L, 8>(s, d, np, nullptr, st);
-    else if (s->kmax <= 16)
-      launch_term<L, 16>(s, d, np, nullptr, st);
-    else if (s->kmax <= 32)
-      launch_term<L, 32>(s, d, np, nullptr, st);
-    else
-      launch_term<L, PHC_MAX_K>(s, d, np, nullptr, st);
+    } else {
+      // point-fastest monomial stage with transposed outputs (see coef_product_pt_kernel)
+      ProfScope ps1(s, d->dev, 1, st);
+      const dim3 grid((unsigned)((np + 127) / 128), (unsigned)s->n_terms);
+      if (s->kmax <= 8)
+        phc::term_kernel<L, 8, true><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, nullptr, nullptr, d->PT,
+                                                          s->n_var, s->E, s->n_terms, s->n_factors, np, d->Y, d->G);
+      else if (s->kmax <= 16)
+        phc::term_kernel<L, 16, true><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, nullptr, nullptr, d->PT,
+                                                           s->n_var, s->E, s->n_terms, s->n_factors, np, d->Y, d->G);
+      else if (s->kmax <= 32)
+        phc::term_kernel<L, 32, true><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, nullptr, nullptr, d->PT,
+                                                           s->n_var, s->E, s->n_terms, s->n_factors, np, d->Y, d->G);
+      else
+        phc::term_kernel<L, PHC_MAX_K, true><<<grid, 128, 0, st>>>(d->term_ptr, d->fac, d->coeff, nullptr, nullptr,
+                                                                  d->PT, s->n_var, s->E, s->n_terms, s->n_factors, np,
+                                                                  d->Y, d->G);
+    }
     const int64_t tiles = (s->n_eq + TI - 1) / TI;
     const int64_t nthr = np * (s->n_var + 1) * tiles;
     ProfScope ps(s, d->dev, 2, st);
@@ -285,9 +295,11 @@ int run_common(const phc_system* s, DeviceState* d, int64_t n_points, const doub
           d->cl_ptr, d->cl_j, d->cl_q, d->cT, T ? d->cT2 : nullptr, T ? T + p0 * L : nullptr, d->Y, d->G, s->n_eq,
           s->n_var, s->n_terms, s->n_factors, np, f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
     } else {
-      phc::coef_product_kernel<L, TI><<<(unsigned)((nthr + 127) / 128), 128, 0, st>>>(
+      (void)nthr;
+      const dim3 grid((unsigned)((np + 127) / 128), (unsigned)((s->n_var + 1) * tiles));
+      phc::coef_product_pt_kernel<L, TI><<<grid, 128, 0, st>>>(
           d->cl_ptr, d->cl_j, d->cl_q, d->cT, T ? d->cT2 : nullptr, T ? T + p0 * L : nullptr, d->Y, d->G, s->n_eq,
-          s->n_var, s->n_terms, s->n_factors, np, f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
+          s->n_var, np, f + p0 * s->n_eq * cd, jac + p0 * (int64_t)s->n_eq * s->n_var * cd);
     }
     CUDA_TRY(cudaGetLastError());
   }
