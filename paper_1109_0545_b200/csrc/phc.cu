@@ -581,11 +581,12 @@ int phc_system_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t lim
     for (int i = 0; i < n_eq; ++i) max_terms = std::max<int64_t>(max_terms, poly_ptr[i + 1] - poly_ptr[i]);
     const int W = s->scan_W;
     s->scan_smem = ((size_t)n_var * 2 * s->E + (size_t)W * n_var + W) * 2 * limbs * sizeof(double);
+    s->scan_S = (int)std::max<int64_t>(1, std::min<int64_t>(148 / n_eq, (max_terms + W - 1) / W));
     // only for terms long enough that the block kernel's per-lane chain (4k - 3 products) is
     // the latency: measured kernel times tiny (k = 4) 9.2 us block vs 10.7 us latency path,
-    // c2 (k = 10) 12.6 vs 12.5, c3 (k = 20) 75 vs 47 (tools/regime_ab.sh)
+    // c2 (k = 10) 12.6 vs 12.5, c3 (k = 20) 75 vs 47 (tools/regime_ab.sh); k <= 2 tracker
+    // systems: the block path is as fast or faster and steadier (tools/track_regime.py)
     s->scan_ok = kmax >= 12 && kmax <= 32 && s->scan_smem <= (size_t)200 * 1024 && max_terms > 0;
-    s->scan_S = (int)std::max<int64_t>(1, std::min<int64_t>(148 / n_eq, (max_terms + W - 1) / W));
   }
   s->ca_per_point = s->plan.usable ? s->plan.ca_per_point : s->ca_per_point;
   DeviceState* d;
