@@ -181,7 +181,10 @@ PHC_DEV qd renorm4_robust(double a0, double a1, double a2, double a3) {
   two_sum(a0, s, c0, c1);
   qd r;
   double e;
-  two_sum(c0, c1, r.x[0], e);
+  // two_sum(c0, c1) would return (c0, c1) unchanged: c1 is the rounding error of c0 = fl(.),
+  // so |c1| <= ulp(c0)/2 and, on a tie, c0 is already even -- skipped (6 DADD per product)
+  r.x[0] = c0;
+  e = c1;
   two_sum(e, c2, r.x[1], e);
   two_sum(e, c3, r.x[2], r.x[3]);
   return r;

@@ -90,7 +90,7 @@ struct HostBlockPlan {
 struct OpFlops { int cm, cm_lazy, ca, ca_lazy, norm, ci; };
 inline OpFlops op_flops(int L) {
   if (L == 2) return {50, 44, 22, 16, 12, 16};
-  return {480, 480, 183, 183, 0, 130};
+  return {468, 468, 183, 183, 0, 130};
 }
 
 struct BlockArgs {
