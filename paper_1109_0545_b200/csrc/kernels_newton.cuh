@@ -39,7 +39,8 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   __shared__ double red_v[32];
   __shared__ int red_i[32];
   __shared__ int s_piv, s_bad;
-  __shared__ __align__(16) double s_inv[2 * L];  // reciprocal of the current pivot
+  __shared__ __align__(16) double s_inv[2 * L];   // reciprocal of the current pivot
+  __shared__ __align__(16) double s_inv2[2 * L];  // ... of the next column's (look-ahead)
   const int64_t p = blockIdx.x;
   if (p >= a.n_points) return;
   const int n = a.n, cols = n + 1, cd = 2 * L;
@@ -73,13 +74,16 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     a.resid[p] = r;
   }
   __syncthreads();
-  // elimination with partial pivoting
-  for (int k = 0; k < n; ++k) {
-    // pivot: largest |M[i][k]|^2 (leading limbs) over i >= k; ties -> smallest i
+  // Elimination with partial pivoting and a one-column look-ahead: while warps 1.. update
+  // the trailing columns k+2.. of step k, warp 0 updates column k+1, finds its pivot and
+  // forms the pivot reciprocal, so the serial reciprocal overlaps the update (three block
+  // barriers per column instead of six).  Same operations per entry as before.
+  // column 0: pivot (block-wide), swap, reciprocal
+  {
     double best = -1.0;
     int bi = n;
-    for (int i = k + tid; i < n; i += T) {
-      const double v = P::abs2_hi(ldm(i, k));
+    for (int i = tid; i < n; i += T) {
+      const double v = P::abs2_hi(ldm(i, 0));
       if (v > best) { best = v; bi = i; }
     }
     for (int o = 16; o; o >>= 1) {
@@ -98,33 +102,78 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       if (!(b > 0.0)) s_bad = 1;
     }
     __syncthreads();
-    if (s_bad) break;
-    const int pv = s_piv;
-    if (pv != k)
-      for (int j = k + tid; j < cols; j += T) {
-        const C u = ldm(k, j), v = ldm(pv, j);
-        stm(k, j, v);
-        stm(pv, j, u);
+    if (!s_bad) {
+      const int pv = s_piv;
+      if (pv != 0)
+        for (int j = tid; j < cols; j += T) {
+          const C u = ldm(0, j), v = ldm(pv, j);
+          stm(0, j, v);
+          stm(pv, j, u);
+        }
+      __syncthreads();
+      if (tid == 0) {
+        const C inv = P::recip(ldm(0, 0));
+        sstore<L>(s_inv, inv);
+        sstore<L>(invd, inv);
       }
-    __syncthreads();
-    if (tid == 0) {
-      const C inv = P::recip(ldm(k, k));
-      sstore<L>(s_inv, inv);
-      sstore<L>(invd + (size_t)k * cd, inv);
+      __syncthreads();
     }
-    __syncthreads();
+  }
+  for (int k = 0; k < n && !s_bad; ++k) {
     const C inv = sload<L>(s_inv);
     // multipliers l_i = M[i][k] / M[k][k], stored in column k
     for (int i = k + 1 + tid; i < n; i += T) stm(i, k, P::mul(ldm(i, k), inv));
-    __syncthreads();
-    // update M[i][j] -= l_i M[k][j], i > k, j > k
-    const int rows = n - k - 1, ucols = cols - k - 1;
-    for (int e = tid; e < rows * ucols; e += T) {
-      const int i = k + 1 + e / ucols, j = k + 1 + e % ucols;
-      stm(i, j, P::sub(ldm(i, j), P::mul(ldm(i, k), ldm(k, j))));
+    __syncthreads();  // (1)
+    if (k == n - 1) break;
+    if (wid == 0) {
+      // look-ahead: column k+1, its pivot among rows k+1.., the pivot reciprocal
+      for (int i = k + 1 + lane; i < n; i += 32)
+        stm(i, k + 1, P::sub(ldm(i, k + 1), P::mul(ldm(i, k), ldm(k, k + 1))));
+      __syncwarp();
+      double best = -1.0;
+      int bi = n;
+      for (int i = k + 1 + lane; i < n; i += 32) {
+        const double v = P::abs2_hi(ldm(i, k + 1));
+        if (v > best) { best = v; bi = i; }
+      }
+      for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+      }
+      if (lane == 0) {
+        if (!(best > 0.0)) {
+          s_bad = 1;
+        } else {
+          s_piv = bi;
+          sstore<L>(s_inv2, P::recip(ldm(bi, k + 1)));
+        }
+      }
+    } else {
+      // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1
+      const int rows = n - k - 1, ucols = cols - k - 2;
+      for (int e = tid - 32; e < rows * ucols; e += T - 32) {
+        const int i = k + 1 + e / ucols, j = k + 2 + e % ucols;
+        stm(i, j, P::sub(ldm(i, j), P::mul(ldm(i, k), ldm(k, j))));
+      }
     }
-    __syncthreads();
+    __syncthreads();  // (2)
+    if (s_bad) break;
+    const int pv = s_piv;
+    if (pv != k + 1)
+      for (int j = k + 1 + tid; j < cols; j += T) {
+        const C u = ldm(k + 1, j), v = ldm(pv, j);
+        stm(k + 1, j, v);
+        stm(pv, j, u);
+      }
+    if (tid == 0) {
+      const C inv2 = sload<L>(s_inv2);
+      sstore<L>(s_inv, inv2);
+      sstore<L>(invd + (size_t)(k + 1) * cd, inv2);
+    }
+    __syncthreads();  // (3)
   }
+  __syncthreads();
   if (s_bad) {
     if (tid == 0) a.status[p] = 1;
     for (int e = tid; e < n; e += T)
