@@ -188,3 +188,22 @@ def test_warp_and_cta_eliminations_agree_bitwise(phc, name):
     torch.cuda.synchronize()
     assert (sa == 0).all() and (sb == 0).all()
     assert torch.equal(Xa[:4095], Xb) and torch.equal(ra[:4095], rb)
+
+
+def test_newton_cta_kernel_singular_and_lookahead_pivot(phc):
+    """The shared-memory CTA elimination (n = 40 QD, one point): a variable absent from the
+    system gives a zero pivot column found by the look-ahead warp -> status 1, x unchanged;
+    the other point of the batch (a regular system) is solved."""
+    from synthetic import random_system
+    s, X = random_system(40, 6, 5, 2, 4, seed=6, points=2)
+    keep = s.var_idx != 39
+    counts = np.add.reduceat(keep.astype(np.int64), s.term_ptr[:-1])
+    counts[np.diff(s.term_ptr) == 0] = 0
+    s.term_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    s.var_idx, s.exponent = s.var_idx[keep].copy(), s.exponent[keep].copy()
+    xn, res, status, h = _gpu_step(phc, s, X)
+    assert (status == 1).all()
+    assert np.array_equal(xn, X)
+    s2, X2 = random_system(40, 6, 5, 2, 4, seed=7, points=1)
+    xn2, res2, st2, _ = _gpu_step(phc, s2, X2)
+    assert st2[0] == 0
