@@ -50,8 +50,11 @@ constexpr int kWarp = 32;
 #ifndef PHC_DD_L2_WARPS
 #define PHC_DD_L2_WARPS 4
 #endif
+#ifndef PHC_OTHER_WARPS
+#define PHC_OTHER_WARPS 8
+#endif
 __host__ __device__ constexpr int block_warps(int L, int layout) {
-  return (L == 2 && layout == 2) ? PHC_DD_L2_WARPS : 8;
+  return (L == 2 && layout == 2) ? PHC_DD_L2_WARPS : PHC_OTHER_WARPS;
 }
 constexpr uint32_t kDummyVar = 0xFFFFu;
 
