@@ -16,18 +16,20 @@
 //  * coef[block][lane][2][L]                                (256-bit vector loads)
 //
 // Per lane (= per term c * prod u_j, u_j = x_{v_j}^{a_j}, d_j = a_j x_{v_j}^{a_j-1}):
-//   backward: s_1 = u_K, s_q = s_{q-1} u_{K-q+1}              (suffixes, the paper's phi)
-//   forward : r_0 = c, g_m = r_{m-1} d_m s_{K-m}, r_m = r_{m-1} u_m  (prefixes psi with c)
-//   value y = r_K; g_m is added into row[rep][var] in shared memory (conflict-free by the
-//   colouring), slot after slot.  y is reduced over the warp with a shuffle tree.
+//   prefixes r_0 = c, r_m = r_{m-1} u_m and suffixes s_1 = u_K, s_q = s_{q-1} u_{K-q+1}
+//   (the paper's psi with c folded in, and phi) run simultaneously, two dependency chains
+//   (do_block); g_m = r_{m-1} d_m s_{K-m}; value y = r_K.  g_m is added into
+//   row[rep][var] in shared memory (conflict-free by the colouring), slot after slot; y is
+//   reduced over the warp with a shuffle tree.
 // That is 4K-3 complex products per term, against the paper's 6k-5.
 //
 // Work split (fixed per system, so every point is evaluated bitwise identically):
-//  * mode A (few blocks per polynomial): a CTA takes one point and a group of
-//    polynomials; warp w owns polynomials w, w+NW, ...; it accumulates all their blocks in
-//    its private rows and writes F[i] and J[i][:] itself.
-//  * mode B (many blocks per polynomial): a CTA takes one (point, polynomial); warp w owns
-//    blocks w, w+NW, ...; the CTA sums the warps' rows in warp order.
+//  * mode A (short polynomials or light terms, plan_blocks): a CTA takes one point and a
+//    group of polynomials (the whole point for batches); warp w owns polynomials w, w+NW,
+//    ...; it accumulates all their blocks in its private rows and writes F[i] and J[i][:]
+//    itself (the grouping does not change any polynomial's arithmetic).
+//  * mode B (>= 4 blocks per polynomial, or >= 2 with K >= 12): a CTA takes one (point,
+//    polynomial); warp w owns blocks w, w+NW, ...; the CTA sums the warps' rows in warp order.
 #pragma once
 #include <cuda_runtime.h>
 
