@@ -200,10 +200,11 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
 }
 
 // ---------------------------------------------------------------------------------------
-// Small systems (n <= 32): one WARP per point, lane i owns row i of [J | -F] (in the warp's
-// slice of shared memory); no block barriers -- the pivot is a warp argmax, every lane
-// computes the pivot reciprocal itself (same inputs, same bits), the row swap is one column
-// per lane.  Same pivot rule, operations and order per entry as newton_solve_kernel, so the
+// Small systems (n <= 32): one WARP per point, [J | -F] in the warp's slice of shared memory;
+// no block barriers -- the pivot is a warp argmax over lane = row, every lane computes the
+// pivot reciprocal itself (same inputs, same bits), the row swap is one column per lane, lane
+// i forms multiplier i, and the trailing update is spread over the lanes by (row, column)
+// pairs.  Same pivot rule, operations and order per entry as newton_solve_kernel, so the
 // two kernels give bitwise identical steps; this one avoids ~5 block barriers per column
 // (the tracker's corrector at n = 8: 26 us -> a few us per call).
 // ---------------------------------------------------------------------------------------
@@ -258,10 +259,15 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     __syncwarp();
     const C inv = P::recip(sload<L>(at(k, k)));
     if (lane == k) inv_diag = inv;
-    if (lane > k && lane < n) {
-      const C l = P::mul(sload<L>(at(lane, k)), inv);
-      sstore<L>(at(lane, k), l);
-      for (int j = k + 1; j < cols; ++j) sstore<L>(at(lane, j), P::sub(sload<L>(at(lane, j)), P::mul(l, sload<L>(at(k, j)))));
+    if (lane > k && lane < n) sstore<L>(at(lane, k), P::mul(sload<L>(at(lane, k)), inv));
+    __syncwarp();
+    // trailing update spread over the lanes by (row, column) pairs: ceil((n-k-1)(n-k) / 32)
+    // entries per lane instead of a whole row of n-k entries
+    const int w = n - k;  // columns k+1 .. n
+    const int ne = (n - k - 1) * w;
+    for (int e = lane; e < ne; e += 32) {
+      const int i = k + 1 + e / w, j = k + 1 + e % w;
+      sstore<L>(at(i, j), P::sub(sload<L>(at(i, j)), P::mul(sload<L>(at(i, k)), sload<L>(at(k, j)))));
     }
     __syncwarp();
   }

@@ -105,6 +105,62 @@ __global__ void accept_kernel(int n, int64_t A, const int32_t* __restrict__ idx,
   }
 }
 
+// Step-size control, step back and stop criterion of Alg. 1 (reading T1) for the
+// active paths of one tracker step, on the device (the host only looks at the statuses once
+// per window of steps, phc_track_paths).  One thread per active path a = 0..A-1:
+//   corrected at the first Newton iteration k whose residual res[k][a] <= tol (a singular
+//   step or a non-finite residual before that fails the correction); accepted steps expand
+//   lambda (capped at step_max) and finish the path when the predictor clipped t to 1;
+//   rejected steps contract lambda and fail the path below step_min; max_steps caps the steps.
+// Paths that stopped earlier in the window (stat != 0) are left untouched (acc = 0).
+struct TrackCtl {
+  double step_min, step_max, expand, contract, tol;
+  int max_newton, max_steps;
+};
+__global__ void control_kernel(int64_t A, const int32_t* __restrict__ idx, const TrackCtl c,
+                               const double* __restrict__ res, const int32_t* __restrict__ nst,
+                               const int32_t* __restrict__ clipped, int32_t* __restrict__ acc,
+                               int32_t* __restrict__ stat, double* __restrict__ lam, int64_t* __restrict__ steps,
+                               int64_t* __restrict__ succ, int64_t* __restrict__ iters,
+                               double* __restrict__ min_step, double* __restrict__ sum_step) {
+  const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= A) return;
+  const int64_t p = idx[a];
+  if (stat[p] != 0) {
+    acc[a] = 0;
+    return;
+  }
+  bool conv = false, bad = false;
+  int64_t it = 0;
+  for (int k = 0; k < c.max_newton && !conv && !bad; ++k) {
+    ++it;
+    const double r = res[(int64_t)k * A + a];
+    if (nst[(int64_t)k * A + a] != 0 || !isfinite(r))
+      bad = true;
+    else if (r <= c.tol)
+      conv = true;
+  }
+  iters[p] += it;
+  const int64_t sp = ++steps[p];
+  const bool ok = conv && !bad;
+  acc[a] = ok ? 1 : 0;
+  int32_t st = 0;
+  double l = lam[p];
+  if (ok) {
+    succ[p] += 1;
+    min_step[p] = fmin(min_step[p], l);
+    sum_step[p] += l;
+    if (clipped[a]) st = 1;  // reached t = 1 with a successful correction there
+    l = fmin(l * c.expand, c.step_max);
+  } else {
+    l *= c.contract;
+    if (l < c.step_min) st = 2;
+  }
+  if (st == 0 && sp >= c.max_steps) st = 2;
+  lam[p] = l;
+  stat[p] = st;
+}
+
 // Start: slot 0 = the start solution at t = 0, one valid slot.
 template <int L>
 __global__ void track_init_kernel(int n, int64_t P_, const double* __restrict__ x, int32_t* __restrict__ n_hist,

@@ -70,7 +70,9 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
     ProfScope ps(s, d->dev, 2, st);
     // small systems: one warp per point (bitwise the same step as the CTA kernel)
     const size_t per_warp = (size_t)n * (n + 1) * cd * sizeof(double);
-    if (n <= 32 && (n <= 16 || n_points < 4096)) {
+    static const int warp_env = getenv("PHC_NEWTON_WARP") ? atoi(getenv("PHC_NEWTON_WARP")) : -1;  // A/B hook
+    const bool warp_kernel = warp_env >= 0 ? (n <= 32 && warp_env == 1) : (n <= 32 && (n <= 16 || n_points < 4096));
+    if (warp_kernel) {
       const int wpc = per_warp * 4 <= (size_t)160 * 1024 ? 4 : (per_warp * 2 <= (size_t)160 * 1024 ? 2 : 1);
       const size_t sm = per_warp * wpc;
       const unsigned grid = (unsigned)((np + wpc - 1) / wpc);

@@ -49,13 +49,17 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   const int n = s->n_var, L = s->L;
   const int64_t cd = 2 * L, P = n_paths;
   int rc;
-  DevBuf<double> t_hist, x_hist, lam_d, tc, xc, res_d;
-  DevBuf<int32_t> n_hist, idx_d, clip_d, acc_d, nst_d;
+  DevBuf<double> t_hist, x_hist, lam_d, tc, xc, res_d, minst_d, sumst_d;
+  DevBuf<int32_t> n_hist, idx_d, clip_d, acc_d, nst_d, stat_d;
+  DevBuf<int64_t> steps_d, succ_d, iters_d;
   if ((rc = dalloc(&t_hist.p, (size_t)(P * 3 * L))) || (rc = dalloc(&x_hist.p, (size_t)(P * 3 * n * cd))) ||
       (rc = dalloc(&lam_d.p, (size_t)P)) || (rc = dalloc(&tc.p, (size_t)(P * L))) ||
       (rc = dalloc(&xc.p, (size_t)(P * n * cd))) || (rc = dalloc(&res_d.p, (size_t)P * q.max_newton)) ||
+      (rc = dalloc(&minst_d.p, (size_t)P)) || (rc = dalloc(&sumst_d.p, (size_t)P)) ||
       (rc = dalloc(&n_hist.p, (size_t)P)) || (rc = dalloc(&idx_d.p, (size_t)P)) || (rc = dalloc(&clip_d.p, (size_t)P)) ||
-      (rc = dalloc(&acc_d.p, (size_t)P)) || (rc = dalloc(&nst_d.p, (size_t)P * q.max_newton)))
+      (rc = dalloc(&acc_d.p, (size_t)P)) || (rc = dalloc(&nst_d.p, (size_t)P * q.max_newton)) ||
+      (rc = dalloc(&stat_d.p, (size_t)P)) || (rc = dalloc(&steps_d.p, (size_t)P)) || (rc = dalloc(&succ_d.p, (size_t)P)) ||
+      (rc = dalloc(&iters_d.p, (size_t)P)))
     return rc;
   auto grid = [](int64_t nth) { return (unsigned)((nth + 127) / 128); };
   if (L == 2)
@@ -63,79 +67,69 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   else
     phc::track_init_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, x, n_hist.p, t_hist.p, x_hist.p);
   CUDA_TRY(cudaGetLastError());
-  // host-side per-path control state (Alg. 1 step_size_control / stop_criterion); the arrays
-  // exchanged with the device every step live in pinned memory (truly asynchronous copies)
-  HostBuf<double> lam, res;
-  HostBuf<int32_t> idx, clip, acc, nst;
-  if ((rc = lam.alloc(P)) || (rc = res.alloc((size_t)P * q.max_newton)) || (rc = idx.alloc(P)) ||
-      (rc = clip.alloc(P)) || (rc = acc.alloc(P)) || (rc = nst.alloc((size_t)P * q.max_newton)))
-    return rc;
-  for (int64_t p = 0; p < P; ++p) lam[p] = q.step_init;
-  std::vector<int32_t> stat((size_t)P, 0);
-  std::vector<int64_t> steps((size_t)P, 0), succ((size_t)P, 0), iters((size_t)P, 0);
-  std::vector<double> min_step((size_t)P, 1e300), sum_step((size_t)P, 0.0);
+  // Per-path control state (Alg. 1 step_size_control / stop_criterion) lives on the device
+  // and is updated by control_kernel after every step, so W steps are enqueued back to back
+  // with no host synchronisation; the host reads the statuses once per window and re-compacts
+  // the active paths.  A path that stops inside a window is skipped by the control kernel
+  // for the rest of it (its predictor/corrector work there is wasted, not used), so the
+  // window changes no decision: the result is that of a host check after every step.
+  HostBuf<double> lam, minst;
+  HostBuf<int32_t> idx, stat;
+  if ((rc = lam.alloc(P)) || (rc = minst.alloc(P)) || (rc = idx.alloc(P)) || (rc = stat.alloc(P))) return rc;
+  for (int64_t p = 0; p < P; ++p) {
+    lam[p] = q.step_init;
+    minst[p] = 1e300;
+    stat[p] = 0;
+  }
+  CUDA_TRY(cudaMemcpyAsync(lam_d.p, lam.p, P * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemcpyAsync(minst_d.p, minst.p, P * 8, cudaMemcpyHostToDevice, st));
+  CUDA_TRY(cudaMemsetAsync(sumst_d.p, 0, P * 8, st));
+  CUDA_TRY(cudaMemsetAsync(stat_d.p, 0, P * 4, st));
+  CUDA_TRY(cudaMemsetAsync(steps_d.p, 0, P * 8, st));
+  CUDA_TRY(cudaMemsetAsync(succ_d.p, 0, P * 8, st));
+  CUDA_TRY(cudaMemsetAsync(iters_d.p, 0, P * 8, st));
+  const phc::TrackCtl ctl{q.step_min, q.step_max, q.expand, q.contract, q.tol, q.max_newton, q.max_steps};
+  const char* wenv = getenv("PHC_TRACK_WINDOW");
+  const int window = wenv ? std::max(1, atoi(wenv)) : 8;
   while (true) {
     int64_t A = 0;
     for (int64_t p = 0; p < P; ++p)
       if (stat[p] == 0) idx[A++] = (int32_t)p;
     if (A == 0) break;
     CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
-    CUDA_TRY(cudaMemcpyAsync(lam_d.p, lam.p, P * 8, cudaMemcpyHostToDevice, st));
-    // predict: t_try = min(t + lambda, 1), z_guess by the secant / quadratic predictor (§5)
-    if (L == 2)
-      phc::predict_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
-                                                           q.predictor, tc.p, xc.p, clip_d.p);
-    else
-      phc::predict_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p, nullptr,
-                                                           q.predictor, tc.p, xc.p, clip_d.p);
-    CUDA_TRY(cudaGetLastError());
-    CUDA_TRY(cudaMemcpyAsync(clip.p, clip_d.p, A * 4, cudaMemcpyDeviceToHost, st));
-    // correct: Alg. 2 on h(., t_try).  All max_newton iterations are enqueued back to back
-    // (one host synchronisation per tracker step instead of one per iteration); iteration k
-    // records its residual and status in row k.  A path is corrected at the first iteration
-    // whose residual passes tol (Alg. 2 applies that iteration's update too); the iterations
-    // after it only refine the point further (documented deviation, reading T1).
-    for (int k = 0; k < q.max_newton; ++k)
-      if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p + (size_t)k * A, nst_d.p + (size_t)k * A, st))) return rc;
-    CUDA_TRY(cudaMemcpyAsync(res.p, res_d.p, (size_t)q.max_newton * A * 8, cudaMemcpyDeviceToHost, st));
-    CUDA_TRY(cudaMemcpyAsync(nst.p, nst_d.p, (size_t)q.max_newton * A * 4, cudaMemcpyDeviceToHost, st));
+    for (int w = 0; w < window; ++w) {
+      // predict: t_try = min(t + lambda, 1), z_guess by the secant / quadratic predictor (§5)
+      if (L == 2)
+        phc::predict_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p,
+                                                             nullptr, q.predictor, tc.p, xc.p, clip_d.p);
+      else
+        phc::predict_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, n_hist.p, t_hist.p, x_hist.p, lam_d.p,
+                                                             nullptr, q.predictor, tc.p, xc.p, clip_d.p);
+      CUDA_TRY(cudaGetLastError());
+      // correct: Alg. 2 on h(., t_try).  All max_newton iterations are enqueued back to back;
+      // iteration k records its residual and status in row k.  A path is corrected at the
+      // first iteration whose residual passes tol (Alg. 2 applies that iteration's update
+      // too); the iterations after it only refine the point further (documented deviation,
+      // DESIGN.md reading T1).
+      for (int k = 0; k < q.max_newton; ++k)
+        if ((rc = newton_impl(s, A, xc.p, tc.p, xc.p, res_d.p + (size_t)k * A, nst_d.p + (size_t)k * A, st)))
+          return rc;
+      // step-size control, step back, stop criterion (Alg. 1), then the history shift of the
+      // accepted steps
+      phc::control_kernel<<<grid(A), 128, 0, st>>>(A, idx_d.p, ctl, res_d.p, nst_d.p, clip_d.p, acc_d.p, stat_d.p,
+                                                   lam_d.p, steps_d.p, succ_d.p, iters_d.p, minst_d.p, sumst_d.p);
+      if (L == 2)
+        phc::accept_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p,
+                                                            x_hist.p);
+      else
+        phc::accept_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p,
+                                                            x_hist.p);
+      CUDA_TRY(cudaGetLastError());
+    }
+    CUDA_TRY(cudaMemcpyAsync(stat.p, stat_d.p, P * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<char> conv((size_t)A, 0), bad((size_t)A, 0);
-    for (int64_t a = 0; a < A; ++a) {
-      for (int k = 0; k < q.max_newton && !conv[a] && !bad[a]; ++k) {
-        iters[idx[a]]++;
-        const double r = res[(size_t)k * A + a];
-        if (nst[(size_t)k * A + a] != 0 || !std::isfinite(r))
-          bad[a] = 1;
-        else if (r <= q.tol)
-          conv[a] = 1;
-      }
-    }
-    // step-size control, step back, stop criterion (Alg. 1; SPEC tracker defaults)
-    for (int64_t a = 0; a < A; ++a) {
-      const int32_t p = idx[a];
-      steps[p]++;
-      const bool ok = conv[a] && !bad[a];
-      acc[a] = ok ? 1 : 0;
-      if (ok) {
-        succ[p]++;
-        min_step[p] = std::min(min_step[p], lam[p]);
-        sum_step[p] += lam[p];
-        if (clip[a]) stat[p] = 1;  // reached t = 1 with a successful correction there
-        lam[p] = std::min(lam[p] * q.expand, q.step_max);
-      } else {
-        lam[p] *= q.contract;
-        if (lam[p] < q.step_min) stat[p] = 2;
-      }
-      if (stat[p] == 0 && steps[p] >= q.max_steps) stat[p] = 2;
-    }
-    CUDA_TRY(cudaMemcpyAsync(acc_d.p, acc.p, A * 4, cudaMemcpyHostToDevice, st));
-    if (L == 2)
-      phc::accept_kernel<2><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
-    else
-      phc::accept_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p, x_hist.p);
-    CUDA_TRY(cudaGetLastError());
   }
+  std::vector<int32_t> stat_v(stat.p, stat.p + P);
   if (L == 2)
     phc::track_finish_kernel<2><<<grid(P * n), 128, 0, st>>>(n, P, t_hist.p, x_hist.p, x, t_end);
   else
@@ -144,7 +138,7 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   // end refinement at t = 1 of the paths that arrived (Newton on the target system)
   int64_t A = 0;
   for (int64_t p = 0; p < P; ++p)
-    if (stat[p] == 1) idx[A++] = (int32_t)p;
+    if (stat_v[p] == 1) idx[A++] = (int32_t)p;
   if (q.end_newton > 0 && A > 0) {
     CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
     std::vector<double> ones((size_t)A * L, 0.0);
@@ -156,9 +150,16 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
     phc::scatter_rows_kernel<<<grid(A * n * cd), 128, 0, st>>>(A, n * cd, idx_d.p, xc.p, x);
     CUDA_TRY(cudaGetLastError());
   }
+  std::vector<int64_t> steps((size_t)P), succ((size_t)P), iters((size_t)P);
+  std::vector<double> min_step((size_t)P), sum_step((size_t)P);
+  CUDA_TRY(cudaMemcpyAsync(steps.data(), steps_d.p, P * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(succ.data(), succ_d.p, P * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(iters.data(), iters_d.p, P * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(min_step.data(), minst_d.p, P * 8, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(cudaMemcpyAsync(sum_step.data(), sumst_d.p, P * 8, cudaMemcpyDeviceToHost, st));
   CUDA_TRY(cudaStreamSynchronize(st));
   for (int64_t p = 0; p < P; ++p) {
-    status[p] = stat[p];
+    status[p] = stat_v[p];
     if (path_stats) {
       path_stats[p * 5 + 0] = (double)succ[p];
       path_stats[p * 5 + 1] = (double)steps[p];

@@ -128,3 +128,29 @@ def test_track_rejects_bad_parameters(phc):
     plain = phc.System(s)
     with pytest.raises(phc.PhcError):
         plain.track(_cuda(limbs_from_values([1.0], 2)[None]))
+
+
+def test_track_window_changes_no_decision(phc, monkeypatch):
+    """The device-side step control runs W steps between host checks (phc_track_paths); a
+    path that stops inside a window is frozen by the control kernel, so every window size
+    gives bitwise the same end points, statuses and per-path statistics as W = 1."""
+    s, cf, X0 = total_degree_homotopy(4, 2, seed=3)
+    h = phc.System(s, coeff_target=cf)
+    out = {}
+    for w in (1, 3, 8, 64):
+        monkeypatch.setenv("PHC_TRACK_WINDOW", str(w))
+        Xe, status, stats, te = h.track(_cuda(X0), t_end=True)
+        out[w] = (Xe.cpu().numpy(), status, stats, te.cpu().numpy())
+    for w in (3, 8, 64):
+        for a, b in zip(out[1], out[w]):
+            assert np.array_equal(a, b), w
+    assert (out[1][1] == 1).all()
+
+
+def test_track_max_steps_inside_window(phc, monkeypatch):
+    """max_steps smaller than the window: every path stops at exactly max_steps steps."""
+    s, cf, X0 = total_degree_homotopy(3, 2, seed=7)
+    h = phc.System(s, coeff_target=cf)
+    monkeypatch.setenv("PHC_TRACK_WINDOW", "16")
+    _, status, stats = h.track(_cuda(X0), max_steps=5)
+    assert (status == 2).all() and (stats[:, 1] == 5).all(), (status, stats[:, 1])
