@@ -260,7 +260,9 @@ int phc_profile_read(const phc_system* s, double ms[4], int64_t launches[4], int
  * asynchronous on `stream`).  op 0 two_sum / 1 two_prod: a, b [n] doubles -> out [n][2];
  * 2 add / 3 mul / 4 div of reals: [n][limbs]; 5 complex mul / 6 complex add / 7 lazy complex
  * mul + renormalisation / 8 complex reciprocal (of a): [n][2][limbs]; 9 real times the
- * double b[i][0].  PHC_EINVAL for an unknown op. */
+ * double b[i][0]; 10 complex reciprocal as the eliminations form it (one warp per operand,
+ * the two long divisions on two lanes: must equal op 8 bitwise).  PHC_EINVAL for an
+ * unknown op. */
 int phc_arith_test(int32_t op, int32_t limbs, int64_t n, const double* a, const double* b, double* out, void* stream);
 
 /* Thread-local message describing the last failure in this thread ("" if none). */

@@ -458,8 +458,10 @@ template <> struct Prec<2> {
   PHC_DEV static C neg(const C& a) { C r; r.re = dd_neg(a.re); r.im = dd_neg(a.im); return r; }
   PHC_DEV static C sub(const C& a, const C& b) { return add(a, neg(b)); }
   // 1 / a = conj(a) / |a|^2
+  // |a|^2 (the denominator of the reciprocal)
+  PHC_DEV static real abs2(const C& a) { return dd_add(dd_mul(a.re, a.re), dd_mul(a.im, a.im)); }
   PHC_DEV static C recip(const C& a) {
-    const dd d = dd_add(dd_mul(a.re, a.re), dd_mul(a.im, a.im));
+    const dd d = abs2(a);
     C r;
     r.re = dd_div(a.re, d);
     r.im = dd_neg(dd_div(a.im, d));
@@ -513,8 +515,9 @@ template <> struct Prec<4> {
   PHC_DEV static C mul_int(const C& a, double s) { C r; r.re = mul_int_real(a.re, s); r.im = mul_int_real(a.im, s); return r; }
   PHC_DEV static C neg(const C& a) { C r; r.re = qd_neg(a.re); r.im = qd_neg(a.im); return r; }
   PHC_DEV static C sub(const C& a, const C& b) { return add(a, neg(b)); }
+  PHC_DEV static real abs2(const C& a) { return qd_dot2(a.re, a.re, a.im, a.im); }
   PHC_DEV static C recip(const C& a) {
-    const qd d = qd_dot2(a.re, a.re, a.im, a.im);
+    const qd d = abs2(a);
     C r;
     r.re = qd_div(a.re, d);
     r.im = qd_neg(qd_div(a.im, d));

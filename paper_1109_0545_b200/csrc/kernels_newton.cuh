@@ -9,8 +9,11 @@
 //    row-per-thread assignment a (row, column) grid-stride over the CTA;
 //  * newton_warp_kernel: n <= 32, one warp per point (lane = row), no block barriers;
 //  * the multi-kernel elimination (newton_*_kernel below): matrices beyond shared memory, two
-//    launches per column over all points, the trailing update spread over many SMs.
+//    launches per column over all points, the trailing update spread over many SMs;
+//  * newton_coop_kernel: matrices beyond shared memory and few points, one persistent
+//    cooperative launch (grid-wide barriers instead of kernel boundaries, one per column).
 #pragma once
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -18,6 +21,25 @@
 #include "arith.cuh"
 
 namespace phc {
+
+// The pivot reciprocal (the serial step of every elimination column) computed by a whole
+// warp: lane 0 divides the real part by |a|^2, lane 1 the imaginary part -- P::recip's own
+// operations, so the value is bitwise P::recip(a) -- and every lane receives the result.  The
+// two long divisions then run side by side instead of interleaved in one thread.
+// Call with the full warp converged.
+template <int L>
+PHC_DEV typename Prec<L>::C recip_warp(const typename Prec<L>::C& a, int lane) {
+  using P = Prec<L>;
+  typename P::C r;
+  const typename P::real d = P::abs2(a);
+  const typename P::real q = P::rdiv((lane & 1) ? a.im : a.re, d);
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    r.re.x[i] = __shfl_sync(0xffffffffu, q.x[i], 0);
+    r.im.x[i] = -__shfl_sync(0xffffffffu, q.x[i], 1);
+  }
+  return r;
+}
 
 struct NewtonArgs {
   const double* X;  // [P][n][2][L]
@@ -111,10 +133,12 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
           stm(pv, j, u);
         }
       __syncthreads();
-      if (tid == 0) {
-        const C inv = P::recip(ldm(0, 0));
-        sstore<L>(s_inv, inv);
-        sstore<L>(invd, inv);
+      if (wid == 0) {
+        const C inv = recip_warp<L>(ldm(0, 0), lane);
+        if (lane == 0) {
+          sstore<L>(s_inv, inv);
+          sstore<L>(invd, inv);
+        }
       }
       __syncthreads();
     }
@@ -141,22 +165,29 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
         const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
         if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
       }
-      if (lane == 0) {
-        if (!(best > 0.0)) {
-          s_bad = 1;
-        } else {
+      if (!(best > 0.0)) {
+        if (lane == 0) s_bad = 1;
+      } else {
+        const C inv2 = recip_warp<L>(ldm(bi, k + 1), lane);  // best, bi are warp-uniform
+        if (lane == 0) {
           s_piv = bi;
-          sstore<L>(s_inv2, P::recip(ldm(bi, k + 1)));
+          sstore<L>(s_inv2, inv2);
         }
       }
     } else {
-      // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1
+      // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1, by the warps that do not
+      // share warp 0's scheduler (warp w issues on SMSP w % 4): the look-ahead chain above is
+      // the critical path of the column and runs alone on its SMSP
+      if ((wid & 3) == 0 && nwarp > 4) goto skip_update;
+      const int worker = (nwarp > 4) ? (wid >> 2) * 3 + (wid & 3) - 1 : wid - 1;
+      const int nworker = (nwarp > 4) ? (nwarp >> 2) * 3 : nwarp - 1;
       const int rows = n - k - 1, ucols = cols - k - 2;
-      for (int e = tid - 32; e < rows * ucols; e += T - 32) {
+      for (int e = worker * 32 + lane; e < rows * ucols; e += nworker * 32) {
         const int i = k + 1 + e / ucols, j = k + 2 + e % ucols;
         stm(i, j, P::sub(ldm(i, j), P::mul(ldm(i, k), ldm(k, j))));
       }
     }
+  skip_update:
     __syncthreads();  // (2)
     if (s_bad) break;
     const int pv = s_piv;
@@ -257,7 +288,7 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
         sstore<L>(at(bi, j), u);
       }
     __syncwarp();
-    const C inv = P::recip(sload<L>(at(k, k)));
+    const C inv = recip_warp<L>(sload<L>(at(k, k)), lane);
     if (lane == k) inv_diag = inv;
     if (lane > k && lane < n) sstore<L>(at(lane, k), P::mul(sload<L>(at(lane, k)), inv));
     __syncwarp();
@@ -379,10 +410,12 @@ __global__ void __launch_bounds__(256) newton_pivot_kernel(const NewtonArgs a, i
       sstore<L>(at(pv, j), u);
     }
   __syncthreads();
-  if (tid == 0) {
-    const C inv = P::recip(sload<L>(at(k, k)));
-    sstore<L>(s_inv, inv);
-    sstore<L>(invd + (size_t)k * cd, inv);
+  if (wid == 0) {
+    const C inv = recip_warp<L>(sload<L>(at(k, k)), lane);
+    if (lane == 0) {
+      sstore<L>(s_inv, inv);
+      sstore<L>(invd + (size_t)k * cd, inv);
+    }
   }
   __syncthreads();
   const C inv = sload<L>(s_inv);
@@ -430,6 +463,267 @@ __global__ void __launch_bounds__(256) newton_backsub_kernel(const NewtonArgs a)
   for (int e = tid; e < n; e += T) {
     const double* xp = a.X + ((size_t)p * n + e) * cd;
     cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), sload<L>(at(e, n))));
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// Few points with matrices beyond shared memory (large QD single point: n = 256, 4.2 MB):
+// one persistent cooperative launch of one CTA per SM per point, in place of the 2n launches
+// of the multi-kernel path (whose ~10 us per launch were the cost: 4.9 ms for n = 256).
+// Per column k, one grid-wide barrier:
+//   CTA 0 (look-ahead): column k+1 of rows i > k updated, its pivot (largest leading-limb
+//     modulus, ties to the lowest row), the row exchange (in the permutation perm_g: rows
+//     are not moved), the pivot reciprocal (recip_warp) and the multipliers of column k+1;
+//   CTAs 1..G-1: the trailing update of step k, rows i > k, columns j >= k+2.
+// CTA 0's chain is the critical path, so its operands stay on chip: the updated column in
+// shared memory (pivot search and reciprocal read it there), each thread's multipliers in
+// registers for the next column's update (thread t owns logical rows c+1+t, c+1+t+T, ...
+// of column c in both steps).  Rows are addressed through the permutation (the other CTAs
+// take a snapshot after the barrier); the CTA kernel's row swaps move only columns that are
+// read later, so the per-entry operations, their order and the pivot choices are those of
+// newton_solve_kernel: bitwise the same step (tested).  Back substitution and update on CTA 0.
+// ---------------------------------------------------------------------------------------
+// complex load through L2 (ld.global.cg): the cooperative kernel's CTAs read entries other
+// CTAs wrote before the last grid barrier, never a stale L1 line
+template <int L>
+PHC_DEV typename Prec<L>::C ldl2(const double* p) {
+  typename Prec<L>::C v;
+#pragma unroll
+  for (int q = 0; q < L; q += 2) {
+    const double2 r = __ldcg(reinterpret_cast<const double2*>(p + q));
+    const double2 m = __ldcg(reinterpret_cast<const double2*>(p + L + q));
+    v.re.x[q] = r.x;
+    v.re.x[q + 1] = r.y;
+    v.im.x[q] = m.x;
+    v.im.x[q + 1] = m.y;
+  }
+  return v;
+}
+#ifndef PHC_COOP_TRACE
+#define PHC_COOP_TRACE 0
+#endif
+#if PHC_COOP_TRACE
+__device__ unsigned long long g_coop_trace[4096][6];
+PHC_DEV unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define COOP_T(k, s) \
+  if (tid == 0 && b == 0 && (k) < 4096) g_coop_trace[k][s] = gtime();
+#else
+#define COOP_T(k, s)
+#endif
+// c - a b and a b, as every elimination forms them
+template <int L>
+PHC_DEV typename Prec<L>::C cmul_c(const typename Prec<L>::C& a, const typename Prec<L>::C& b) {
+  return Prec<L>::mul(a, b);
+}
+template <int L>
+PHC_DEV typename Prec<L>::C cfms_c(const typename Prec<L>::C& c, const typename Prec<L>::C& a,
+                                   const typename Prec<L>::C& b) {
+  return Prec<L>::sub(c, Prec<L>::mul(a, b));
+}
+constexpr int kCoopThreads = 256;
+constexpr int kCoopRows = 4;  // chain rows per thread of CTA 0: n <= 1 + 4 * 256
+// shared memory of the cooperative kernel: colv, lmul [n][2L] + perm [n]
+__host__ __device__ inline size_t coop_smem_bytes(int n, int L) {
+  return (size_t)2 * n * 2 * L * sizeof(double) + (size_t)n * sizeof(int);
+}
+template <int L>
+__global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonArgs a,
+                                                                   int32_t* __restrict__ perm_g,  // [2][n]
+                                                                   double* __restrict__ red_g,
+                                                                   int32_t* __restrict__ flag_g) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  using P = Prec<L>;
+  using C = typename P::C;
+  extern __shared__ __align__(16) double csm[];
+  const int n = a.n, cols = n + 1, cd = 2 * L;
+  // CTA 0's on-chip columns, indexed by PHYSICAL row: colv = the look-ahead column c (pivot
+  // search, reciprocal, multipliers), lmul = the multipliers of column c
+  double* colv = csm;
+  double* lmul = colv + (size_t)n * cd;
+  int* perm = reinterpret_cast<int*>(lmul + (size_t)n * cd);  // [n] row permutation
+  __shared__ double red_v[32];
+  __shared__ int red_i[32];
+  __shared__ int s_bad;
+  __shared__ __align__(16) double s_inv[2 * L];
+  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
+  const int G = gridDim.x, b = blockIdx.x;
+  auto cval = [&](const double* base, int ph) { return sload<L>(base + (size_t)ph * cd); };
+  // CTA 0, warp 0: final argmax over the warps' candidates (ties to the lowest logical row),
+  // exchange of logical rows c and the winner, pivot reciprocal.  Uniform across warp 0.
+  auto pivot_and_recip = [&](double* invd, int c) {
+    double best = lane < nwarp ? red_v[lane] : -1.0;
+    int bi = lane < nwarp ? red_i[lane] : n;
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (!(best > 0.0)) {
+      if (lane == 0) {
+        s_bad = 1;
+        flag_g[0] = 1;
+      }
+      return;
+    }
+    const int ph = perm[bi];  // physical pivot row (all lanes read before lane 0 swaps)
+    __syncwarp();
+    const C inv = recip_warp<L>(cval(colv, ph), lane);
+    if (lane == 0) {
+      perm[bi] = perm[c];
+      perm[c] = ph;
+      sstore<L>(s_inv, inv);
+      sstore<L>(invd + (size_t)c * cd, inv);
+    }
+  };
+  // CTA 0: multipliers l_i = colv / pivot of the logical rows i > c (after the exchange)
+  auto multipliers = [&](double* M, int c) {
+    const C inv = sload<L>(s_inv);
+    for (int i = c + 1 + tid; i < n; i += T) {
+      const int ph = perm[i];
+      const C l = cmul_c<L>(cval(colv, ph), inv);
+      sstore<L>(lmul + (size_t)ph * cd, l);
+      sstore<L>(M + ((size_t)ph * cols + c) * cd, l);
+    }
+    // the permutation after exchange c goes to buffer c & 1: the other CTAs read buffer
+    // (c - 1) & 1 while this one is written (no torn snapshot)
+    for (int i = tid; i < n; i += T) perm_g[(size_t)(c & 1) * n + i] = perm[i];
+  };
+  // per-thread candidate -> warp argmax -> red_v / red_i
+  auto warp_candidates = [&](double best, int bi) {
+    for (int o = 16; o; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
+    }
+    if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
+  };
+  for (int64_t p = 0; p < a.n_points; ++p) {
+    double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
+    double* invd = M + (size_t)n * cols * cd;
+    auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
+    const double* Fp = a.F + (size_t)p * n * cd;
+    const double* Jp = a.J + (size_t)p * n * n * cd;
+    // [J | -F] and the residual, spread over the grid
+    double rmax = 0.0;
+    for (int64_t e = (int64_t)b * T + tid; e < (int64_t)n * cols; e += (int64_t)G * T) {
+      const int i = (int)(e / cols), j = (int)(e % cols);
+      if (j < n) {
+        sstore<L>(at(i, j), cload<L>(Jp + ((size_t)i * n + j) * cd));
+      } else {
+        const C f = cload<L>(Fp + (size_t)i * cd);
+        rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
+        sstore<L>(at(i, j), P::neg(f));
+      }
+    }
+    for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    if (lane == 0) red_v[wid] = rmax;
+    __syncthreads();
+    if (tid == 0) {
+      double r = 0.0;
+      for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
+      red_g[b] = r;
+      s_bad = 0;
+    }
+    if (b == 0 && tid == 0) flag_g[0] = 0;
+    grid.sync();
+    if (b == 0) {
+      // column 0: pivot, exchange, reciprocal, multipliers; column 1 kept for step 0
+      if (tid == 0) {
+        double r = 0.0;
+        for (int q = 0; q < G; ++q) r = fmax(r, __ldcg(red_g + q));
+        a.resid[p] = r;
+      }
+      double best = -1.0;
+      int bi = n;
+      for (int i = tid; i < n; i += T) {
+        perm[i] = i;
+        const C v = ldl2<L>(at(i, 0));
+        sstore<L>(colv + (size_t)i * cd, v);
+        const double m = P::abs2_hi(v);
+        if (m > best) { best = m; bi = i; }
+      }
+      warp_candidates(best, bi);
+      __syncthreads();
+      if (wid == 0) pivot_and_recip(invd, 0);
+      __syncthreads();
+      if (!s_bad) multipliers(M, 0);
+    }
+    grid.sync();
+    for (int k = 0; k < n - 1; ++k) {
+      if (b == 0) {
+        if (s_bad) break;
+        COOP_T(k, 0)
+        // look-ahead column k+1: v = M[i][k+1] - l_i u_k (u_k = column k+1 of pivot row k)
+        const C uk = ldl2<L>(at(perm[k], k + 1));
+        double best = -1.0;
+        int bi = n;
+#pragma unroll
+        for (int q = 0; q < kCoopRows; ++q) {
+          const int i = k + 1 + tid + q * T;
+          if (i < n) {
+            const int ph = perm[i];
+            const C v = cfms_c<L>(ldl2<L>(at(ph, k + 1)), cval(lmul, ph), uk);
+            sstore<L>(colv + (size_t)ph * cd, v);
+            const double m = P::abs2_hi(v);
+            if (m > best) { best = m; bi = i; }
+          }
+        }
+        warp_candidates(best, bi);
+        __syncthreads();
+        COOP_T(k, 1)
+        if (wid == 0) pivot_and_recip(invd, k + 1);
+        __syncthreads();
+        COOP_T(k, 2)
+        if (!s_bad) multipliers(M, k + 1);
+        COOP_T(k, 3)
+      } else {
+        if (tid == 0) s_bad = __ldcg(flag_g);
+        __syncthreads();
+        if (s_bad) break;  // grid-uniform: written before the last barrier
+        for (int i = tid; i < n; i += T) perm[i] = __ldcg(perm_g + (size_t)(k & 1) * n + i);
+        __syncthreads();
+        // trailing update of step k: rows i > k, columns j >= k + 2 (CTA 0 takes k+1)
+        const int rows = n - k - 1, ucols = cols - k - 2;
+        const int64_t ne = ucols > 0 ? (int64_t)rows * ucols : 0;
+        const double* prow = at(perm[k], 0);
+        for (int64_t e = (int64_t)(b - 1) * T + tid; e < ne; e += (int64_t)(G - 1) * T) {
+          const int i = k + 1 + (int)(e / ucols), j = k + 2 + (int)(e % ucols);
+          double* rw = at(perm[i], 0);
+          sstore<L>(rw + (size_t)j * cd, cfms_c<L>(ldl2<L>(rw + (size_t)j * cd), ldl2<L>(rw + (size_t)k * cd),
+                                                   ldl2<L>(prow + (size_t)j * cd)));
+        }
+      }
+      COOP_T(k, 4)
+      grid.sync();
+      COOP_T(k, 5)
+    }
+    if (b == 0) {
+      if (s_bad) {
+        if (tid == 0) a.status[p] = 1;
+        for (int e = tid; e < n; e += T)
+          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
+      } else {
+        for (int i = n - 1; i >= 0; --i) {
+          if (tid == 0) sstore<L>(at(perm[i], n), cmul_c<L>(ldl2<L>(at(perm[i], n)), ldl2<L>(invd + (size_t)i * cd)));
+          __syncthreads();
+          const C xi = ldl2<L>(at(perm[i], n));
+          for (int r = tid; r < i; r += T)
+            sstore<L>(at(perm[r], n), cfms_c<L>(ldl2<L>(at(perm[r], n)), ldl2<L>(at(perm[r], i)), xi));
+          __syncthreads();
+        }
+        for (int e = tid; e < n; e += T) {
+          const double* xp = a.X + ((size_t)p * n + e) * cd;
+          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), ldl2<L>(at(perm[e], n))));
+        }
+        if (tid == 0) a.status[p] = 0;
+      }
+    }
+    grid.sync();  // perm_g, red_g and flag_g are reused by the next point
   }
 }
 

@@ -4,6 +4,7 @@
 // exact rationals.  Not on the evaluation path.
 #pragma once
 #include "arith.cuh"
+#include "kernels_newton.cuh"
 
 namespace phc {
 
@@ -18,6 +19,7 @@ enum ArithOp {
   kCplxMulLazyNorm = 7,  // the hot path's lazy product followed by its renormalisation
   kCplxRecip = 8,        // out = 1 / a
   kRealMulD = 9,         // out = a * b[.][0] (QD x double / DD x double)
+  kCplxRecipWarp = 10,   // out = 1 / a by recip_warp (kernels_newton.cuh), one warp per element
 };
 
 template <int L>
@@ -67,6 +69,20 @@ __global__ void arith_test_kernel(int op, int64_t n, const double* __restrict__ 
     }
     default: break;
   }
+}
+
+// op 10: one warp per element, the eliminations' two-lane reciprocal
+template <int L>
+__global__ void recip_warp_test_kernel(int64_t n, const double* __restrict__ a, double* __restrict__ out) {
+  using P = Prec<L>;
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (i >= n) return;  // warp-uniform
+  typename P::C v;
+  for (int q = 0; q < L; ++q) { v.re.x[q] = a[(i * 2) * L + q]; v.im.x[q] = a[(i * 2 + 1) * L + q]; }
+  const typename P::C r = recip_warp<L>(v, lane);
+  if (lane == 0)
+    for (int q = 0; q < L; ++q) { out[(i * 2) * L + q] = r.re.x[q]; out[(i * 2 + 1) * L + q] = r.im.x[q]; }
 }
 
 }  // namespace phc

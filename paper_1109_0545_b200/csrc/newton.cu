@@ -5,6 +5,8 @@
 
 namespace phc_rt {
 
+constexpr int64_t kCoopMaxPoints = 4;  // cooperative elimination up to this many points per call
+
 // Multi-kernel elimination (kernels_newton.cuh) for matrices beyond shared memory.
 template <int L>
 void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
@@ -16,6 +18,46 @@ void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
     if (work > 0) phc::newton_update_kernel<L><<<dim3((unsigned)((work + 255) / 256), (unsigned)np), 256, 0, st>>>(a, k);
   }
   phc::newton_backsub_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
+}
+
+// One cooperative launch per chunk (kernels_newton.cuh newton_coop_kernel): one CTA per SM.
+template <int L>
+int newton_coop(const phc::NewtonArgs& a, DeviceState* d, cudaStream_t st) {
+  static std::mutex mu;
+  static std::map<int, int> sms;  // device -> SM count (cooperative grid size)
+  int G;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = sms.find(d->dev);
+    if (it == sms.end()) {
+      int nsm = 0;
+      CUDA_TRY(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, d->dev));
+      it = sms.emplace(d->dev, nsm).first;
+    }
+    G = it->second;
+  }
+  const size_t smem = phc::coop_smem_bytes(a.n, L);
+  if (smem > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_coop_kernel<L>, smem));
+  int nb = 0;
+  CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, phc::newton_coop_kernel<L>, phc::kCoopThreads, smem));
+  if (nb < 1) return fail(PHC_ECUDA, "cooperative elimination kernel does not fit an SM");
+  const int64_t need = G + a.n + 2;
+  if (d->naux_cap < need) {
+    cudaStreamSynchronize(st);
+    if (d->nAux) cudaFree(d->nAux);
+    d->nAux = nullptr;
+    d->naux_cap = 0;
+    int rc = dalloc(&d->nAux, (size_t)need);
+    if (rc) return rc;
+    d->naux_cap = need;
+  }
+  double* red = d->nAux;
+  int32_t* perm = reinterpret_cast<int32_t*>(d->nAux + G);
+  int32_t* flag = perm + 2 * a.n;
+  phc::NewtonArgs args = a;
+  void* kargs[] = {(void*)&args, (void*)&perm, (void*)&red, (void*)&flag};
+  CUDA_TRY(cudaLaunchCooperativeKernel((const void*)phc::newton_coop_kernel<L>, dim3((unsigned)G), dim3(phc::kCoopThreads), kargs, smem, st));
+  return PHC_OK;
 }
 
 int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const double* T, double* x_new,
@@ -36,20 +78,27 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
   const int n = s->n_eq, L = s->L;
   const int64_t cd = 2 * L;
   const size_t mat = ((size_t)n * (n + 1) + n) * cd * sizeof(double);  // [J | -F] + pivot reciprocals
-  const bool smem = mat <= (size_t)200 * 1024;
+  const bool smem = mat <= (size_t)200 * 1024 && !getenv("PHC_NEWTON_GLOBAL");  // (test hook: global-memory paths)
   const int64_t per_point = (int64_t)n * n * cd * 8 + (smem ? 0 : (int64_t)mat);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)512 << 20) / per_point));
   if (d->n_cap < chunk) {
     cudaStreamSynchronize(st);
-    for (double** q : {&d->nF, &d->nJ, &d->nM}) {
+    for (double** q : {&d->nF, &d->nJ}) {
       if (*q) cudaFree(*q);
       *q = nullptr;
     }
     d->n_cap = 0;
     if ((rc = dalloc(&d->nF, (size_t)(chunk * n * cd)))) return rc;
     if ((rc = dalloc(&d->nJ, (size_t)(chunk * n * n * cd)))) return rc;
-    if (!smem && (rc = dalloc(&d->nM, (size_t)chunk * mat / sizeof(double)))) return rc;
     d->n_cap = chunk;
+  }
+  if (!smem && d->nM_cap < chunk) {  // global elimination matrices, sized separately
+    cudaStreamSynchronize(st);
+    if (d->nM) cudaFree(d->nM);
+    d->nM = nullptr;
+    d->nM_cap = 0;
+    if ((rc = dalloc(&d->nM, (size_t)chunk * mat / sizeof(double)))) return rc;
+    d->nM_cap = chunk;
   }
   // few points: 512 threads spread one elimination over the whole SM; batches: 128-256 per point
   const int threads = n_points < 148 ? 512 : (n <= 48 ? 128 : 256);
@@ -70,7 +119,7 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
     ProfScope ps(s, d->dev, 2, st);
     // small systems: one warp per point (bitwise the same step as the CTA kernel)
     const size_t per_warp = (size_t)n * (n + 1) * cd * sizeof(double);
-    static const int warp_env = getenv("PHC_NEWTON_WARP") ? atoi(getenv("PHC_NEWTON_WARP")) : -1;  // A/B hook
+    const int warp_env = getenv("PHC_NEWTON_WARP") ? atoi(getenv("PHC_NEWTON_WARP")) : -1;  // A/B hook
     const bool warp_kernel = warp_env >= 0 ? (n <= 32 && warp_env == 1) : (n <= 32 && (n <= 16 || n_points < 4096));
     if (warp_kernel) {
       const int wpc = per_warp * 4 <= (size_t)160 * 1024 ? 4 : (per_warp * 2 <= (size_t)160 * 1024 ? 2 : 1);
@@ -86,10 +135,17 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
       CUDA_TRY(cudaGetLastError());
       continue;
     }
+    // matrices beyond shared memory: one cooperative launch for few points (the points one
+    // after another, each over all SMs), the multi-kernel path (all points at once) otherwise
+    const int coop_env = getenv("PHC_NEWTON_COOP") ? atoi(getenv("PHC_NEWTON_COOP")) : -1;  // A/B hook
+    const bool coop_ok = n <= 1 + phc::kCoopRows * phc::kCoopThreads && phc::coop_smem_bytes(n, L) <= (size_t)200 * 1024;
+    const bool coop = coop_ok && (coop_env >= 0 ? coop_env == 1 : np <= kCoopMaxPoints);
     if (L == 2) {
       if (smem) {
         if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2>, mat));
         phc::newton_solve_kernel<2><<<(unsigned)np, threads, mat, st>>>(a);
+      } else if (coop) {
+        if ((rc = newton_coop<2>(a, d, st))) return rc;
       } else {
         newton_multi<2>(a, np, st);
       }
@@ -97,6 +153,8 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
       if (smem) {
         if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4>, mat));
         phc::newton_solve_kernel<4><<<(unsigned)np, threads, mat, st>>>(a);
+      } else if (coop) {
+        if ((rc = newton_coop<4>(a, d, st))) return rc;
       } else {
         newton_multi<4>(a, np, st);
       }

@@ -87,7 +87,9 @@ struct DeviceState {
   double* nF = nullptr;
   double* nJ = nullptr;
   double* nM = nullptr;
-  int64_t n_cap = 0;
+  int64_t n_cap = 0, nM_cap = 0;
+  double* nAux = nullptr;  // cooperative elimination: per-CTA residuals, row permutation, flag
+  int64_t naux_cap = 0;
   // latency (warp-scan) path: partial rows of the S splits
   double* part = nullptr;
   int64_t part_cap = 0;
@@ -104,7 +106,8 @@ struct DeviceState {
     for (void* p : {(void*)term_ptr, (void*)fac, (void*)coeff, (void*)poly_ptr, (void*)jptr, (void*)jidx, (void*)PT,
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
                     (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
-                    (void*)cl_q, (void*)cT, (void*)part, (void*)count, (void*)cT2})
+                    (void*)cl_q, (void*)cT, (void*)part, (void*)count, (void*)cT2, (void*)nF, (void*)nJ,
+                    (void*)nM, (void*)nAux})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (stream2) cudaStreamDestroy(stream2);

@@ -10,11 +10,20 @@ extern "C" {
 int phc_arith_test(int32_t op, int32_t limbs, int64_t n, const double* a, const double* b, double* out, void* stream) {
   g_err.clear();
   if (limbs != 2 && limbs != 4) return fail(PHC_EUNSUPPORTED, "limbs must be 2 or 4");
-  if (op < 0 || op > 9) return fail(PHC_EINVAL, "unknown op %d", op);
+  if (op < 0 || op > 10) return fail(PHC_EINVAL, "unknown op %d", op);
   if (n < 0) return fail(PHC_EINVAL, "n < 0");
   if (n == 0) return PHC_OK;
   if (!a || !b || !out) return fail(PHC_EINVAL, "NULL pointer");
   cudaStream_t st = (cudaStream_t)stream;
+  if (op == phc::kCplxRecipWarp) {
+    const unsigned wgrid = (unsigned)((n + 3) / 4);
+    if (limbs == 2)
+      phc::recip_warp_test_kernel<2><<<wgrid, 128, 0, st>>>(n, a, out);
+    else
+      phc::recip_warp_test_kernel<4><<<wgrid, 128, 0, st>>>(n, a, out);
+    CUDA_TRY(cudaGetLastError());
+    return PHC_OK;
+  }
   const unsigned grid = (unsigned)((n + 127) / 128);
   if (limbs == 2)
     phc::arith_test_kernel<2><<<grid, 128, 0, st>>>(op, n, a, b, out);

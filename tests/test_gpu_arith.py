@@ -136,3 +136,18 @@ def test_signed_zero_and_exact_cases(phc):
         z = za * zb
         assert np.array_equal(out[:, 0, 0], z.real) and np.array_equal(out[:, 1, 0], z.imag)
         assert (out[:, :, 1:] == 0).all()
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_warp_reciprocal_equals_reciprocal(phc, L):
+    """The eliminations' pivot reciprocal (recip_warp: the two long divisions on two lanes)
+    is P::recip bitwise, including signed zeros and tiny/huge moduli."""
+    rng = np.random.default_rng(40 + L)
+    n = 4000
+    a = np.stack([real_limbs(rand_reals(rng, n, L, 30), L), real_limbs(rand_reals(rng, n, L, 30), L)], axis=1)
+    a[:5, 1] = 0.0                       # real operands
+    a[5:10, 0] = 0.0                     # imaginary operands
+    a[10:15, 1] = -0.0
+    r8 = run(phc, 8, L, a, a, (n, 2, L))
+    r10 = run(phc, 10, L, a, a, (n, 2, L))
+    assert np.array_equal(r8.view(np.uint64), r10.view(np.uint64))

@@ -145,9 +145,12 @@ def test_newton_singular_and_in_place(phc):
     assert torch.equal(out, B)
 
 
-def test_newton_multi_kernel_path_vs_oracle(phc):
-    """n = 64 QD: [J | -F] (266 KB) exceeds shared memory, so the elimination runs as two
-    launches per column over many SMs (kernels_newton.cuh, multi-kernel path)."""
+@pytest.mark.parametrize("coop", ["0", "1"])
+def test_newton_multi_kernel_path_vs_oracle(phc, monkeypatch, coop):
+    """n = 64 QD: [J | -F] (266 KB) exceeds shared memory, so the elimination runs in global
+    memory over many SMs: two launches per column (multi-kernel path, coop = 0) or one
+    cooperative launch with a grid barrier per column (coop = 1)."""
+    monkeypatch.setenv("PHC_NEWTON_COOP", coop)
     from synthetic import random_system
     s, X = random_system(64, 8, 6, 3, 4, seed=3, points=2)
     xn, res, status, h = _gpu_step(phc, s, X)
@@ -160,9 +163,11 @@ def test_newton_multi_kernel_path_vs_oracle(phc):
         assert err <= _tol(4, 64, cond), (p, err, cond)
 
 
-def test_newton_multi_kernel_singular(phc):
-    """Multi-kernel path: a variable absent from the system -> zero pivot column -> status 1,
-    x unchanged; the other point of the batch is unaffected."""
+@pytest.mark.parametrize("coop", ["0", "1"])
+def test_newton_multi_kernel_singular(phc, monkeypatch, coop):
+    """Global-memory paths: a variable absent from the system -> zero pivot column -> status 1,
+    x unchanged, for both points."""
+    monkeypatch.setenv("PHC_NEWTON_COOP", coop)
     from synthetic import random_system
     s, X = random_system(60, 6, 5, 2, 4, seed=4, points=2)
     keep = s.var_idx != 59
@@ -207,3 +212,39 @@ def test_newton_cta_kernel_singular_and_lookahead_pivot(phc):
     s2, X2 = random_system(40, 6, 5, 2, 4, seed=7, points=1)
     xn2, res2, st2, _ = _gpu_step(phc, s2, X2)
     assert st2[0] == 0
+
+
+@pytest.mark.parametrize("name,points", [("c3", 3), ("c2", 2)])
+def test_global_eliminations_equal_shared_memory_kernel_bitwise(phc, monkeypatch, name, points):
+    """The three CTA-level eliminations -- shared memory (one CTA per point), multi-kernel and
+    cooperative (global memory, forced with PHC_NEWTON_GLOBAL) -- make the same pivot choices
+    and the same operations per entry in the same order: bitwise equal steps."""
+    s, X = config_system(name, seed=9, points=points)
+    h = phc.System(s)
+    Xd = torch.from_numpy(X).cuda()
+    monkeypatch.setenv("PHC_NEWTON_WARP", "0")
+    ref = h.newton_step(Xd)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("PHC_NEWTON_GLOBAL", "1")
+    for coop in ("0", "1"):
+        monkeypatch.setenv("PHC_NEWTON_COOP", coop)
+        out = h.newton_step(Xd)
+        torch.cuda.synchronize()
+        for a, b in zip(ref, out):
+            assert torch.equal(a, b), coop
+
+
+def test_cooperative_elimination_singular_first_column(phc, monkeypatch):
+    """Cooperative path, zero pivot in column 0 (variable 0 absent): status 1, x unchanged."""
+    from synthetic import random_system
+    s, X = random_system(40, 6, 5, 2, 4, seed=8, points=1)
+    keep = s.var_idx != 0
+    counts = np.add.reduceat(keep.astype(np.int64), s.term_ptr[:-1])
+    counts[np.diff(s.term_ptr) == 0] = 0
+    s.term_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    s.var_idx, s.exponent = s.var_idx[keep].copy(), s.exponent[keep].copy()
+    monkeypatch.setenv("PHC_NEWTON_GLOBAL", "1")
+    monkeypatch.setenv("PHC_NEWTON_COOP", "1")
+    xn, res, status, h = _gpu_step(phc, s, X)
+    assert status[0] == 1
+    assert np.array_equal(xn, X)

@@ -1,0 +1,41 @@
+// Single-thread dependent-chain latency of the DD/QD complex operations (clock cycles per op):
+// the serial parts of the eliminations (pivot reciprocal, multiplier, update entry) are
+// bound by these, not by FP64 throughput.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -I paper_1109_0545_b200/csrc tools/op_latency.cu -o /tmp/op_latency
+#include <cstdio>
+#include "arith.cuh"
+using namespace phc;
+
+template <int L, int OP>
+__global__ void lat(double* out, long long* cyc, int reps) {
+  using P = Prec<L>;
+  typename P::C x = P::one(), y = P::one();
+  x.re.x[0] = 0.9; x.im.x[0] = 0.3; x.re.x[1] = 1e-17;
+  y.re.x[0] = 0.8; y.im.x[0] = -0.6; y.im.x[1] = 3e-18;
+  long long t0 = clock64();
+  for (int i = 0; i < reps; ++i) {
+    if constexpr (OP == 0) x = P::recip(x);
+    if constexpr (OP == 1) x = P::mul(x, y);
+    if constexpr (OP == 2) x = P::add(x, y);
+    if constexpr (OP == 3) x = P::sub(x, P::mul(x, y));
+  }
+  long long t1 = clock64();
+  out[0] = x.re.x[0] + x.im.x[0];
+  cyc[0] = (t1 - t0) / reps;
+}
+
+int main() {
+  double* o;
+  long long* c;
+  cudaMalloc(&o, 8);
+  cudaMalloc(&c, 8);
+  const char* names[] = {"recip", "mul", "add", "x - x*y"};
+  long long h;
+#define RUN(L, OP)                                  \
+  lat<L, OP><<<1, 1>>>(o, c, 64);                   \
+  lat<L, OP><<<1, 1>>>(o, c, 256);                  \
+  cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);     \
+  printf("L=%d %-8s %lld cycles\n", L, names[OP], h);
+  RUN(2, 0) RUN(2, 1) RUN(2, 2) RUN(2, 3) RUN(4, 0) RUN(4, 1) RUN(4, 2) RUN(4, 3)
+  return 0;
+}
