@@ -117,7 +117,12 @@ int phc_eval_jacobian_batch_host(const phc_system* s, int64_t n_points, const do
  *   x_new[p] := x_p + dz
  *   status[p] := 0, or 1 when a pivot column is exactly zero (x_new[p] := x_p).
  * x, x_new [n_points][n][2][L], residual [n_points] (double), status [n_points] (int32):
- * device pointers on the home device; x_new may alias x.  Asynchronous on `stream`. */
+ * device pointers on the home device; x_new may alias x.  Asynchronous on `stream`.
+ * The elimination runs one warp per point (n <= 32 and few points), one CTA per point with
+ * [J | -F] in shared memory, or -- matrices beyond shared memory -- one cooperative launch
+ * over all SMs (<= 4 points) or two launches per column (more points); all of them make the
+ * same pivot choices and operations per entry, so the step is bitwise the same in every
+ * regime.  Uses cudaLaunchCooperativeKernel in the cooperative regime. */
 int phc_newton_step_batch(const phc_system* s, int64_t n_points, const double* x, double* x_new, double* residual,
                           int32_t* status, void* stream);
 
@@ -215,7 +220,9 @@ typedef struct phc_track_params {
  * points), correct with Newton on h(., t_try) (phc_newton_step_homotopy_batch), accept when
  * the residual reaches tol within max_newton iterations (history updated only on success),
  * otherwise step back; step-size control as in phc_track_params.  All active paths advance
- * together (one batched corrector call per Newton iteration over the active paths only).
+ * together (one batched corrector call per Newton iteration); the step-size control runs on
+ * the device and the host re-compacts the active paths every 8 steps (paths that stopped in
+ * between are frozen, so the decisions are those of a check after every step).
  *   x          [n_paths][n_var][2][limbs] DEVICE pointer: start solutions in, end points out
  *              (the last accepted point of every path, refined by end_newton iterations for
  *              the paths that reached t = 1)
