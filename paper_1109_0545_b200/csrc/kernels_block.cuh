@@ -608,6 +608,65 @@ inline bool colour_block(const std::vector<std::vector<std::pair<int, int>>>& te
   return true;
 }
 
+// Lane placement for layout 2 with few slots: reorder the terms of every block over its lanes
+// (lane l has class l % kClasses) so that each (class, var) occurs in at most Kc terms.
+// Greedy, heaviest terms first, each to the class with free lanes that keeps its largest
+// (class, var) count lowest (ties: most free lanes, then lowest class).  False when some
+// block cannot be balanced.
+template <class S>
+bool balance_lane_classes(const S& s, const std::vector<std::vector<int64_t>>& bterms, int Kc,
+                          std::vector<std::vector<int64_t>>* out) {
+  std::vector<uint8_t> deg((size_t)kClasses * s.n_var, 0);
+  out->assign(bterms.size(), {});
+  for (size_t b = 0; b < bterms.size(); ++b) {
+    const std::vector<int64_t>& ts = bterms[b];
+    const int m = (int)ts.size();
+    int cap[kClasses];
+    for (int c = 0; c < kClasses; ++c) cap[c] = 0;
+    for (int l = 0; l < m; ++l) cap[l % kClasses]++;
+    std::vector<int> order(m);
+    for (int j = 0; j < m; ++j) order[j] = j;
+    std::stable_sort(order.begin(), order.end(), [&](int x, int y) {
+      return s.term_ptr[ts[x] + 1] - s.term_ptr[ts[x]] > s.term_ptr[ts[y] + 1] - s.term_ptr[ts[y]];
+    });
+    std::vector<std::vector<int64_t>> by_class(kClasses);
+    bool ok = true;
+    for (int j : order) {
+      const int64_t t = ts[j];
+      int best = -1, best_cost = 1 << 30;
+      for (int c = 0; c < kClasses; ++c) {
+        if (!cap[c]) continue;
+        int cost = 0;
+        for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q)
+          cost = std::max(cost, deg[(size_t)c * s.n_var + (s.fac[q] & 0xffffu)] + 1);
+        if (cost < best_cost || (cost == best_cost && cap[c] > cap[best])) {
+          best = c;
+          best_cost = cost;
+        }
+      }
+      if (best < 0 || best_cost > Kc) {
+        ok = false;
+        break;
+      }
+      cap[best]--;
+      by_class[best].push_back(t);
+      for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q) deg[(size_t)best * s.n_var + (s.fac[q] & 0xffffu)]++;
+    }
+    for (int c = 0; c < kClasses; ++c)  // reset the counts this block touched
+      for (int64_t t : by_class[c])
+        for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q) deg[(size_t)c * s.n_var + (s.fac[q] & 0xffffu)] = 0;
+    if (!ok) return false;
+    std::vector<int64_t>& lanes = (*out)[b];
+    lanes.resize(m);
+    int taken[kClasses] = {0};
+    for (int l = 0; l < m; ++l) {
+      const int c = l % kClasses;
+      lanes[l] = by_class[c][taken[c]++];
+    }
+  }
+  return true;
+}
+
 template <class S>
 void plan_blocks(const S& s, HostBlockPlan* plan) {
   plan->usable = false;
@@ -619,7 +678,7 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
   const int nw2 = block_warps(L, 2);
   const size_t l2_bytes = pt1 * kClasses + (size_t)nw2 * kClasses * s.n_var * cdb + nw2 * cdb;
   const int layout = (L == 2 && l2_bytes <= (size_t)200 * 1024) ? 2 : 1;
-  const int K = compiled_K(std::max(s.kmax, layout == 2 ? 4 : 1));
+  int K = compiled_K(std::max(s.kmax, layout == 2 ? 4 : 1));
   if (K == 0 || s.n_var >= (int)kDummyVar) return;
   // blocks
   std::vector<int32_t> blk(1, 0);
@@ -636,6 +695,18 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
     max_blocks_per_poly = std::max(max_blocks_per_poly, nb);
   }
   const int64_t nb = (int64_t)bterms.size();
+  // Layout 2 colours (lane, (class, var)) edges: an accumulator (class, var) is shared by the
+  // 4 lanes of a class, so K >= 4 in general.  Systems with k <= 2 (quadratic systems, the
+  // tracker's total-degree homotopies) can often do with K = 2 slots -- half the padded
+  // products -- when the terms of each block are placed on lanes so that no (class, var)
+  // is used by more than 2 of them (then a 2-edge-colouring exists, Koenig).  Greedy
+  // placement; any block that does not balance keeps the plain order and K = 4.
+  std::vector<std::vector<int64_t>> bterms2;
+  const bool balanced = layout == 2 && s.kmax <= 2 && balance_lane_classes(s, bterms, 2, &bterms2);
+  if (balanced) {
+    bterms.swap(bterms2);
+    K = 2;
+  }
   // replicas needed: max over blocks and variables of ceil(d_v / K)
   int R = 1;
   for (auto& ts : bterms) {
@@ -646,39 +717,52 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
     for (int v = 0; v < s.n_var; ++v) R = std::max(R, (d[v] + K - 1) / K);
   }
   if (R > 255) return;
-  std::vector<uint32_t> fac((size_t)nb * K * kWarp);
-  std::vector<double> coef((size_t)nb * kWarp * 2 * L, 0.0);
-  std::vector<int64_t> slot_term((size_t)nb * kWarp, -1);
-  for (int64_t b = 0; b < nb; ++b) {
-    std::vector<std::vector<std::pair<int, int>>> terms;
-    for (int64_t t : bterms[b]) {
-      std::vector<std::pair<int, int>> f;
-      for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q)
-        f.push_back({(int)(s.fac[q] & 0xffffu), (int)((s.fac[q] >> 16) & 0xffu)});
-      terms.push_back(f);
-    }
-    std::vector<std::vector<int>> slot, rep;
-    if (layout == 2) {
-      // right nodes are (class, var): lanes of different classes never share an accumulator
-      auto cterms = terms;
-      for (size_t l = 0; l < cterms.size(); ++l)
-        for (auto& f : cterms[l]) f.first += s.n_var * (int)(l % kClasses);
-      if (!colour_block(cterms, s.n_var * kClasses, K, 1, &slot, &rep)) return;
-    } else if (!colour_block(terms, s.n_var, K, R, &slot, &rep)) {
-      return;
-    }
-    for (int l = 0; l < kWarp; ++l) {
-      for (int q = 0; q < K; ++q) fac[((size_t)b * K + q) * kWarp + l] = kDummyVar | (1u << 16);
-      if (l >= (int)terms.size()) continue;
-      for (size_t j = 0; j < terms[l].size(); ++j) {
-        const int q = slot[l][j];
-        fac[((size_t)b * K + q) * kWarp + l] =
-            (uint32_t)terms[l][j].first | ((uint32_t)terms[l][j].second << 16) | ((uint32_t)rep[l][j] << 24);
+  std::vector<uint32_t> fac;
+  std::vector<double> coef;
+  std::vector<int64_t> slot_term;
+  // slot assignment by edge colouring and packing; false when a block does not colour
+  auto pack = [&]() -> bool {
+    fac.assign((size_t)nb * K * kWarp, 0u);
+    coef.assign((size_t)nb * kWarp * 2 * L, 0.0);
+    slot_term.assign((size_t)nb * kWarp, -1);
+    for (int64_t b = 0; b < nb; ++b) {
+      std::vector<std::vector<std::pair<int, int>>> terms;
+      for (int64_t t : bterms[b]) {
+        std::vector<std::pair<int, int>> f;
+        for (int64_t q = s.term_ptr[t]; q < s.term_ptr[t + 1]; ++q)
+          f.push_back({(int)(s.fac[q] & 0xffffu), (int)((s.fac[q] >> 16) & 0xffu)});
+        terms.push_back(f);
       }
-      const int64_t t = bterms[b][l];
-      slot_term[(size_t)b * kWarp + l] = t;
-      for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
+      std::vector<std::vector<int>> slot, rep;
+      if (layout == 2) {
+        // right nodes are (class, var): lanes of different classes never share an accumulator
+        auto cterms = terms;
+        for (size_t l = 0; l < cterms.size(); ++l)
+          for (auto& f : cterms[l]) f.first += s.n_var * (int)(l % kClasses);
+        if (!colour_block(cterms, s.n_var * kClasses, K, 1, &slot, &rep)) return false;
+      } else if (!colour_block(terms, s.n_var, K, R, &slot, &rep)) {
+        return false;
+      }
+      for (int l = 0; l < kWarp; ++l) {
+        for (int q = 0; q < K; ++q) fac[((size_t)b * K + q) * kWarp + l] = kDummyVar | (1u << 16);
+        if (l >= (int)terms.size()) continue;
+        for (size_t j = 0; j < terms[l].size(); ++j) {
+          const int q = slot[l][j];
+          fac[((size_t)b * K + q) * kWarp + l] =
+              (uint32_t)terms[l][j].first | ((uint32_t)terms[l][j].second << 16) | ((uint32_t)rep[l][j] << 24);
+        }
+        const int64_t t = bterms[b][l];
+        slot_term[(size_t)b * kWarp + l] = t;
+        for (int c = 0; c < 2 * L; ++c) coef[((size_t)b * kWarp + l) * 2 * L + c] = s.coeff[(size_t)t * 2 * L + c];
+      }
     }
+    return true;
+  };
+  if (!pack()) {
+    if (!balanced) return;
+    bterms.swap(bterms2);  // the balanced placement did not colour with 2 slots: plain order, K = 4
+    K = compiled_K(4);
+    if (!pack()) return;
   }
   // mode A (a warp owns whole polynomials, the CTA's power table serves up to 4 nw of them)
   // or mode B (a CTA owns a polynomial, its warps split the blocks, one warp per block up to
