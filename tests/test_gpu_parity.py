@@ -360,3 +360,43 @@ def test_remote_shard_branches_on_one_gpu(phc, mode, monkeypatch):
     torch.cuda.synchronize()
     assert torch.equal(F1, F2) and torch.equal(J1, J2)
     assert torch.equal(H1, H2) and torch.equal(K1, K2)
+
+
+def _quadratic_system(n, terms_per_poly, seed, hub=False):
+    """k <= 2 DD system: every polynomial has `terms_per_poly` random monomials of degree <= 2
+    (hub: every term of polynomial i contains x_0, so a block cannot spread (class, x_0) over
+    2 lanes per class and the planner must keep K = 4)."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    polys = []
+    for _ in range(n):
+        terms = []
+        for _t in range(terms_per_poly):
+            if hub:
+                b = int(rng.integers(1, n))
+                terms.append([(0, 1), (b, int(rng.integers(1, 3)))])
+            else:
+                k = int(rng.integers(0, 3))
+                vs = sorted(rng.choice(n, size=k, replace=False).tolist())
+                terms.append([(v, int(rng.integers(1, 3))) for v in vs])
+        polys.append(terms)
+    T = n * terms_per_poly
+    vals = np.exp(2j * np.pi * rng.random(T)) * rng.uniform(0.5, 2.0, T)
+    s = system_from_terms(n, n, 2, polys, limbs_from_values(vals, 2))
+    X = np.stack([limbs_from_values(np.exp(2j * np.pi * rng.random(n)), 2) for _ in range(3)])
+    return s, X
+
+
+@pytest.mark.parametrize("hub,K", [(False, 2), (True, 4)])
+def test_low_degree_lane_placement(phc, hub, K):
+    """k <= 2 systems: the planner places each block's terms on lanes so that no (class, var)
+    accumulator is shared by more than two lanes and colours with K = 2 slots; a system whose
+    blocks cannot be balanced (one variable in every term) keeps K = 4.  Both match the exact
+    oracle (3 points, batch kernel), structural zeros exact."""
+    s, X = _quadratic_system(12, 70, seed=5 if not hub else 6, hub=hub)
+    F, J, h = gpu_eval(phc, s, X, devices=[0])
+    st = h.stats
+    assert st["layout"] == 2 and st["K"] == K, st
+    for p in range(X.shape[0]):
+        ar, Fo, Jo = oracle_point(s, X[p], arith="exact")
+        ef, ej = compare_point(ar, Fo, Jo, F[p], J[p], 2)
+        assert ef <= TOL[2] and ej <= TOL[2], (p, ef, ej)
