@@ -43,7 +43,9 @@ PHC_DEV double sub_(double a, double b) { return __dadd_rn(a, -b); }
 PHC_DEV double mul_(double a, double b) { return __dmul_rn(a, b); }
 PHC_DEV double fma_(double a, double b, double c) { return __fma_rn(a, b, c); }
 
-// s + e == a + b exactly (6 DADD).
+// s + e == a + b exactly (6 DADD).  (Ordering the operands by magnitude for a 3-DADD fast
+// two-sum -- DSETP on |a|, |b| plus selects -- measured slower: batch DD -4%, large QD -5 to
+// -10%; profiles/README.md.)
 PHC_DEV void two_sum(double a, double b, double& s, double& e) {
   s = add_(a, b);
   double bb = sub_(s, a);
