@@ -570,6 +570,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
       }
       return;
     }
+    PHC_CHECK(bi >= c && bi < n);
     const int ph = perm[bi];  // physical pivot row (all lanes read before lane 0 swaps)
     __syncwarp();
     const C inv = recip_warp<L>(cval(colv, ph), lane);
@@ -685,7 +686,10 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
         if (tid == 0) s_bad = __ldcg(flag_g);
         __syncthreads();
         if (s_bad) break;  // grid-uniform: written before the last barrier
-        for (int i = tid; i < n; i += T) perm[i] = __ldcg(perm_g + (size_t)(k & 1) * n + i);
+        for (int i = tid; i < n; i += T) {
+          perm[i] = __ldcg(perm_g + (size_t)(k & 1) * n + i);
+          PHC_CHECK(perm[i] >= 0 && perm[i] < n);
+        }
         __syncthreads();
         // trailing update of step k: rows i > k, columns j >= k + 2 (CTA 0 takes k+1)
         const int rows = n - k - 1, ucols = cols - k - 2;

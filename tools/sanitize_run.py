@@ -1,7 +1,8 @@
 """One small call of every kernel family, for compute-sanitizer:
 block kernel (layouts 0/1/2, plain and homotopy), latency path (warp scan, split reduction),
-generic path (k > 32), common-support path (both regimes), Newton (warp, CTA, multi-kernel),
-predictor, tracker, arithmetic self-test, sharded calls (repeated devices)."""
+generic path (k > 32), common-support path (both regimes), Newton (warp, CTA, cooperative,
+multi-kernel), predictor, tracker (K = 2 lane placement, device-side control), arithmetic
+self-test incl. the warp reciprocal, sharded calls (repeated devices)."""
 import os
 import sys
 
@@ -47,7 +48,9 @@ phc.System(s).newton_step(cuda(X))
 s, X = config_system("c3", seed=1, points=2)
 phc.System(s).newton_step(cuda(X))
 s, X = random_system(52, 4, 3, 2, 4, seed=4, points=2)
-phc.System(s).newton_step(cuda(X))
+phc.System(s).newton_step(cuda(X))            # cooperative (<= 4 points)
+s, X = random_system(52, 4, 3, 2, 4, seed=4, points=6)
+phc.System(s).newton_step(cuda(X))            # multi-kernel (> 4 points)
 # tracker + predictor
 s, cf, X0 = total_degree_homotopy(2, 2, seed=5)
 phc.System(s, coeff_target=cf).track(cuda(X0), max_steps=40)
@@ -56,5 +59,6 @@ from paper_1109_0545_b200.system import _ptr  # noqa: E402
 a = cuda(np.ones((64, 2, 4)))
 o = torch.empty_like(a)
 phc.phc_arith_test(5, 4, 64, _ptr(a), _ptr(a), _ptr(o), None)
+phc.phc_arith_test(10, 4, 64, _ptr(a), _ptr(a), _ptr(o), None)
 torch.cuda.synchronize()
 print("sanitize run ok")
