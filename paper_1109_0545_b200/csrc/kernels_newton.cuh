@@ -53,6 +53,20 @@ struct NewtonArgs {
   int64_t n_points;
 };
 
+// Shared memory of newton_solve_kernel: [J | -F], the pivot reciprocals, two row permutations.
+__host__ __device__ inline size_t solve_smem_bytes(int n, int L) {
+  return ((size_t)n * (n + 1) + n) * 2 * L * sizeof(double) + (size_t)2 * n * sizeof(int);
+}
+
+// One CTA per point, [J | -F] in shared memory, one block barrier per column.  Rows are
+// addressed through a permutation (row exchanges swap two entries, rows are not moved), kept
+// twice: warps 1.. run the trailing update of step k through `cur` while warp 0 -- the
+// look-ahead -- updates column k+1, finds its pivot, writes the exchanged permutation to
+// `nxt`, forms the pivot reciprocal (recip_warp) and the multipliers of column k+1; then one
+// __syncthreads and the buffers swap roles.  The look-ahead chain is the critical path of a
+// column, so the update runs on the warps that do not share warp 0's scheduler (warp w issues
+// on SMSP w % 4).  Same pivot choices and per-entry operations, in the same order, as the
+// other eliminations (bitwise equal steps, tested).
 template <int L>
 __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   using P = Prec<L>;
@@ -60,32 +74,30 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   extern __shared__ __align__(16) double nsm[];
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  __shared__ int s_piv, s_bad;
-  __shared__ __align__(16) double s_inv[2 * L];   // reciprocal of the current pivot
-  __shared__ __align__(16) double s_inv2[2 * L];  // ... of the next column's (look-ahead)
+  __shared__ int s_bad;
   const int64_t p = blockIdx.x;
   if (p >= a.n_points) return;
   const int n = a.n, cols = n + 1, cd = 2 * L;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
   double* M = nsm;
   double* invd = M + (size_t)n * cols * cd;  // n pivot reciprocals after the matrix
-  auto at = [&](int i, int j) { return M + ((size_t)i * cols + j) * cd; };
-  auto ldm = [&](int i, int j) { return sload<L>(at(i, j)); };  // generic: shared or global
-  auto stm = [&](int i, int j, const C& v) { sstore<L>(at(i, j), v); };
+  int* pbuf = reinterpret_cast<int*>(invd + (size_t)n * cd);  // [2][n] row permutations
+  auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
-  // load [J | -F]; residual max_i |F_i|
+  // load [J | -F]; residual max_i |F_i|; identity permutation
   double rmax = 0.0;
   for (int e = tid; e < n * cols; e += T) {
     const int i = e / cols, j = e % cols;
     if (j < n) {
-      stm(i, j, cload<L>(Jp + ((size_t)i * n + j) * cd));
+      sstore<L>(at(i, j), cload<L>(Jp + ((size_t)i * n + j) * cd));
     } else {
       const C f = cload<L>(Fp + (size_t)i * cd);
       rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
-      stm(i, j, P::neg(f));
+      sstore<L>(at(i, j), P::neg(f));
     }
   }
+  for (int i = tid; i < n; i += T) pbuf[i] = i;
   for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
   if (lane == 0) red_v[wid] = rmax;
   if (tid == 0) s_bad = 0;
@@ -95,17 +107,13 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
     a.resid[p] = r;
   }
-  __syncthreads();
-  // Elimination with partial pivoting and a one-column look-ahead: while warps 1.. update
-  // the trailing columns k+2.. of step k, warp 0 updates column k+1, finds its pivot and
-  // forms the pivot reciprocal, so the serial reciprocal overlaps the update (three block
-  // barriers per column instead of six).  Same operations per entry as before.
-  // column 0: pivot (block-wide), swap, reciprocal
-  {
+  // warp 0: pivot of column c among logical rows c.. of `src`, exchanged permutation to `dst`,
+  // reciprocal, multipliers of column c (rows > c).  False when the column is zero.
+  auto pivot_column = [&](const int* src, int* dst, int c) -> bool {
     double best = -1.0;
     int bi = n;
-    for (int i = tid; i < n; i += T) {
-      const double v = P::abs2_hi(ldm(i, 0));
+    for (int i = c + lane; i < n; i += 32) {
+      const double v = P::abs2_hi(sload<L>(at(src[i], c)));
       if (v > best) { best = v; bi = i; }
     }
     for (int o = 16; o; o >>= 1) {
@@ -113,98 +121,49 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
       if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
     }
-    if (lane == 0) { red_v[wid] = best; red_i[wid] = bi; }
-    __syncthreads();
-    if (tid == 0) {
-      double b = -1.0;
-      int ix = n;
-      for (int w = 0; w < nwarp; ++w)
-        if (red_v[w] > b || (red_v[w] == b && red_i[w] < ix)) { b = red_v[w]; ix = red_i[w]; }
-      s_piv = ix;
-      if (!(b > 0.0)) s_bad = 1;
+    if (!(best > 0.0)) return false;
+    for (int i = lane; i < n; i += 32) dst[i] = (i == c) ? src[bi] : (i == bi ? src[c] : src[i]);
+    __syncwarp();
+    const C inv = recip_warp<L>(sload<L>(at(dst[c], c)), lane);
+    if (lane == 0) sstore<L>(invd + (size_t)c * cd, inv);
+    for (int i = c + 1 + lane; i < n; i += 32) {
+      double* m = at(dst[i], c);
+      sstore<L>(m, P::mul(sload<L>(m), inv));
     }
-    __syncthreads();
-    if (!s_bad) {
-      const int pv = s_piv;
-      if (pv != 0)
-        for (int j = tid; j < cols; j += T) {
-          const C u = ldm(0, j), v = ldm(pv, j);
-          stm(0, j, v);
-          stm(pv, j, u);
-        }
-      __syncthreads();
-      if (wid == 0) {
-        const C inv = recip_warp<L>(ldm(0, 0), lane);
-        if (lane == 0) {
-          sstore<L>(s_inv, inv);
-          sstore<L>(invd, inv);
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int k = 0; k < n && !s_bad; ++k) {
-    const C inv = sload<L>(s_inv);
-    // multipliers l_i = M[i][k] / M[k][k], stored in column k
-    for (int i = k + 1 + tid; i < n; i += T) stm(i, k, P::mul(ldm(i, k), inv));
-    __syncthreads();  // (1)
-    if (k == n - 1) break;
+    return true;
+  };
+  int cur = 0;  // pbuf + cur * n: the permutation after the exchanges of columns < k + 1
+  if (wid == 0 && !pivot_column(pbuf, pbuf + n, 0) && lane == 0) s_bad = 1;
+  __syncthreads();
+  cur = 1;
+  for (int k = 0; k < n - 1 && !s_bad; ++k) {
+    const int* pc = pbuf + cur * n;
+    int* pn = pbuf + (cur ^ 1) * n;
     if (wid == 0) {
-      // look-ahead: column k+1, its pivot among rows k+1.., the pivot reciprocal
-      for (int i = k + 1 + lane; i < n; i += 32)
-        stm(i, k + 1, P::sub(ldm(i, k + 1), P::mul(ldm(i, k), ldm(k, k + 1))));
-      __syncwarp();
-      double best = -1.0;
-      int bi = n;
+      // look-ahead: column k+1 of the rows below k, then its pivot, exchange, multipliers
+      const double* pk = at(pc[k], k + 1);
       for (int i = k + 1 + lane; i < n; i += 32) {
-        const double v = P::abs2_hi(ldm(i, k + 1));
-        if (v > best) { best = v; bi = i; }
+        double* m = at(pc[i], k + 1);
+        sstore<L>(m, P::sub(sload<L>(m), P::mul(sload<L>(at(pc[i], k)), sload<L>(pk))));
       }
-      for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-        if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-      }
-      if (!(best > 0.0)) {
-        if (lane == 0) s_bad = 1;
-      } else {
-        const C inv2 = recip_warp<L>(ldm(bi, k + 1), lane);  // best, bi are warp-uniform
-        if (lane == 0) {
-          s_piv = bi;
-          sstore<L>(s_inv2, inv2);
-        }
-      }
-    } else {
-      // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1, by the warps that do not
-      // share warp 0's scheduler (warp w issues on SMSP w % 4): the look-ahead chain above is
-      // the critical path of the column and runs alone on its SMSP
-      if ((wid & 3) == 0 && nwarp > 4) goto skip_update;
+      __syncwarp();
+      if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad = 1;
+    } else if ((wid & 3) != 0 || nwarp <= 4) {
+      // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1, off warp 0's SMSP
       const int worker = (nwarp > 4) ? (wid >> 2) * 3 + (wid & 3) - 1 : wid - 1;
       const int nworker = (nwarp > 4) ? (nwarp >> 2) * 3 : nwarp - 1;
       const int rows = n - k - 1, ucols = cols - k - 2;
+      const double* prow = at(pc[k], 0);
       for (int e = worker * 32 + lane; e < rows * ucols; e += nworker * 32) {
         const int i = k + 1 + e / ucols, j = k + 2 + e % ucols;
-        stm(i, j, P::sub(ldm(i, j), P::mul(ldm(i, k), ldm(k, j))));
+        double* rw = at(pc[i], 0);
+        sstore<L>(rw + (size_t)j * cd,
+                  P::sub(sload<L>(rw + (size_t)j * cd), P::mul(sload<L>(rw + (size_t)k * cd), sload<L>(prow + (size_t)j * cd))));
       }
     }
-  skip_update:
-    __syncthreads();  // (2)
-    if (s_bad) break;
-    const int pv = s_piv;
-    if (pv != k + 1)
-      for (int j = k + 1 + tid; j < cols; j += T) {
-        const C u = ldm(k + 1, j), v = ldm(pv, j);
-        stm(k + 1, j, v);
-        stm(pv, j, u);
-      }
-    if (tid == 0) {
-      const C inv2 = sload<L>(s_inv2);
-      sstore<L>(s_inv, inv2);
-      sstore<L>(invd + (size_t)(k + 1) * cd, inv2);
-    }
-    __syncthreads();  // (3)
+    __syncthreads();
+    cur ^= 1;
   }
-  __syncthreads();
   if (s_bad) {
     if (tid == 0) a.status[p] = 1;
     for (int e = tid; e < n; e += T)
@@ -212,20 +171,19 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     return;
   }
   // back substitution: x_i = M[i][n] / M[i][i], then M[r][n] -= M[r][i] x_i for r < i
+  const int* pf = pbuf + cur * n;
   for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) {
-      const C inv = sload<L>(invd + (size_t)i * cd);
-      stm(i, n, P::mul(ldm(i, n), inv));
-    }
+    if (tid == 0) sstore<L>(at(pf[i], n), P::mul(sload<L>(at(pf[i], n)), sload<L>(invd + (size_t)i * cd)));
     __syncthreads();
-    const C xi = ldm(i, n);
-    for (int r = tid; r < i; r += T) stm(r, n, P::sub(ldm(r, n), P::mul(ldm(r, i), xi)));
+    const C xi = sload<L>(at(pf[i], n));
+    for (int r = tid; r < i; r += T)
+      sstore<L>(at(pf[r], n), P::sub(sload<L>(at(pf[r], n)), P::mul(sload<L>(at(pf[r], i)), xi)));
     __syncthreads();
   }
   // z := z + dz
   for (int e = tid; e < n; e += T) {
     const double* xp = a.X + ((size_t)p * n + e) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), ldm(e, n)));
+    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), sload<L>(at(pf[e], n))));
   }
   if (tid == 0) a.status[p] = 0;
 }

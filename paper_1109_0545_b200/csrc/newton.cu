@@ -78,7 +78,8 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
   const int n = s->n_eq, L = s->L;
   const int64_t cd = 2 * L;
   const size_t mat = ((size_t)n * (n + 1) + n) * cd * sizeof(double);  // [J | -F] + pivot reciprocals
-  const bool smem = mat <= (size_t)200 * 1024 && !getenv("PHC_NEWTON_GLOBAL");  // (test hook: global-memory paths)
+  const size_t smat = phc::solve_smem_bytes(n, L);                                     // + permutations
+  const bool smem = smat <= (size_t)200 * 1024 && !getenv("PHC_NEWTON_GLOBAL");  // (test hook: global-memory paths)
   const int64_t per_point = (int64_t)n * n * cd * 8 + (smem ? 0 : (int64_t)mat);
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_points, ((int64_t)512 << 20) / per_point));
   if (d->n_cap < chunk) {
@@ -142,8 +143,8 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
     const bool coop = coop_ok && (coop_env >= 0 ? coop_env == 1 : np <= kCoopMaxPoints);
     if (L == 2) {
       if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2>, mat));
-        phc::newton_solve_kernel<2><<<(unsigned)np, threads, mat, st>>>(a);
+        if (smat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<2>, smat));
+        phc::newton_solve_kernel<2><<<(unsigned)np, threads, smat, st>>>(a);
       } else if (coop) {
         if ((rc = newton_coop<2>(a, d, st))) return rc;
       } else {
@@ -151,8 +152,8 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
       }
     } else {
       if (smem) {
-        if (mat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4>, mat));
-        phc::newton_solve_kernel<4><<<(unsigned)np, threads, mat, st>>>(a);
+        if (smat > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_solve_kernel<4>, smat));
+        phc::newton_solve_kernel<4><<<(unsigned)np, threads, smat, st>>>(a);
       } else if (coop) {
         if ((rc = newton_coop<4>(a, d, st))) return rc;
       } else {
