@@ -6,6 +6,21 @@
 
 using namespace phc_rt;
 
+namespace {
+// the tracker's private stream, its ordering event and the window graph
+struct TrackStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t e = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  ~TrackStream() {
+    if (s) cudaStreamSynchronize(s);
+    if (ex) cudaGraphExecDestroy(ex);
+    if (e) cudaEventDestroy(e);
+    if (s) cudaStreamDestroy(s);
+  }
+};
+}  // namespace
+
 extern "C" {
 
 int phc_predict_batch(int32_t limbs, int32_t n_var, int64_t n_paths, int32_t order, const int32_t* n_hist,
@@ -45,7 +60,17 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
       q.end_newton < 0 || q.predictor < 0 || q.predictor > 2)
     return fail(PHC_EINVAL, "invalid tracker parameters");
   DeviceGuard g(s->home);
-  cudaStream_t st = (cudaStream_t)stream;
+  // the tracker runs on a private stream ordered after the caller's (`stream` may be the
+  // legacy default stream, which cannot be captured into a graph); it is synchronous
+  TrackStream ts_guard;
+  {
+    cudaStream_t user = (cudaStream_t)stream;
+    CUDA_TRY(cudaStreamCreateWithFlags(&ts_guard.s, cudaStreamNonBlocking));
+    CUDA_TRY(cudaEventCreateWithFlags(&ts_guard.e, cudaEventDisableTiming));
+    CUDA_TRY(cudaEventRecord(ts_guard.e, user));
+    CUDA_TRY(cudaStreamWaitEvent(ts_guard.s, ts_guard.e, 0));
+  }
+  cudaStream_t st = ts_guard.s;
   const int n = s->n_var, L = s->L;
   const int64_t cd = 2 * L, P = n_paths;
   int rc;
@@ -91,12 +116,8 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
   const phc::TrackCtl ctl{q.step_min, q.step_max, q.expand, q.contract, q.tol, q.max_newton, q.max_steps};
   const char* wenv = getenv("PHC_TRACK_WINDOW");
   const int window = wenv ? std::max(1, atoi(wenv)) : 8;
-  while (true) {
-    int64_t A = 0;
-    for (int64_t p = 0; p < P; ++p)
-      if (stat[p] == 0) idx[A++] = (int32_t)p;
-    if (A == 0) break;
-    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
+  // W tracker steps over the A active paths of idx_d
+  auto enqueue_window = [&](int64_t A) -> int {
     for (int w = 0; w < window; ++w) {
       // predict: t_try = min(t + lambda, 1), z_guess by the secant / quadratic predictor (§5)
       if (L == 2)
@@ -125,6 +146,60 @@ int phc_track_paths(const phc_system* cs, int64_t n_paths, double* x, const phc_
         phc::accept_kernel<4><<<grid(A * n), 128, 0, st>>>(n, A, idx_d.p, acc_d.p, tc.p, xc.p, n_hist.p, t_hist.p,
                                                             x_hist.p);
       CUDA_TRY(cudaGetLastError());
+    }
+    return PHC_OK;
+  };
+  // After a first window of plain launches (it also sizes every workspace), a window is one
+  // CUDA graph launch: captured once per active-path count A (cudaGraphExecUpdate when the
+  // topology allows), so a window of ~11 W kernels costs one launch on the host.  The
+  // few-path tracker is launch-bound without it.  PHC_TRACK_GRAPH=0 disables the graphs.
+  bool use_graph = !(getenv("PHC_TRACK_GRAPH") && atoi(getenv("PHC_TRACK_GRAPH")) == 0);
+  bool warmed = false;
+  int64_t graph_A = -1;
+  while (true) {
+    int64_t A = 0;
+    for (int64_t p = 0; p < P; ++p)
+      if (stat[p] == 0) idx[A++] = (int32_t)p;
+    if (A == 0) break;
+    CUDA_TRY(cudaMemcpyAsync(idx_d.p, idx.p, A * 4, cudaMemcpyHostToDevice, st));
+    if (use_graph && warmed && A != graph_A) {
+      cudaGraph_t gr = nullptr;
+      CUDA_TRY(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+      const int rc_cap = enqueue_window(A);
+      const cudaError_t ce = cudaStreamEndCapture(st, &gr);
+      if (rc_cap != PHC_OK || ce != cudaSuccess || gr == nullptr) {
+        if (gr) cudaGraphDestroy(gr);
+        cudaGetLastError();
+        g_err.clear();
+        use_graph = false;  // not capturable here: plain launches from now on
+      } else {
+        bool ok = false;
+        if (ts_guard.ex) {
+          cudaGraphExecUpdateResultInfo info;
+          ok = cudaGraphExecUpdate(ts_guard.ex, gr, &info) == cudaSuccess;
+          if (!ok) {
+            cudaGetLastError();
+            cudaGraphExecDestroy(ts_guard.ex);
+            ts_guard.ex = nullptr;
+          }
+        }
+        if (!ok) {
+          const cudaError_t ie = cudaGraphInstantiate(&ts_guard.ex, gr, 0);
+          if (ie != cudaSuccess) {
+            cudaGetLastError();
+            ts_guard.ex = nullptr;
+            use_graph = false;
+          }
+        }
+        cudaGraphDestroy(gr);
+        graph_A = use_graph ? A : -1;
+      }
+    }
+    if (use_graph && warmed && graph_A == A) {
+      CUDA_TRY(cudaGraphLaunch(ts_guard.ex, st));
+    } else {
+      if ((rc = enqueue_window(A))) return rc;
+      warmed = true;
     }
     CUDA_TRY(cudaMemcpyAsync(stat.p, stat_d.p, P * 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(cudaStreamSynchronize(st));

@@ -154,3 +154,19 @@ def test_track_max_steps_inside_window(phc, monkeypatch):
     monkeypatch.setenv("PHC_TRACK_WINDOW", "16")
     _, status, stats = h.track(_cuda(X0), max_steps=5)
     assert (status == 2).all() and (stats[:, 1] == 5).all(), (status, stats[:, 1])
+
+
+def test_track_graph_equals_plain_launches(phc, monkeypatch):
+    """Windows replayed as CUDA graphs (re-captured or updated whenever the number of active
+    paths changes) give bitwise the results of plain launches (PHC_TRACK_GRAPH=0)."""
+    s, cf, X0 = total_degree_homotopy(4, 2, seed=11)
+    h = phc.System(s, coeff_target=cf)
+    out = {}
+    for g in ("0", "1"):
+        monkeypatch.setenv("PHC_TRACK_GRAPH", g)
+        Xe, status, stats, te = h.track(_cuda(X0), t_end=True)
+        out[g] = (Xe.cpu().numpy(), status, stats, te.cpu().numpy())
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
+    assert (out["1"][1] == 1).all()
+    assert len(set(out["1"][2][:, 1].tolist())) > 1  # paths stop at different steps: A changes
