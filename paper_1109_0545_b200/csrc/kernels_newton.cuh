@@ -79,10 +79,36 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   if (p >= a.n_points) return;
   const int n = a.n, cols = n + 1, cd = 2 * L;
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
-  double* M = nsm;
-  double* invd = M + (size_t)n * cols * cd;  // n pivot reciprocals after the matrix
+  // [J | -F] as two planes, real parts then imaginary parts ([n][n+1][L] each): the lanes of
+  // a warp read consecutive entries of a row, 16-byte DD parts at a 16-byte stride, so a
+  // quarter-warp's LDS.128 is one conflict-free wavefront (the interleaved [re][im] layout
+  // put two lanes on each bank: 46% of the wavefronts were conflicts)
+  double* Mre = nsm;
+  double* Mim = Mre + (size_t)n * cols * L;
+  double* invd = Mim + (size_t)n * cols * L;  // n pivot reciprocals after the matrix
   int* pbuf = reinterpret_cast<int*>(invd + (size_t)n * cd);  // [2][n] row permutations
-  auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
+  auto ldE = [&](int r, int c) -> C {
+    C v;
+    const size_t o = ((size_t)r * cols + c) * L;
+#pragma unroll
+    for (int q = 0; q < L; q += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(Mre + o + q);
+      const double2 y = *reinterpret_cast<const double2*>(Mim + o + q);
+      v.re.x[q] = x.x;
+      v.re.x[q + 1] = x.y;
+      v.im.x[q] = y.x;
+      v.im.x[q + 1] = y.y;
+    }
+    return v;
+  };
+  auto stE = [&](int r, int c, const C& v) {
+    const size_t o = ((size_t)r * cols + c) * L;
+#pragma unroll
+    for (int q = 0; q < L; q += 2) {
+      *reinterpret_cast<double2*>(Mre + o + q) = make_double2(v.re.x[q], v.re.x[q + 1]);
+      *reinterpret_cast<double2*>(Mim + o + q) = make_double2(v.im.x[q], v.im.x[q + 1]);
+    }
+  };
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
   // load [J | -F]; residual max_i |F_i|; identity permutation
@@ -90,11 +116,11 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   for (int e = tid; e < n * cols; e += T) {
     const int i = e / cols, j = e % cols;
     if (j < n) {
-      sstore<L>(at(i, j), cload<L>(Jp + ((size_t)i * n + j) * cd));
+      stE(i, j, cload<L>(Jp + ((size_t)i * n + j) * cd));
     } else {
       const C f = cload<L>(Fp + (size_t)i * cd);
       rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
-      sstore<L>(at(i, j), P::neg(f));
+      stE(i, j, P::neg(f));
     }
   }
   for (int i = tid; i < n; i += T) pbuf[i] = i;
@@ -113,7 +139,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     double best = -1.0;
     int bi = n;
     for (int i = c + lane; i < n; i += 32) {
-      const double v = P::abs2_hi(sload<L>(at(src[i], c)));
+      const double v = P::abs2_hi(ldE(src[i], c));
       if (v > best) { best = v; bi = i; }
     }
     for (int o = 16; o; o >>= 1) {
@@ -124,12 +150,9 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     if (!(best > 0.0)) return false;
     for (int i = lane; i < n; i += 32) dst[i] = (i == c) ? src[bi] : (i == bi ? src[c] : src[i]);
     __syncwarp();
-    const C inv = recip_warp<L>(sload<L>(at(dst[c], c)), lane);
+    const C inv = recip_warp<L>(ldE(dst[c], c), lane);
     if (lane == 0) sstore<L>(invd + (size_t)c * cd, inv);
-    for (int i = c + 1 + lane; i < n; i += 32) {
-      double* m = at(dst[i], c);
-      sstore<L>(m, P::mul(sload<L>(m), inv));
-    }
+    for (int i = c + 1 + lane; i < n; i += 32) stE(dst[i], c, P::mul(ldE(dst[i], c), inv));
     return true;
   };
   int cur = 0;  // pbuf + cur * n: the permutation after the exchanges of columns < k + 1
@@ -141,11 +164,9 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     int* pn = pbuf + (cur ^ 1) * n;
     if (wid == 0) {
       // look-ahead: column k+1 of the rows below k, then its pivot, exchange, multipliers
-      const double* pk = at(pc[k], k + 1);
-      for (int i = k + 1 + lane; i < n; i += 32) {
-        double* m = at(pc[i], k + 1);
-        sstore<L>(m, P::sub(sload<L>(m), P::mul(sload<L>(at(pc[i], k)), sload<L>(pk))));
-      }
+      const C pk = ldE(pc[k], k + 1);
+      for (int i = k + 1 + lane; i < n; i += 32)
+        stE(pc[i], k + 1, P::sub(ldE(pc[i], k + 1), P::mul(ldE(pc[i], k), pk)));
       __syncwarp();
       if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad = 1;
     } else if ((wid & 3) != 0 || nwarp <= 4) {
@@ -153,12 +174,11 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       const int worker = (nwarp > 4) ? (wid >> 2) * 3 + (wid & 3) - 1 : wid - 1;
       const int nworker = (nwarp > 4) ? (nwarp >> 2) * 3 : nwarp - 1;
       const int rows = n - k - 1, ucols = cols - k - 2;
-      const double* prow = at(pc[k], 0);
+      const int pr = pc[k];
       for (int e = worker * 32 + lane; e < rows * ucols; e += nworker * 32) {
         const int i = k + 1 + e / ucols, j = k + 2 + e % ucols;
-        double* rw = at(pc[i], 0);
-        sstore<L>(rw + (size_t)j * cd,
-                  P::sub(sload<L>(rw + (size_t)j * cd), P::mul(sload<L>(rw + (size_t)k * cd), sload<L>(prow + (size_t)j * cd))));
+        const int r = pc[i];
+        stE(r, j, P::sub(ldE(r, j), P::mul(ldE(r, k), ldE(pr, j))));
       }
     }
     __syncthreads();
@@ -173,17 +193,16 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   // back substitution: x_i = M[i][n] / M[i][i], then M[r][n] -= M[r][i] x_i for r < i
   const int* pf = pbuf + cur * n;
   for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) sstore<L>(at(pf[i], n), P::mul(sload<L>(at(pf[i], n)), sload<L>(invd + (size_t)i * cd)));
+    if (tid == 0) stE(pf[i], n, P::mul(ldE(pf[i], n), sload<L>(invd + (size_t)i * cd)));
     __syncthreads();
-    const C xi = sload<L>(at(pf[i], n));
-    for (int r = tid; r < i; r += T)
-      sstore<L>(at(pf[r], n), P::sub(sload<L>(at(pf[r], n)), P::mul(sload<L>(at(pf[r], i)), xi)));
+    const C xi = ldE(pf[i], n);
+    for (int r = tid; r < i; r += T) stE(pf[r], n, P::sub(ldE(pf[r], n), P::mul(ldE(pf[r], i), xi)));
     __syncthreads();
   }
   // z := z + dz
   for (int e = tid; e < n; e += T) {
     const double* xp = a.X + ((size_t)p * n + e) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), sload<L>(at(pf[e], n))));
+    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), ldE(pf[e], n)));
   }
   if (tid == 0) a.status[p] = 0;
 }
