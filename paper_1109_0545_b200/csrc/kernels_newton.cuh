@@ -225,16 +225,40 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t p = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;
   if (p >= a.n_points) return;  // warp-uniform
-  double* M = wsm + (size_t)wib * n * cols * cd;
-  auto at = [&](int i, int j) { return M + ((size_t)i * cols + j) * cd; };
+  // the warp's [J | -F] as real and imaginary planes (as in newton_solve_kernel)
+  double* Mre = wsm + (size_t)wib * n * cols * cd;
+  double* Mim = Mre + (size_t)n * cols * L;
+  auto ldE = [&](int r, int c) -> C {
+    C v;
+    const size_t o = ((size_t)r * cols + c) * L;
+#pragma unroll
+    for (int q = 0; q < L; q += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(Mre + o + q);
+      const double2 y = *reinterpret_cast<const double2*>(Mim + o + q);
+      v.re.x[q] = x.x;
+      v.re.x[q + 1] = x.y;
+      v.im.x[q] = y.x;
+      v.im.x[q + 1] = y.y;
+    }
+    return v;
+  };
+  auto stE = [&](int r, int c, const C& v) {
+    const size_t o = ((size_t)r * cols + c) * L;
+#pragma unroll
+    for (int q = 0; q < L; q += 2) {
+      *reinterpret_cast<double2*>(Mre + o + q) = make_double2(v.re.x[q], v.re.x[q + 1]);
+      *reinterpret_cast<double2*>(Mim + o + q) = make_double2(v.im.x[q], v.im.x[q + 1]);
+    }
+  };
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
+  // coalesced: consecutive lanes read consecutive entries of J
+  for (int e = lane; e < n * n; e += 32) stE(e / n, e % n, cload<L>(Jp + (size_t)e * cd));
   double rmax = 0.0;
   if (lane < n) {
-    for (int j = 0; j < n; ++j) sstore<L>(at(lane, j), cload<L>(Jp + ((size_t)lane * n + j) * cd));
     const C f = cload<L>(Fp + (size_t)lane * cd);
     rmax = sqrt(P::abs2_hi(f));
-    sstore<L>(at(lane, n), P::neg(f));
+    stE(lane, n, P::neg(f));
   }
   for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
   if (lane == 0) a.resid[p] = rmax;
@@ -244,7 +268,7 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     double best = -1.0;
     int bi = n;
     if (lane >= k && lane < n) {
-      best = P::abs2_hi(sload<L>(at(lane, k)));
+      best = P::abs2_hi(ldE(lane, k));
       bi = lane;
     }
     for (int o = 16; o; o >>= 1) {
@@ -260,14 +284,14 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     }
     if (bi != k)
       for (int j = k + lane; j < cols; j += 32) {
-        const C u = sload<L>(at(k, j)), v = sload<L>(at(bi, j));
-        sstore<L>(at(k, j), v);
-        sstore<L>(at(bi, j), u);
+        const C u = ldE(k, j), v = ldE(bi, j);
+        stE(k, j, v);
+        stE(bi, j, u);
       }
     __syncwarp();
-    const C inv = recip_warp<L>(sload<L>(at(k, k)), lane);
+    const C inv = recip_warp<L>(ldE(k, k), lane);
     if (lane == k) inv_diag = inv;
-    if (lane > k && lane < n) sstore<L>(at(lane, k), P::mul(sload<L>(at(lane, k)), inv));
+    if (lane > k && lane < n) stE(lane, k, P::mul(ldE(lane, k), inv));
     __syncwarp();
     // trailing update spread over the lanes by (row, column) pairs: ceil((n-k-1)(n-k) / 32)
     // entries per lane instead of a whole row of n-k entries
@@ -275,21 +299,21 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     const int ne = (n - k - 1) * w;
     for (int e = lane; e < ne; e += 32) {
       const int i = k + 1 + e / w, j = k + 1 + e % w;
-      sstore<L>(at(i, j), P::sub(sload<L>(at(i, j)), P::mul(sload<L>(at(i, k)), sload<L>(at(k, j)))));
+      stE(i, j, P::sub(ldE(i, j), P::mul(ldE(i, k), ldE(k, j))));
     }
     __syncwarp();
   }
   // back substitution, column oriented as in newton_solve_kernel
   for (int i = n - 1; i >= 0; --i) {
-    if (lane == i) sstore<L>(at(i, n), P::mul(sload<L>(at(i, n)), inv_diag));
+    if (lane == i) stE(i, n, P::mul(ldE(i, n), inv_diag));
     __syncwarp();
-    const C xi = sload<L>(at(i, n));
-    if (lane < i) sstore<L>(at(lane, n), P::sub(sload<L>(at(lane, n)), P::mul(sload<L>(at(lane, i)), xi)));
+    const C xi = ldE(i, n);
+    if (lane < i) stE(lane, n, P::sub(ldE(lane, n), P::mul(ldE(lane, i), xi)));
     __syncwarp();
   }
   if (lane < n) {
     const double* xp = a.X + ((size_t)p * n + lane) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), sload<L>(at(lane, n))));
+    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), ldE(lane, n)));
   }
   if (lane == 0) a.status[p] = 0;
 }
