@@ -139,37 +139,6 @@ PHC_DEV typename Prec<L>::C warp_sum(typename Prec<L>::C v) {
   return Prec<L>::norm(v);
 }
 
-// Power-table row of variable v (row a2): U[a-1] = x^a, Dd[a-1] = a x^(a-1), a = 1..E.
-template <int L>
-PHC_DEV void power_row(const typename Prec<L>::C& x, int E, double* row, bool smem) {
-  using P = Prec<L>;
-  using C = typename P::C;
-  C pw = P::one();
-  for (int a = 1; a <= E; ++a) {
-    const C dd = (a == 1) ? pw : P::mul_int(pw, (double)a);
-    pw = (a == 1) ? x : P::mul(pw, x);
-    if (smem) {
-      sstore<L>(row + (E + a - 1) * 2 * L, dd);
-      sstore<L>(row + (a - 1) * 2 * L, pw);
-    } else {
-      cstore<L>(row + (E + a - 1) * 2 * L, dd);
-      cstore<L>(row + (a - 1) * 2 * L, pw);
-    }
-  }
-}
-template <int L>
-PHC_DEV void dummy_row(int E, double* row, bool smem) {
-  using P = Prec<L>;
-  for (int a = 1; a <= E; ++a) {
-    if (smem) {
-      sstore<L>(row + (a - 1) * 2 * L, P::one());
-      sstore<L>(row + (E + a - 1) * 2 * L, P::zero());
-    } else {
-      cstore<L>(row + (a - 1) * 2 * L, P::one());
-      cstore<L>(row + (E + a - 1) * 2 * L, P::zero());
-    }
-  }
-}
 
 // x^e for 0 <= e < 256 by binary powering (square-and-multiply from the top bit): at most
 // 2 log2(e) products on the dependency path instead of e - 1.
@@ -326,7 +295,7 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   };
   auto ld = [&](int e) -> C {
     if constexpr (LAYOUT == 2) return cls_load<L>(reinterpret_cast<const double2*>(pt), NE, e, cls);
-    else if constexpr (LAYOUT == 1) return sload<L>(pt + (size_t)e * 2 * L);
+    else if constexpr (LAYOUT == 1) return row_ld<L>(pt, (size_t)e);
     else return cload<L>(pt + (size_t)e * 2 * L);
   };
   auto word_at = [&](int j) { return __ldg(fw + (j - 1) * kWarp); };  // factor j, 1-based
@@ -487,12 +456,19 @@ block_kernel(const BlockArgs a) {
     const int NE = (a.n_var + 1) * twoE;
     rows_all = smem + (size_t)NE * cd * (LAYOUT == 2 ? kClasses : 1);
     if constexpr (LAYOUT == 1) {
+      // one thread per variable: U = x^e and Dd = e x^(e-1) by repeated multiplication, stored
+      // as swizzled entries (row_st, like the row accumulators); the dummy row is U = 1, Dd = 0
       for (int v = threadIdx.x; v <= a.n_var; v += blockDim.x) {
-        double* row = pt + (size_t)v * twoE * cd;
-        if (v == a.n_var)
-          dummy_row<L>(a.E, row, true);
-        else
-          power_row<L>(cload<L>(a.X + (p * a.n_var + v) * cd), a.E, row, true);
+        const size_t e0 = (size_t)v * twoE;
+        C pw = P::one();
+        const C x = (v == a.n_var) ? P::one() : cload<L>(a.X + (p * a.n_var + v) * cd);
+        for (int e = 1; e <= a.E; ++e) {
+          C dd = (e == 1) ? pw : P::mul_int(pw, (double)e);
+          pw = (e == 1) ? x : P::mul(pw, x);
+          if (v == a.n_var) dd = P::zero();
+          row_st<L>(pt, e0 + e - 1, pw);
+          row_st<L>(pt, e0 + a.E + e - 1, dd);
+        }
       }
     } else {
       // one thread per (variable, class): each computes the row (E-1 products; cheap)
