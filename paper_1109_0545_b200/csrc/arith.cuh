@@ -599,4 +599,43 @@ PHC_DEV void sstore(double* p, const typename Prec<L>::C& v) {
     q[3] = make_double2(v.im.x[2], v.im.x[3]);
   }
 }
+
+// Shared-memory complex arrays gathered by lanes at random entries (row accumulators and
+// power tables of the block kernel's layouts 0/1, the latency path; entry idx, 2L doubles =
+// L 16-byte units).  PHC_ROW_SWIZZLE rotates the units of entry idx by (idx >> s), s = log2(8 / L), so
+// the lanes of a quarter-warp, which touch distinct entries, spread one LDS.128 over all 8
+// bank groups instead of 2 (QD) or 4 (DD).
+#ifndef PHC_ROW_SWIZZLE
+#define PHC_ROW_SWIZZLE 1
+#endif
+template <int L>
+PHC_DEV typename Prec<L>::C row_ld(const double* rows, size_t idx) {
+  typename Prec<L>::C v;
+  const double2* b = reinterpret_cast<const double2*>(rows) + idx * L;
+  constexpr int sh = (L == 4) ? 1 : 2;
+#pragma unroll
+  for (int q = 0; q < L; ++q) {
+    const int pos = PHC_ROW_SWIZZLE ? ((q + (int)(idx >> sh)) & (L - 1)) : q;
+    const double2 d = b[pos];
+    if (q < L / 2) {
+      v.re.x[2 * q] = d.x;
+      v.re.x[2 * q + 1] = d.y;
+    } else {
+      v.im.x[2 * q - L] = d.x;
+      v.im.x[2 * q - L + 1] = d.y;
+    }
+  }
+  return v;
+}
+template <int L>
+PHC_DEV void row_st(double* rows, size_t idx, const typename Prec<L>::C& v) {
+  double2* b = reinterpret_cast<double2*>(rows) + idx * L;
+  constexpr int sh = (L == 4) ? 1 : 2;
+#pragma unroll
+  for (int q = 0; q < L; ++q) {
+    const int pos = PHC_ROW_SWIZZLE ? ((q + (int)(idx >> sh)) & (L - 1)) : q;
+    b[pos] = (q < L / 2) ? make_double2(v.re.x[2 * q], v.re.x[2 * q + 1])
+                         : make_double2(v.im.x[2 * q - L], v.im.x[2 * q - L + 1]);
+  }
+}
 }  // namespace phc

@@ -128,8 +128,8 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
     const int v = idx / a.E, e = idx % a.E + 1;
     const C x = cload<L>(a.X + (p * a.n_var + v) * cd);
     const C pm = cpow_scan<L>(x, e - 1);
-    sstore<L>(pt + ((size_t)v * twoE + e - 1) * cd, e == 1 ? x : P::mul(pm, x));
-    sstore<L>(pt + ((size_t)v * twoE + a.E + e - 1) * cd, e == 1 ? pm : P::mul_int(pm, (double)e));
+    row_st<L>(pt, (size_t)v * twoE + e - 1, e == 1 ? x : P::mul(pm, x));
+    row_st<L>(pt, (size_t)v * twoE + a.E + e - 1, e == 1 ? pm : P::mul_int(pm, (double)e));
   }
   for (int e = threadIdx.x; e < W * a.n_var * cd / 2; e += blockDim.x)
     reinterpret_cast<double2*>(rows)[e] = make_double2(0.0, 0.0);
@@ -142,7 +142,6 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
   const int64_t t0 = a.poly_ptr[i], nt = a.poly_ptr[i + 1] - t0;
   const int64_t r0 = t0 + nt * s / a.S, r1 = t0 + nt * (s + 1) / a.S;  // this split's terms
   PHC_CHECK(nt >= 0 && r0 <= r1);
-  double* myrow = rows + (size_t)warp * a.n_var * cd;
   C fsum = P::zero();
   for (int64_t t = r0 + warp; t < r1; t += W) {
     const int64_t f0 = a.term_ptr[t];
@@ -156,8 +155,8 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
       v = (int)(w & 0xffffu);
       const int e = (int)((w >> 16) & 0xffu);
       PHC_CHECK(v < a.n_var && e >= 1 && e <= a.E);
-      u = sload<L>(pt + ((size_t)v * twoE + e - 1) * cd);
-      d = sload<L>(pt + ((size_t)v * twoE + a.E + e - 1) * cd);
+      u = row_ld<L>(pt, (size_t)v * twoE + e - 1);
+      d = row_ld<L>(pt, (size_t)v * twoE + a.E + e - 1);
     }
     // every lane multiplies (by 1 where the scan has no partner): no divergence around the
     // out-of-line product
@@ -179,9 +178,9 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
     if (lane == 0) before = c;
     if (lane == 31) after = P::one();
     const C g = smul<L>(smul<L>(before, d), after);
-    if (lane < k) {
-      double* acc = myrow + (size_t)v * cd;
-      sstore<L>(acc, P::add(sload<L>(acc), g));
+    if (lane < k) {  // entry index relative to `rows` (the swizzle depends on it)
+      const size_t idx = (size_t)warp * a.n_var + v;
+      row_st<L>(rows, idx, P::add(row_ld<L>(rows, idx), g));
     }
     const C y = shfl_c<L>(pre, 31, false);  // only lane 0 reads lane 31's full product
     if (k == 0) {                           // constant term: value c
@@ -198,8 +197,8 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
   for (int col = threadIdx.x; col <= a.n_var; col += blockDim.x) {
     C acc;
     if (col < a.n_var) {
-      acc = sload<L>(rows + (size_t)col * cd);
-      for (int w = 1; w < W; ++w) acc = P::add(acc, sload<L>(rows + ((size_t)w * a.n_var + col) * cd));
+      acc = row_ld<L>(rows, (size_t)col);
+      for (int w = 1; w < W; ++w) acc = P::add(acc, row_ld<L>(rows, (size_t)w * a.n_var + col));
     } else {
       acc = sload<L>(fpart);
       for (int w = 1; w < W; ++w) acc = P::add(acc, sload<L>(fpart + (size_t)w * cd));
