@@ -11,6 +11,26 @@ from . import _lib
 def _ptr(a):
     return ctypes.c_void_p(a.ctypes.data) if isinstance(a, np.ndarray) else ctypes.c_void_p(a.data_ptr())
 
+def _stream_handle(stream, device):
+    """cudaStream_t of `stream`, else of the current stream of `device` (the raw-pointer query
+    when this torch build has it: a few microseconds cheaper per call than
+    torch.cuda.current_stream(), which matters for single small evaluations)."""
+    if stream is not None:
+        return stream.cuda_stream
+    idx = device.index if device.index is not None else 0
+    if _RAW_STREAM is not None:
+        return _RAW_STREAM(idx)
+    import torch
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+try:
+    import torch as _torch
+    _RAW_STREAM = getattr(_torch._C, "_cuda_getCurrentRawStream", None)
+except Exception:  # torch without CUDA support: the handle-creating calls fail later anyway
+    _RAW_STREAM = None
+
+
 
 class System:
     """A system handle: ``System(arrays, device=0)`` with ``arrays`` having the attributes
@@ -99,7 +119,7 @@ class System:
             f = torch.empty((self.n_eq, 2, L), dtype=torch.float64, device=x.device)
         if jac is None:
             jac = torch.empty((self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=x.device)
-        st = (stream or torch.cuda.current_stream(x.device)).cuda_stream
+        st = _stream_handle(stream, x.device)
         _lib.phc_eval_jacobian(self._h, _ptr(x), _ptr(f), _ptr(jac), ctypes.c_void_p(st))
         return f, jac
 
@@ -114,7 +134,7 @@ class System:
             F = torch.empty((P, self.n_eq, 2, L), dtype=torch.float64, device=X.device)
         if J is None:
             J = torch.empty((P, self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=X.device)
-        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        st = _stream_handle(stream, X.device)
         if devices:
             dv = (ctypes.c_int32 * len(devices))(*devices)
             nd = len(devices)
@@ -135,7 +155,7 @@ class System:
             X_new = torch.empty_like(X)
         res = torch.empty(P, dtype=torch.float64, device=X.device)
         status = torch.empty(P, dtype=torch.int32, device=X.device)
-        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        st = _stream_handle(stream, X.device)
         _lib.phc_newton_step_batch(self._h, P, _ptr(X), _ptr(X_new), _ptr(res), _ptr(status), ctypes.c_void_p(st))
         return X_new, res, status
 
@@ -152,7 +172,7 @@ class System:
             F = torch.empty((P, self.n_eq, 2, L), dtype=torch.float64, device=X.device)
         if J is None:
             J = torch.empty((P, self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=X.device)
-        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        st = _stream_handle(stream, X.device)
         if devices:
             dv = (ctypes.c_int32 * len(devices))(*devices)
             nd = len(devices)
@@ -173,7 +193,7 @@ class System:
             X_new = torch.empty_like(X)
         res = torch.empty(P, dtype=torch.float64, device=X.device)
         status = torch.empty(P, dtype=torch.int32, device=X.device)
-        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        st = _stream_handle(stream, X.device)
         _lib.phc_newton_step_homotopy_batch(self._h, P, _ptr(X), _ptr(T), _ptr(X_new), _ptr(res), _ptr(status),
                                             ctypes.c_void_p(st))
         return X_new, res, status
@@ -196,7 +216,7 @@ class System:
         status = np.zeros(P, dtype=np.int32)
         stats = np.zeros((P, 5))
         te = torch.empty((P, L), dtype=torch.float64, device=X.device) if t_end else None
-        st = (stream or torch.cuda.current_stream(X.device)).cuda_stream
+        st = _stream_handle(stream, X.device)
         _lib.phc_track_paths(self._h, P, _ptr(Xe), prm, _ptr(status), _ptr(stats),
                              _ptr(te) if te is not None else None, ctypes.c_void_p(st))
         return (Xe, status, stats, te) if t_end else (Xe, status, stats)
@@ -236,7 +256,7 @@ def predict_batch(order, n_hist, t_hist, x_hist, t_new, out=None, stream=None):
     P, _, n, _, L = x_hist.shape
     if out is None:
         out = torch.empty((P, n, 2, L), dtype=torch.float64, device=x_hist.device)
-    st = (stream or torch.cuda.current_stream(x_hist.device)).cuda_stream
+    st = _stream_handle(stream, x_hist.device)
     _lib.phc_predict_batch(L, n, P, order, _ptr(n_hist), _ptr(t_hist), _ptr(x_hist), _ptr(t_new), _ptr(out),
                            ctypes.c_void_p(st))
     return out
