@@ -170,3 +170,32 @@ def test_track_graph_equals_plain_launches(phc, monkeypatch):
         assert np.array_equal(a, b)
     assert (out["1"][1] == 1).all()
     assert len(set(out["1"][2][:, 1].tolist())) > 1  # paths stop at different steps: A changes
+
+
+def test_track_graph_fallback_when_regime_changes(phc, monkeypatch):
+    """A k = 12 monomial in every polynomial makes few-path corrector calls take the latency
+    path, whose workspace is first allocated when the active paths drop -- inside a window
+    capture.  The tracker must fall back to plain launches there and still give bitwise the
+    results of a run without graphs."""
+    n, L = 12, 2
+    s, cf, X0 = total_degree_homotopy(n, L, seed=13)
+    big = [(v, 1) for v in range(n)]
+    polys = [[list(fac) for _, fac in s.terms(i)] + [big] for i in range(n)]
+    M = len(polys[0]) - 1
+    start = np.zeros((n * (M + 1), 2, L))
+    target = np.zeros((n * (M + 1), 2, L))
+    for i in range(n):
+        start[i * (M + 1):i * (M + 1) + M] = s.coeff[i * M:(i + 1) * M]
+        target[i * (M + 1):i * (M + 1) + M] = cf[i * M:(i + 1) * M]
+        target[i * (M + 1) + M, 0, 0] = 1e-3  # small k = 12 term in the target only
+    s2 = system_from_terms(n, n, L, polys, start)
+    h = phc.System(s2, coeff_target=target)
+    assert h.stats["kmax"] == 12
+    X = _cuda(X0[[0, 5, 17, 99, 1000, 2047, 3000, 4095]])
+    out = {}
+    for g in ("0", "1"):
+        monkeypatch.setenv("PHC_TRACK_GRAPH", g)
+        Xe, status, stats = h.track(X.clone(), max_steps=3000)
+        out[g] = (Xe.cpu().numpy(), status, stats)
+    for a, b in zip(out["0"], out["1"]):
+        assert np.array_equal(a, b)
