@@ -222,7 +222,9 @@ typedef struct phc_track_params {
  * otherwise step back; step-size control as in phc_track_params.  All active paths advance
  * together (one batched corrector call per Newton iteration); the step-size control runs on
  * the device and the host re-compacts the active paths every 8 steps (paths that stopped in
- * between are frozen, so the decisions are those of a check after every step).
+ * between are frozen, so the decisions are those of a check after every step).  The work runs
+ * on a private stream ordered after `stream`, each window of 8 steps replayed as a CUDA graph
+ * (captured per active-path count; plain launches where a capture is not possible).
  *   x          [n_paths][n_var][2][limbs] DEVICE pointer: start solutions in, end points out
  *              (the last accepted point of every path, refined by end_newton iterations for
  *              the paths that reached t = 1)
