@@ -248,3 +248,29 @@ def test_cooperative_elimination_singular_first_column(phc, monkeypatch):
     xn, res, status, h = _gpu_step(phc, s, X)
     assert status[0] == 1
     assert np.array_equal(xn, X)
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_newton_fuzz_shapes(phc, seed):
+    """Random square systems of varied size and precision through every elimination regime
+    (warp kernel n <= 32, shared-memory CTA kernel, cooperative and multi-kernel global
+    paths for matrices beyond shared memory), each sampled point against the oracle step
+    within the error budget."""
+    from synthetic import random_system
+    rng = np.random.Generator(np.random.PCG64(500 + seed))
+    L = int(rng.choice([2, 4]))
+    n = int(rng.choice([3, 9, 20, 33, 45, 70]))
+    P = int(rng.choice([1, 2, 6]))
+    m = int(rng.integers(3, 9))
+    k = int(min(n, rng.integers(1, 6)))
+    s, X = random_system(n, m, k, int(rng.integers(1, 4)), L, seed=600 + seed, points=P)
+    xn, res, status, h = _gpu_step(phc, s, X)
+    F, Jd = h.eval_batch(torch.from_numpy(X).cuda())
+    for p in sorted({0, P - 1}):
+        Jc = Jd.cpu().numpy()[p][..., 0, 0] + 1j * Jd.cpu().numpy()[p][..., 1, 0]
+        cond = np.linalg.cond(Jc)
+        if not np.isfinite(cond) or cond > 1e12:
+            continue  # numerically singular draw: nothing to compare at this precision
+        assert status[p] == 0
+        err = _check_point(s, X[p], xn[p], res[p])
+        assert err <= _tol(L, n, cond), (seed, n, L, P, p, err, cond)
