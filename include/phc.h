@@ -173,6 +173,22 @@ int phc_eval_homotopy_batch(const phc_system* s, int64_t n_points, const double*
 int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t,
                                    double* x_new, double* residual, int32_t* status, void* stream);
 
+/* Alg. 2 complete: Newton's method to tolerance per point,
+ *   i := 0; ||h|| := 1;  while ||h|| > tol and i < max_it:  ||h|| := max_k |h_k(z)| at z,
+ *   solve J dz = -h, z := z + dz, i := i + 1;           fail := ||h|| >= tol
+ * -- the residual tested is the one computed at the start of the iteration, so the update of
+ * the iteration whose residual passes is applied (the paper's loop).  t: NULL for the system
+ * itself, else [n_points][limbs] (DEVICE) for the homotopy h(., t) (phc_system_set_target).
+ * Per point out (DEVICE): x_out [n_points][n][2][limbs] (may alias x), residual [n_points]
+ * (the last one computed; 1.0 when max_it = 0), iterations [n_points] (int32), status
+ * [n_points] (int32): 0 converged, 1 failed (residual >= tol when the loop ended, or not
+ * finite), 2 singular Jacobian (x_out = the point at which it was met).  Every point runs the
+ * same kernels as phc_newton_step_batch, so its iterates are bitwise those of calling that
+ * function i times; finished points are frozen.  tol >= 0, max_it >= 0; synchronous. */
+int phc_newton_solve_batch(const phc_system* s, int64_t n_points, const double* x, const double* t, double tol,
+                           int32_t max_it, double* x_out, double* residual, int32_t* iterations, int32_t* status,
+                           void* stream);
+
 /* The "old" evaluator of Table 6: a handle for the (n_var + 1)-variable system
  * in which every term c x^a of the homotopy becomes c_s x^a - c_s t x^a + c_f t x^a with t
  * the variable n_var.  Evaluating it with phc_eval_jacobian[_batch] at (x, t) (t as a

@@ -17,6 +17,7 @@ from ._lib import (  # noqa: F401
     phc_last_error,
     phc_newton_step_batch,
     phc_newton_step_homotopy_batch,
+    phc_newton_solve_batch,
     phc_eval_homotopy_batch,
     phc_system_set_target,
     phc_system_create_common,

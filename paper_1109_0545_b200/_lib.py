@@ -34,6 +34,7 @@ EXPORTED = (
     "phc_track_paths",
     "phc_eval_homotopy_batch",
     "phc_newton_step_homotopy_batch",
+    "phc_newton_solve_batch",
     "phc_homotopy_old_create",
     "phc_system_stats",
     "phc_fp64_peak",
@@ -92,6 +93,8 @@ def _load():
     lib.phc_eval_homotopy_batch.restype = ctypes.c_int
     lib.phc_newton_step_homotopy_batch.argtypes = [P, i64, P, P, P, P, P, P]
     lib.phc_newton_step_homotopy_batch.restype = ctypes.c_int
+    lib.phc_newton_solve_batch.argtypes = [P, i64, P, P, ctypes.c_double, i32, P, P, P, P, P]
+    lib.phc_newton_solve_batch.restype = ctypes.c_int
     lib.phc_homotopy_old_create.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, P, P, i32]
     lib.phc_homotopy_old_create.restype = ctypes.c_int
     lib.phc_system_stats.argtypes = [P, P]
@@ -176,6 +179,10 @@ def phc_eval_homotopy_batch(h, n_points, x, t, f, jac, devices, n_devices, strea
 
 def phc_newton_step_homotopy_batch(h, n_points, x, t, x_new, residual, status, stream):
     return check(lib.phc_newton_step_homotopy_batch(h, n_points, x, t, x_new, residual, status, stream))
+
+
+def phc_newton_solve_batch(h, n_points, x, t, tol, max_it, x_out, residual, iterations, status, stream):
+    return check(lib.phc_newton_solve_batch(h, n_points, x, t, tol, max_it, x_out, residual, iterations, status, stream))
 
 
 def phc_homotopy_old_create(n_eq, n_var, limbs, n_terms, poly_ptr, term_ptr, var_idx, exponent, coeff_start,

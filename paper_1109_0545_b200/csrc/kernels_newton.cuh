@@ -207,6 +207,52 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   if (tid == 0) a.status[p] = 0;
 }
 
+// Alg. 2's loop control (phc_newton_solve_batch) after Newton iteration k (0-based) of all
+// points: a point still running records the iteration, its residual and the updated point,
+// and stops when the residual it tested passed (!(res > tol)), was not finite, or its
+// Jacobian was singular, or when k was the last iteration.  One thread per (point, coordinate);
+// coordinate 0 also writes the scalars.  The running flags are double-buffered by iteration
+// parity (act_cur read by every thread of a point, act_next written by coordinate 0), so no
+// thread of a point can see the flag its own iteration clears.
+template <int L>
+__global__ void newton_exit_kernel(int n, int64_t P_, int k, int max_it, double tol, const double* __restrict__ res,
+                                   const int32_t* __restrict__ st, const double* __restrict__ xw,
+                                   const int32_t* __restrict__ act_cur, int32_t* __restrict__ act_next,
+                                   double* __restrict__ x_out, double* __restrict__ residual,
+                                   int32_t* __restrict__ iterations, int32_t* __restrict__ status) {
+  constexpr int cd = 2 * L;
+  const int64_t gid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (gid >= P_ * n) return;
+  const int64_t p = gid / n;
+  const int i = (int)(gid % n);
+  if (!act_cur[p]) {
+    if (i == 0) act_next[p] = 0;
+    return;
+  }
+  for (int c = 0; c < cd; ++c) x_out[(p * n + i) * cd + c] = xw[(p * n + i) * cd + c];
+  if (i != 0) return;
+  const double r = res[p];
+  iterations[p] = k + 1;
+  residual[p] = r;
+  int32_t out = -1;  // -1: keep iterating
+  if (st[p] != 0) out = 2;
+  else if (!isfinite(r)) out = 1;
+  else if (!(r > tol)) out = (r >= tol) ? 1 : 0;
+  else if (k + 1 >= max_it) out = 1;
+  if (out >= 0) status[p] = out;
+  act_next[p] = out < 0 ? 1 : 0;
+}
+static __global__ void newton_solve_init_kernel(int64_t P_, int32_t* __restrict__ active, double* __restrict__ residual,
+                                                int32_t* __restrict__ iterations, int32_t* __restrict__ status,
+                                                double tol, int max_it) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P_) return;
+  active[p] = max_it > 0 ? 1 : 0;  // parity-0 running flags
+  residual[p] = 1.0;                   // the paper's initial ||h|| := 1
+  iterations[p] = 0;
+  status[p] = (1.0 >= tol) ? 1 : 0;    // the value for max_it = 0 (fail := ||h|| >= tol)
+}
+
 // ---------------------------------------------------------------------------------------
 // Small systems (n <= 32): one WARP per point, [J | -F] in the warp's slice of shared memory;
 // no block barriers -- the pivot is a warp argmax over lane = row, every lane computes the

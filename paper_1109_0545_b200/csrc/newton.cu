@@ -185,4 +185,58 @@ int phc_newton_step_homotopy_batch(const phc_system* s, int64_t n_points, const 
   return newton_impl(s, n_points, x, t, x_new, residual, status, stream);
 }
 
+int phc_newton_solve_batch(const phc_system* s, int64_t n_points, const double* x, const double* t, double tol,
+                           int32_t max_it, double* x_out, double* residual, int32_t* iterations, int32_t* status,
+                           void* stream) {
+  g_err.clear();
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (!(tol >= 0.0) || max_it < 0) return fail(PHC_EINVAL, "tol >= 0 and max_it >= 0 required");
+  if (t && !s->has_target) return fail(PHC_EINVAL, "no target coefficients: call phc_system_set_target first");
+  if (s->n_eq != s->n_var) return fail(PHC_EINVAL, "Newton needs a square system (n_eq %d != n_var %d)", s->n_eq, s->n_var);
+  if (n_points < 0) return fail(PHC_EINVAL, "n_points < 0");
+  if (n_points == 0) return PHC_OK;
+  if (!x || !x_out || !residual || !iterations || !status) return fail(PHC_EINVAL, "NULL pointer");
+  if ((((uintptr_t)x) | ((uintptr_t)x_out)) & 31) return fail(PHC_EINVAL, "x/x_out must be 32-byte aligned");
+  DeviceGuard g(s->home);
+  cudaStream_t st = (cudaStream_t)stream;
+  const int n = s->n_var, L = s->L;
+  const int64_t cd = 2 * L, P = n_points;
+  int rc;
+  DevBuf<double> xw, res;
+  DevBuf<int32_t> stt, active;
+  if ((rc = dalloc(&xw.p, (size_t)(P * n * cd))) || (rc = dalloc(&res.p, (size_t)P)) ||
+      (rc = dalloc(&stt.p, (size_t)P)) || (rc = dalloc(&active.p, (size_t)(2 * P))))
+    return rc;
+  CUDA_TRY(cudaMemcpyAsync(xw.p, x, (size_t)(P * n * cd) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  auto grid = [](int64_t nth) { return (unsigned)((nth + 127) / 128); };
+  phc::newton_solve_init_kernel<<<grid(P), 128, 0, st>>>(P, active.p, residual, iterations, status, tol, max_it);
+  if (max_it == 0)
+    CUDA_TRY(cudaMemcpyAsync(x_out, x, (size_t)(P * n * cd) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  CUDA_TRY(cudaGetLastError());
+  HostBuf<int32_t> act;
+  if ((rc = act.alloc((size_t)P))) return rc;
+  constexpr int kCheck = 4;  // iterations between host checks for an early end of the batch
+  for (int k = 0; k < max_it; ++k) {
+    if ((rc = newton_impl(s, P, xw.p, t, xw.p, res.p, stt.p, st))) return rc;
+    if (L == 2)
+      phc::newton_exit_kernel<2><<<grid(P * n), 128, 0, st>>>(n, P, k, max_it, tol, res.p, stt.p, xw.p,
+                                                             active.p + (k & 1) * P, active.p + ((k + 1) & 1) * P,
+                                                             x_out, residual, iterations, status);
+    else
+      phc::newton_exit_kernel<4><<<grid(P * n), 128, 0, st>>>(n, P, k, max_it, tol, res.p, stt.p, xw.p,
+                                                             active.p + (k & 1) * P, active.p + ((k + 1) & 1) * P,
+                                                             x_out, residual, iterations, status);
+    CUDA_TRY(cudaGetLastError());
+    if ((k + 1) % kCheck == 0 && k + 1 < max_it) {
+      CUDA_TRY(cudaMemcpyAsync(act.p, active.p + ((k + 1) & 1) * P, (size_t)P * 4, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(cudaStreamSynchronize(st));
+      bool any = false;
+      for (int64_t p = 0; p < P && !any; ++p) any = act[p] != 0;
+      if (!any) break;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(st));
+  return PHC_OK;
+}
+
 }  // extern "C"

@@ -159,6 +159,27 @@ class System:
         _lib.phc_newton_step_batch(self._h, P, _ptr(X), _ptr(X_new), _ptr(res), _ptr(status), ctypes.c_void_p(st))
         return X_new, res, status
 
+    def newton_solve(self, X, tol, max_it, T=None, X_out=None, stream=None):
+        """Alg. 2 to tolerance per point (phc_newton_solve_batch): X [P, n, 2, L] (and T [P, L]
+        for the homotopy h(., t)) on the home device -> (X_out, residual [P] float64,
+        iterations [P] int32, status [P] int32: 0 converged, 1 failed, 2 singular)."""
+        import torch
+
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        if T is not None:
+            self._check(T, (P, L))
+        if X_out is None:
+            X_out = torch.empty_like(X)
+        res = torch.empty(P, dtype=torch.float64, device=X.device)
+        its = torch.empty(P, dtype=torch.int32, device=X.device)
+        status = torch.empty(P, dtype=torch.int32, device=X.device)
+        st = _stream_handle(stream, X.device)
+        _lib.phc_newton_solve_batch(self._h, P, _ptr(X), _ptr(T) if T is not None else None, float(tol), int(max_it),
+                                    _ptr(X_out), _ptr(res), _ptr(its), _ptr(status), ctypes.c_void_p(st))
+        return X_out, res, its, status
+
     def eval_homotopy_batch(self, X, T, F=None, J=None, devices=None, stream=None):
         """h(., t_p) at X [P, n_var, 2, L] with T [P, L] (real t limbs), both on the home
         device -> (F, J) as eval_batch (NEXT-3)."""

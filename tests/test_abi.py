@@ -116,6 +116,7 @@ def test_next_row_entry_points_validate_without_device():
     assert lib.phc_system_set_target(None, None) == L.PHC_EINVAL
     assert lib.phc_eval_homotopy_batch(None, 1, None, None, None, None, None, 0, None) == L.PHC_EINVAL
     assert lib.phc_newton_step_homotopy_batch(None, 1, None, None, None, None, None, None) == L.PHC_EINVAL
+    assert lib.phc_newton_solve_batch(None, 1, None, None, 1e-20, 4, None, None, None, None, None) == L.PHC_EINVAL
     h = P()
     assert lib.phc_homotopy_old_create(ctypes.byref(h), 0, 1, 2, 0, None, None, None, None, None, None, 0) == L.PHC_EINVAL
     assert lib.phc_system_create_common(ctypes.byref(h), 2, 2, 2, 0, None, None, None, None, 0) == L.PHC_EINVAL

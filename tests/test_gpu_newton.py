@@ -274,3 +274,62 @@ def test_newton_fuzz_shapes(phc, seed):
         assert status[p] == 0
         err = _check_point(s, X[p], xn[p], res[p])
         assert err <= _tol(L, n, cond), (seed, n, L, P, p, err, cond)
+
+
+@pytest.mark.parametrize("n,k,L,tol", [(12, 4, 2, 1e-26), (40, 10, 4, 1e-55)])
+def test_newton_solve_equals_repeated_steps(phc, n, k, L, tol):
+    """Alg. 2 to tolerance (phc_newton_solve_batch) from points near a known root: every point
+    stops after the iteration whose residual (tested before its update) passed tol; its
+    result, residual and iteration count equal those of calling the Newton step the same
+    number of times (bitwise), and the result is the root to working precision."""
+    s = _root_system(n, k, L, seed=n + 1)
+    rng = np.random.default_rng(3)
+    P = 5
+    x0 = [[1 + d * complex(*rng.uniform(-1, 1, 2)) for _ in range(n)] for d in (1e-2, 1e-3, 1e-4, 1e-6, 1e-9)]
+    X = torch.from_numpy(np.stack([limbs_from_values(v, L) for v in x0])).cuda()
+    h = phc.System(s)
+    Xo, res, its, st = h.newton_solve(X, tol, 20)
+    torch.cuda.synchronize()
+    assert (st == 0).all(), (st, its, res)
+    its = its.cpu().numpy()
+    assert len(set(its.tolist())) > 1  # the points stop at different iterations
+    for p in range(P):
+        Y = X[p:p + 1].clone()
+        last = None
+        for _ in range(int(its[p])):
+            Y, r, sp = h.newton_step(Y, Y)
+            last = r
+        torch.cuda.synchronize()
+        assert torch.equal(Y[0], Xo[p]) and float(last[0]) == float(res[p])
+        assert float(res[p]) <= tol
+    from fractions import Fraction
+    xo = Xo.cpu().numpy()
+    err = max(abs(complex(float(sum(Fraction(float(d)) for d in xo[p, v, 0]) - 1), float(sum(Fraction(float(d)) for d in xo[p, v, 1]))))
+              for p in range(P) for v in range(n))
+    assert err <= (1e-28 if L == 2 else 1e-60), err
+
+
+def test_newton_solve_edge_cases(phc):
+    """max_it = 0 (point returned, residual 1, status fail unless tol > 1), max_it reached
+    (status 1), a singular Jacobian (status 2, point where it was met), the SPEC example
+    x^2 - 4 from x = 1 converging to 2."""
+    L = 2
+    s = system_from_terms(1, 1, L, [[[(0, 2)], []]], limbs_from_values([1, -4], L))
+    h = phc.System(s)
+    X = torch.from_numpy(limbs_from_values([1.0], L)[None].copy()).cuda()
+    Xo, res, its, st = h.newton_solve(X, 1e-25, 0)
+    torch.cuda.synchronize()
+    assert torch.equal(Xo, X) and int(its[0]) == 0 and float(res[0]) == 1.0 and int(st[0]) == 1
+    Xo, res, its, st = h.newton_solve(X, 1e-25, 2)
+    assert int(st[0]) == 1 and int(its[0]) == 2
+    Xo, res, its, st = h.newton_solve(X, 1e-25, 30)
+    torch.cuda.synchronize()
+    assert int(st[0]) == 0 and int(its[0]) < 30
+    z = Xo.cpu().numpy()[0, 0]
+    assert abs(float(z[0, 0]) - 2.0) == 0.0 and abs(z[0, 1]) < 1e-30 and z[1, 0] == 0.0
+    # singular at the start: f = x^2 + 1 at x = 0 -> residual 1, J = 0
+    s0 = system_from_terms(1, 1, L, [[[(0, 2)], []]], limbs_from_values([1, 1], L))
+    X0 = torch.zeros((1, 1, 2, L), dtype=torch.float64, device="cuda")
+    Xo, res, its, st = phc.System(s0).newton_solve(X0, 1e-25, 5)
+    torch.cuda.synchronize()
+    assert int(st[0]) == 2 and int(its[0]) == 1 and torch.equal(Xo, X0)

@@ -51,6 +51,8 @@ s, X = random_system(52, 4, 3, 2, 4, seed=4, points=2)
 phc.System(s).newton_step(cuda(X))            # cooperative (<= 4 points)
 s, X = random_system(52, 4, 3, 2, 4, seed=4, points=6)
 phc.System(s).newton_step(cuda(X))            # multi-kernel (> 4 points)
+s, X = config_system("c2", seed=1, points=3)
+phc.System(s).newton_solve(cuda(X), 1e-20, 6)  # Alg. 2 to tolerance
 # tracker + predictor
 s, cf, X0 = total_degree_homotopy(2, 2, seed=5)
 phc.System(s, coeff_target=cf).track(cuda(X0), max_steps=40)
