@@ -3,15 +3,18 @@
 // partial pivoting on [J | -F] ("the largest number in the current column",
 // P:342-343), back substitution and the update z := z + dz.
 //
-// Three kernels, one result (same pivot rule, same operations per entry, same order):
+// Four eliminations, one result (same pivot rule, same operations per entry, same order;
+// tested bitwise):
 //  * newton_solve_kernel: one CTA per point, [J | -F] in shared memory (n (n+1) complex values
-//    up to ~200 KB); the paper's per-column pivot barrier is a __syncthreads, its
-//    row-per-thread assignment a (row, column) grid-stride over the CTA;
+//    up to ~200 KB, real and imaginary planes); the paper's per-column pivot barrier
+//     is one __syncthreads per column after a look-ahead warp, its row-per-thread
+//    assignment a (row, column) grid-stride over the CTA;
 //  * newton_warp_kernel: n <= 32, one warp per point (lane = row), no block barriers;
 //  * the multi-kernel elimination (newton_*_kernel below): matrices beyond shared memory, two
 //    launches per column over all points, the trailing update spread over many SMs;
 //  * newton_coop_kernel: matrices beyond shared memory and few points, one persistent
 //    cooperative launch (grid-wide barriers instead of kernel boundaries, one per column).
+// Plus the loop control of Alg. 2 to tolerance (newton_exit_kernel, phc_newton_solve_batch).
 #pragma once
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
