@@ -56,6 +56,31 @@ struct NewtonArgs {
   int64_t n_points;
 };
 
+// Complex entries kept as a real and an imaginary plane (the shared-memory eliminations):
+// entry offset o (in doubles within a plane), L doubles per part, 16-byte accesses.
+template <int L>
+PHC_DEV typename Prec<L>::C plane_ld(const double* re, const double* im, size_t o) {
+  typename Prec<L>::C v;
+#pragma unroll
+  for (int q = 0; q < L; q += 2) {
+    const double2 x = *reinterpret_cast<const double2*>(re + o + q);
+    const double2 y = *reinterpret_cast<const double2*>(im + o + q);
+    v.re.x[q] = x.x;
+    v.re.x[q + 1] = x.y;
+    v.im.x[q] = y.x;
+    v.im.x[q + 1] = y.y;
+  }
+  return v;
+}
+template <int L>
+PHC_DEV void plane_st(double* re, double* im, size_t o, const typename Prec<L>::C& v) {
+#pragma unroll
+  for (int q = 0; q < L; q += 2) {
+    *reinterpret_cast<double2*>(re + o + q) = make_double2(v.re.x[q], v.re.x[q + 1]);
+    *reinterpret_cast<double2*>(im + o + q) = make_double2(v.im.x[q], v.im.x[q + 1]);
+  }
+}
+
 // Shared memory of newton_solve_kernel: [J | -F], the pivot reciprocals, two row permutations.
 __host__ __device__ inline size_t solve_smem_bytes(int n, int L) {
   return ((size_t)n * (n + 1) + n) * 2 * L * sizeof(double) + (size_t)2 * n * sizeof(int);
@@ -90,28 +115,8 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   double* Mim = Mre + (size_t)n * cols * L;
   double* invd = Mim + (size_t)n * cols * L;  // n pivot reciprocals after the matrix
   int* pbuf = reinterpret_cast<int*>(invd + (size_t)n * cd);  // [2][n] row permutations
-  auto ldE = [&](int r, int c) -> C {
-    C v;
-    const size_t o = ((size_t)r * cols + c) * L;
-#pragma unroll
-    for (int q = 0; q < L; q += 2) {
-      const double2 x = *reinterpret_cast<const double2*>(Mre + o + q);
-      const double2 y = *reinterpret_cast<const double2*>(Mim + o + q);
-      v.re.x[q] = x.x;
-      v.re.x[q + 1] = x.y;
-      v.im.x[q] = y.x;
-      v.im.x[q + 1] = y.y;
-    }
-    return v;
-  };
-  auto stE = [&](int r, int c, const C& v) {
-    const size_t o = ((size_t)r * cols + c) * L;
-#pragma unroll
-    for (int q = 0; q < L; q += 2) {
-      *reinterpret_cast<double2*>(Mre + o + q) = make_double2(v.re.x[q], v.re.x[q + 1]);
-      *reinterpret_cast<double2*>(Mim + o + q) = make_double2(v.im.x[q], v.im.x[q + 1]);
-    }
-  };
+  auto ldE = [&](int r, int c) { return plane_ld<L>(Mre, Mim, ((size_t)r * cols + c) * L); };
+  auto stE = [&](int r, int c, const C& v) { plane_st<L>(Mre, Mim, ((size_t)r * cols + c) * L, v); };
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
   // load [J | -F]; residual max_i |F_i|; identity permutation
@@ -277,28 +282,8 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
   // the warp's [J | -F] as real and imaginary planes (as in newton_solve_kernel)
   double* Mre = wsm + (size_t)wib * n * cols * cd;
   double* Mim = Mre + (size_t)n * cols * L;
-  auto ldE = [&](int r, int c) -> C {
-    C v;
-    const size_t o = ((size_t)r * cols + c) * L;
-#pragma unroll
-    for (int q = 0; q < L; q += 2) {
-      const double2 x = *reinterpret_cast<const double2*>(Mre + o + q);
-      const double2 y = *reinterpret_cast<const double2*>(Mim + o + q);
-      v.re.x[q] = x.x;
-      v.re.x[q + 1] = x.y;
-      v.im.x[q] = y.x;
-      v.im.x[q + 1] = y.y;
-    }
-    return v;
-  };
-  auto stE = [&](int r, int c, const C& v) {
-    const size_t o = ((size_t)r * cols + c) * L;
-#pragma unroll
-    for (int q = 0; q < L; q += 2) {
-      *reinterpret_cast<double2*>(Mre + o + q) = make_double2(v.re.x[q], v.re.x[q + 1]);
-      *reinterpret_cast<double2*>(Mim + o + q) = make_double2(v.im.x[q], v.im.x[q + 1]);
-    }
-  };
+  auto ldE = [&](int r, int c) { return plane_ld<L>(Mre, Mim, ((size_t)r * cols + c) * L); };
+  auto stE = [&](int r, int c, const C& v) { plane_st<L>(Mre, Mim, ((size_t)r * cols + c) * L, v); };
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
   // coalesced: consecutive lanes read consecutive entries of J
