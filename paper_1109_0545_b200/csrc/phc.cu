@@ -359,25 +359,26 @@ int eval_batch_impl(const phc_system* cs, int64_t n_points, const double* x, con
   if (n_points == 0) return PHC_OK;
   if (!x || !f || !jac) return fail(PHC_EINVAL, "NULL x/f/jac");
   if ((((uintptr_t)x) | ((uintptr_t)f) | ((uintptr_t)jac)) & 31) return fail(PHC_EINVAL, "x/f/jac must be 32-byte aligned");
-  std::vector<int> devs;
-  if (!devices || n_devices <= 0)
-    devs.push_back(s->home);
-  else
-    devs.assign(devices, devices + n_devices);
-  int ndev = 0;
-  cudaGetDeviceCount(&ndev);
-  for (int dv : devs)
-    if (dv < 0 || dv >= ndev) return fail(PHC_EINVAL, "device %d out of range", dv);
   cudaStream_t st = (cudaStream_t)stream;
-  DeviceGuard g(s->home);
-  const int64_t cd = 2 * s->L;
-  const int64_t G = (int64_t)devs.size();
-  if (G == 1 && devs[0] == s->home) {
+  if (!devices || n_devices <= 0 || (n_devices == 1 && devices[0] == s->home)) {
+    // the common case, on the home device (no device-list bookkeeping on the latency path)
+    DeviceGuard g(s->home);
     DeviceState* d;
     int rc = get_device_state(s, s->home, &d);
     if (rc) return rc;
     return run_on_device(s, d, n_points, x, T, f, jac, st);
   }
+  std::vector<int> devs(devices, devices + n_devices);
+  static const int ndev = [] {
+    int c = 0;
+    cudaGetDeviceCount(&c);
+    return c;
+  }();
+  for (int dv : devs)
+    if (dv < 0 || dv >= ndev) return fail(PHC_EINVAL, "device %d out of range", dv);
+  DeviceGuard g(s->home);
+  const int64_t cd = 2 * s->L;
+  const int64_t G = (int64_t)devs.size();
   // sharded: contiguous equal ranges [g P / G, (g+1) P / G)
   cudaEvent_t start;
   CUDA_TRY(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
