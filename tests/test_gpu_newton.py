@@ -250,7 +250,7 @@ def test_cooperative_elimination_singular_first_column(phc, monkeypatch):
     assert np.array_equal(xn, X)
 
 
-@pytest.mark.parametrize("seed", range(12))
+@pytest.mark.parametrize("seed", range(int(__import__("os").environ.get("PHC_FUZZ_SEEDS_NEWTON", "12"))))
 def test_newton_fuzz_shapes(phc, seed):
     """Random square systems of varied size and precision through every elimination regime
     (warp kernel n <= 32, shared-memory CTA kernel, cooperative and multi-kernel global
