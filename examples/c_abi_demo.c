@@ -4,6 +4,7 @@
  * exact values (SPEC S:158, S:218 style hand computations):
  *   F = (12 + 3 - 2i, 30 - 625) = (15 - 2i, -595)
  *   J = [[2 x0 x1, x0^2, 0], [x1 x2, x0 x2, x0 x1 - 4 x2^3]] = [[12, 4, 0], [15, 10, -494]]
+ * Then Alg. 2 to tolerance (phc_newton_solve_batch) on x^2 - 4 = 0 from x = 1: the root 2.
  * Build: gcc -O2 c_abi_demo.c -I../include -L../paper_1109_0545_b200 -lphc
  *        -I/usr/local/cuda/include -L/usr/local/cuda/lib64 -lcudart  */
 #include <cuda_runtime.h>
@@ -53,5 +54,37 @@ int main(void) {
   cudaFree(dx);
   cudaFree(df);
   cudaFree(dj);
-  return bad;
+  /* Newton's method to tolerance on g = x^2 - 4 */
+  const int64_t gp[2] = {0, 2}, gt[3] = {0, 1, 1};
+  const int32_t gv[1] = {0}, ge[1] = {2};
+  double gc[2][2][2];
+  memset(gc, 0, sizeof gc);
+  gc[0][0][0] = 1.0;
+  gc[1][0][0] = -4.0;
+  phc_system* g = NULL;
+  rc = phc_system_create(&g, 1, 1, L, 2, gp, gt, gv, ge, &gc[0][0][0], 0);
+  if (rc) { printf("create failed: %d %s\n", rc, phc_last_error()); return 1; }
+  double z0[1][2][2] = {{{1.0, 0.0}, {0.0, 0.0}}}, z[1][2][2];
+  double *dz, *dres;
+  int32_t *dits, *dst;
+  cudaMalloc((void**)&dz, sizeof z0);
+  cudaMalloc((void**)&dres, sizeof(double));
+  cudaMalloc((void**)&dits, sizeof(int32_t));
+  cudaMalloc((void**)&dst, sizeof(int32_t));
+  cudaMemcpy(dz, z0, sizeof z0, cudaMemcpyHostToDevice);
+  rc = phc_newton_solve_batch(g, 1, dz, NULL, 1e-28, 20, dz, dres, dits, dst, NULL);
+  if (rc) { printf("newton failed: %d %s\n", rc, phc_last_error()); return 1; }
+  int32_t its = 0, stn = -1;
+  cudaMemcpy(z, dz, sizeof z, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&its, dits, sizeof its, cudaMemcpyDeviceToHost);
+  cudaMemcpy(&stn, dst, sizeof stn, cudaMemcpyDeviceToHost);
+  const int nbad = stn != 0 || z[0][0][0] != 2.0 || z[0][1][0] != 0.0;
+  printf("Newton on x^2 - 4 from 1: %d iterations, x = %.17g, status %d; %s\n", its, z[0][0][0], stn,
+         nbad ? "MISMATCH" : "exact");
+  phc_system_destroy(g);
+  cudaFree(dz);
+  cudaFree(dres);
+  cudaFree(dits);
+  cudaFree(dst);
+  return bad | nbad;
 }

@@ -1,5 +1,6 @@
 """The boundary is a C ABI: a plain C program (examples/c_abi_demo.c, gcc, no Python in the
-loop) creates a system, evaluates it on the device and checks the exact values."""
+loop) creates a system, evaluates it on the device and checks the exact values, then runs
+Alg. 2 to tolerance on x^2 - 4 from 1 (root 2 exactly)."""
 import os
 import subprocess
 
