@@ -17,11 +17,25 @@ def _limbs_to_mpc(re_limbs, im_limbs):
                       mpmath.fsum([mpmath.mpf(float(d)) for d in im_limbs]))
 
 
+def _check_shapes(ref_values, gpu_limbs):
+    """The two sides must describe the same N complex values: ``gpu_limbs`` is [N][2][L]
+    (real limbs, imaginary limbs) and ``ref_values`` has exactly N entries.  A mismatch is an
+    error, never a silent truncation (``zip`` would compare only the common prefix)."""
+    ref_values = list(ref_values)
+    gpu_limbs = np.asarray(gpu_limbs)
+    if gpu_limbs.ndim != 3 or gpu_limbs.shape[1] != 2 or gpu_limbs.shape[2] < 1:
+        raise ValueError(f"gpu limbs must be [N][2][L], got shape {gpu_limbs.shape}")
+    if len(ref_values) != gpu_limbs.shape[0]:
+        raise ValueError(f"{len(ref_values)} oracle values against {gpu_limbs.shape[0]} GPU values")
+    return ref_values, gpu_limbs
+
+
 def rel_errors(ar, ref_values, gpu_limbs, prec=1024):
     """Normwise relative error of ``gpu_limbs`` (float64 [N][2][L]) against the
     oracle values ``ref_values`` (N values of arithmetic ``ar``).  Returns
-    (err, max_abs_delta, max_abs_ref) as floats."""
-    gpu_limbs = np.asarray(gpu_limbs)
+    (err, max_abs_delta, max_abs_ref) as floats.  Raises ValueError when the two
+    sides do not hold the same number of values."""
+    ref_values, gpu_limbs = _check_shapes(ref_values, gpu_limbs)
     with mpmath.workprec(prec):
         inf_d = mpmath.mpf(0)
         inf_r = mpmath.mpf(0)
@@ -45,8 +59,10 @@ def rel_errors(ar, ref_values, gpu_limbs, prec=1024):
 
 def exact_equal_limbs(ar, ref_values, gpu_limbs):
     """True iff every GPU value equals the exact oracle value exactly (bitwise for
-    exactly representable results, P5)."""
-    for ref, g in zip(ref_values, np.asarray(gpu_limbs)):
+    exactly representable results, P5).  Raises ValueError when the two sides do not
+    hold the same number of values."""
+    ref_values, gpu_limbs = _check_shapes(ref_values, gpu_limbs)
+    for ref, g in zip(ref_values, gpu_limbs):
         gv = ar.from_limbs(g[0], g[1])
         a, b, e = ar.add(gv, ar.scale_int(ref, -1))
         if a != 0 or b != 0:

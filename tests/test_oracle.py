@@ -294,3 +294,101 @@ def test_error_metric_detects_a_lost_limb():
     lim[3, 0, 1] = 0.0
     err, _, _ = rel_errors(EX, F, lim)
     assert err > 1e-20
+
+
+# ---------------------------------------------------------------------------
+# the comparators themselves (oracle/compare.py): exact_equal_limbs decides every bitwise
+# P4/P5 GPU test, rel_errors every tolerance test; pin both against values built here
+# from Python Fractions (independent of ExactArith.from_limbs)
+# ---------------------------------------------------------------------------
+
+def _fraction_to_exact(fr):
+    """Fraction with a power-of-two denominator -> ExactArith real (m, e)."""
+    num, den = fr.numerator, fr.denominator
+    assert den & (den - 1) == 0
+    return num, -(den.bit_length() - 1)
+
+
+def _exact_from_fractions(re, im):
+    (a, ea), (b, eb) = _fraction_to_exact(re), _fraction_to_exact(im)
+    e = min(ea, eb)
+    return (a << (ea - e), b << (eb - e), e)
+
+
+def _random_limbs(rng, N, L):
+    """N normalised complex values of L limbs each (leading limb ~U(-1, 1), each next limb
+    below half an ulp of the previous one)."""
+    out = np.zeros((N, 2, L))
+    for j in range(N):
+        for p in range(2):
+            h = rng.uniform(-1, 1)
+            for l in range(L):
+                out[j, p, l] = h
+                h = rng.uniform(-0.5, 0.5) * np.spacing(abs(h))
+    return out
+
+
+@pytest.mark.parametrize("L", [2, 4])
+def test_exact_equal_limbs_pinned(L):
+    from oracle import exact_equal_limbs
+    rng = np.random.default_rng(11 + L)
+    lim = _random_limbs(rng, 6, L)
+    refs = [_exact_from_fractions(sum(Fraction(float(d)) for d in lim[j, 0]),
+                                  sum(Fraction(float(d)) for d in lim[j, 1])) for j in range(6)]
+    assert exact_equal_limbs(EX, refs, lim)
+    # a one-ulp change of ANY limb of either part of any value is seen
+    for j in (0, 5):
+        for p in (0, 1):
+            for l in range(L):
+                bad = lim.copy()
+                bad[j, p, l] = np.nextafter(bad[j, p, l], np.inf)
+                assert not exact_equal_limbs(EX, refs, bad), (j, p, l)
+    # conjugation (imaginary part negated) and swapped parts are seen
+    bad = lim.copy()
+    bad[2, 1] = -bad[2, 1]
+    assert not exact_equal_limbs(EX, refs, bad)
+    bad = lim.copy()
+    bad[3] = bad[3, ::-1]
+    assert not exact_equal_limbs(EX, refs, bad)
+    # the same VALUE in a different (non-normalised) limb split is equal: values, not bits
+    alt = lim.copy()
+    h = alt[1, 0, 0]
+    u = np.spacing(abs(h))
+    alt[1, 0, 0] = h + u
+    alt[1, 0, 1] = alt[1, 0, 1] - u
+    assert Fraction(float(alt[1, 0, 1])) == Fraction(float(lim[1, 0, 1])) - Fraction(float(u))
+    assert exact_equal_limbs(EX, refs, alt)
+
+
+@pytest.mark.parametrize("fn", ["exact", "rel"])
+def test_comparators_reject_length_and_shape_mismatch(fn):
+    """A truncated or over-long GPU array, or one in the wrong layout, is an error: zip() would
+    otherwise compare only the common prefix and pass."""
+    from oracle import exact_equal_limbs
+    rng = np.random.default_rng(3)
+    lim = _random_limbs(rng, 5, 4)
+    refs = [_exact_from_fractions(sum(Fraction(float(d)) for d in lim[j, 0]),
+                                  sum(Fraction(float(d)) for d in lim[j, 1])) for j in range(5)]
+    call = (lambda r, g: exact_equal_limbs(EX, r, g)) if fn == "exact" else (lambda r, g: rel_errors(EX, r, g))
+    call(refs, lim)
+    with pytest.raises(ValueError):
+        call(refs, lim[:4])          # GPU side truncated
+    with pytest.raises(ValueError):
+        call(refs[:4], lim)          # oracle side truncated
+    with pytest.raises(ValueError):
+        call(refs, lim.transpose(0, 2, 1))  # [N][L][2] instead of [N][2][L]
+    with pytest.raises(ValueError):
+        call(refs, lim.reshape(5, -1))
+
+
+def test_rel_errors_pinned_values():
+    """rel_errors against hand-computed norms: one entry off by exactly 2^-60 in a vector whose
+    largest modulus is 2 (and Frobenius norm sqrt(1 + 4 + 4)) gives max(2^-60 / 2, 2^-60 / 3)."""
+    vals = [(1, 0, 0), (0, 2, 0), (2, 0, 0)]
+    lim = np.zeros((3, 2, 2))
+    lim[0, 0, 0], lim[1, 1, 0], lim[2, 0, 0] = 1.0, 2.0, 2.0
+    assert rel_errors(EX, vals, lim)[0] == 0.0
+    lim[1, 0, 1] = 2.0 ** -60           # real part of entry 1 gains 2^-60
+    err, dmax, rmax = rel_errors(EX, vals, lim)
+    assert dmax == 2.0 ** -60 and rmax == 2.0
+    assert err == pytest.approx(2.0 ** -61, rel=1e-12)  # inf-norm ratio 2^-61 > Frobenius 2^-60/3
