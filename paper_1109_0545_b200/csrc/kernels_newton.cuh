@@ -25,6 +25,11 @@
 
 namespace phc {
 
+// Residual maximum that propagates NaN (fmax drops it): once an operand is NaN the result is
+// NaN, so a non-finite F always reaches resid[] and the !isfinite(r) exits in phc.h fire.
+__device__ __forceinline__ double nan_max(double a, double b) { return (b != b || b > a) ? b : a; }
+
+
 // The pivot reciprocal (the serial step of every elimination column) computed by a whole
 // warp: lane 0 divides the real part by |a|^2, lane 1 the imaginary part -- P::recip's own
 // operations, so the value is bitwise P::recip(a) -- and every lane receives the result.  The
@@ -102,7 +107,10 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   extern __shared__ __align__(16) double nsm[];
   __shared__ double red_v[32];
   __shared__ int red_i[32];
-  __shared__ int s_bad;
+  // s_bad[c & 1] = 1 when pivot column c is zero.  Double-buffered: warp 0 writes column
+  // k + 1's slot during iteration k while the other warps may still be reading column k's
+  // slot in the loop condition (one slot would let them leave the loop one barrier early)
+  __shared__ int s_bad[2];
   const int64_t p = blockIdx.x;
   if (p >= a.n_points) return;
   const int n = a.n, cols = n + 1, cd = 2 * L;
@@ -127,18 +135,18 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       stE(i, j, cload<L>(Jp + ((size_t)i * n + j) * cd));
     } else {
       const C f = cload<L>(Fp + (size_t)i * cd);
-      rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
+      rmax = nan_max(rmax, sqrt(P::abs2_hi(f)));
       stE(i, j, P::neg(f));
     }
   }
   for (int i = tid; i < n; i += T) pbuf[i] = i;
-  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  for (int o = 16; o; o >>= 1) rmax = nan_max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
   if (lane == 0) red_v[wid] = rmax;
-  if (tid == 0) s_bad = 0;
+  if (tid == 0) s_bad[0] = s_bad[1] = 0;
   __syncthreads();
   if (tid == 0) {
     double r = 0.0;
-    for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
+    for (int w = 0; w < nwarp; ++w) r = nan_max(r, red_v[w]);
     a.resid[p] = r;
   }
   // warp 0: pivot of column c among logical rows c.. of `src`, exchanged permutation to `dst`,
@@ -164,10 +172,10 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     return true;
   };
   int cur = 0;  // pbuf + cur * n: the permutation after the exchanges of columns < k + 1
-  if (wid == 0 && !pivot_column(pbuf, pbuf + n, 0) && lane == 0) s_bad = 1;
+  if (wid == 0 && !pivot_column(pbuf, pbuf + n, 0) && lane == 0) s_bad[0] = 1;
   __syncthreads();
   cur = 1;
-  for (int k = 0; k < n - 1 && !s_bad; ++k) {
+  for (int k = 0; k < n - 1 && !s_bad[k & 1]; ++k) {
     const int* pc = pbuf + cur * n;
     int* pn = pbuf + (cur ^ 1) * n;
     if (wid == 0) {
@@ -176,7 +184,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       for (int i = k + 1 + lane; i < n; i += 32)
         stE(pc[i], k + 1, P::sub(ldE(pc[i], k + 1), P::mul(ldE(pc[i], k), pk)));
       __syncwarp();
-      if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad = 1;
+      if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad[(k + 1) & 1] = 1;
     } else if ((wid & 3) != 0 || nwarp <= 4) {
       // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1, off warp 0's SMSP
       const int worker = (nwarp > 4) ? (wid >> 2) * 3 + (wid & 3) - 1 : wid - 1;
@@ -192,7 +200,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     __syncthreads();
     cur ^= 1;
   }
-  if (s_bad) {
+  if (s_bad[0] | s_bad[1]) {
     if (tid == 0) a.status[p] = 1;
     for (int e = tid; e < n; e += T)
       cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
@@ -255,7 +263,8 @@ static __global__ void newton_solve_init_kernel(int64_t P_, int32_t* __restrict_
                                                 double tol, int max_it) {
   const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= P_) return;
-  active[p] = max_it > 0 ? 1 : 0;  // parity-0 running flags
+  // parity-0 running flags: Alg. 2 enters its loop only while ||h|| = 1 > tol
+  active[p] = (max_it > 0 && 1.0 > tol) ? 1 : 0;
   residual[p] = 1.0;                   // the paper's initial ||h|| := 1
   iterations[p] = 0;
   status[p] = (1.0 >= tol) ? 1 : 0;    // the value for max_it = 0 (fail := ||h|| >= tol)
@@ -294,7 +303,7 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     rmax = sqrt(P::abs2_hi(f));
     stE(lane, n, P::neg(f));
   }
-  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  for (int o = 16; o; o >>= 1) rmax = nan_max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
   if (lane == 0) a.resid[p] = rmax;
   __syncwarp();
   C inv_diag = P::zero();  // lane i keeps 1 / U[i][i] for the back substitution
@@ -383,16 +392,16 @@ __global__ void __launch_bounds__(256) newton_load_kernel(const NewtonArgs a) {
       sstore<L>(M + (size_t)e * cd, cload<L>(Jp + ((size_t)i * n + j) * cd));
     } else {
       const C f = cload<L>(Fp + (size_t)i * cd);
-      rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
+      rmax = nan_max(rmax, sqrt(P::abs2_hi(f)));
       sstore<L>(M + (size_t)e * cd, P::neg(f));
     }
   }
-  for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+  for (int o = 16; o; o >>= 1) rmax = nan_max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
   if (lane == 0) red_v[wid] = rmax;
   __syncthreads();
   if (tid == 0) {
     double r = 0.0;
-    for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
+    for (int w = 0; w < nwarp; ++w) r = nan_max(r, red_v[w]);
     a.resid[p] = r;
     a.status[p] = 0;
   }
@@ -601,7 +610,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
     if (!(best > 0.0)) {
       if (lane == 0) {
         s_bad = 1;
-        flag_g[0] = 1;
+        flag_g[c & 1] = 1;  // column c's slot: see the read in the k loop
       }
       return;
     }
@@ -652,26 +661,26 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
         sstore<L>(at(i, j), cload<L>(Jp + ((size_t)i * n + j) * cd));
       } else {
         const C f = cload<L>(Fp + (size_t)i * cd);
-        rmax = fmax(rmax, sqrt(P::abs2_hi(f)));
+        rmax = nan_max(rmax, sqrt(P::abs2_hi(f)));
         sstore<L>(at(i, j), P::neg(f));
       }
     }
-    for (int o = 16; o; o >>= 1) rmax = fmax(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
+    for (int o = 16; o; o >>= 1) rmax = nan_max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
     if (lane == 0) red_v[wid] = rmax;
     __syncthreads();
     if (tid == 0) {
       double r = 0.0;
-      for (int w = 0; w < nwarp; ++w) r = fmax(r, red_v[w]);
+      for (int w = 0; w < nwarp; ++w) r = nan_max(r, red_v[w]);
       red_g[b] = r;
       s_bad = 0;
     }
-    if (b == 0 && tid == 0) flag_g[0] = 0;
+    if (b == 0 && tid == 0) flag_g[0] = flag_g[1] = 0;
     grid.sync();
     if (b == 0) {
       // column 0: pivot, exchange, reciprocal, multipliers; column 1 kept for step 0
       if (tid == 0) {
         double r = 0.0;
-        for (int q = 0; q < G; ++q) r = fmax(r, __ldcg(red_g + q));
+        for (int q = 0; q < G; ++q) r = nan_max(r, __ldcg(red_g + q));
         a.resid[p] = r;
       }
       double best = -1.0;
@@ -718,9 +727,12 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
         if (!s_bad) multipliers(M, k + 1);
         COOP_T(k, 3)
       } else {
-        if (tid == 0) s_bad = __ldcg(flag_g);
+        // column k's pivot status, written by CTA 0 before the last grid barrier.  Column k+1's
+        // status goes to the other slot during this iteration, so an early write cannot make
+        // this CTA leave the loop one grid barrier before CTA 0 (barrier counts would diverge)
+        if (tid == 0) s_bad = __ldcg(flag_g + (k & 1));
         __syncthreads();
-        if (s_bad) break;  // grid-uniform: written before the last barrier
+        if (s_bad) break;  // grid-uniform
         for (int i = tid; i < n; i += T) {
           perm[i] = __ldcg(perm_g + (size_t)(k & 1) * n + i);
           PHC_CHECK(perm[i] >= 0 && perm[i] < n);

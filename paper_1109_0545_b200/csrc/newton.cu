@@ -210,9 +210,12 @@ int phc_newton_solve_batch(const phc_system* s, int64_t n_points, const double* 
   CUDA_TRY(cudaMemcpyAsync(xw.p, x, (size_t)(P * n * cd) * sizeof(double), cudaMemcpyDeviceToDevice, st));
   auto grid = [](int64_t nth) { return (unsigned)((nth + 127) / 128); };
   phc::newton_solve_init_kernel<<<grid(P), 128, 0, st>>>(P, active.p, residual, iterations, status, tol, max_it);
-  if (max_it == 0)
+  // x_out := x for points that never enter the loop (max_it = 0, or tol >= 1 = the initial
+  // ||h||); the exit kernel overwrites the entries of every point that runs
+  if (x_out != x)
     CUDA_TRY(cudaMemcpyAsync(x_out, x, (size_t)(P * n * cd) * sizeof(double), cudaMemcpyDeviceToDevice, st));
   CUDA_TRY(cudaGetLastError());
+  if (!(1.0 > tol)) max_it = 0;  // the loop condition ||h|| > tol fails before the first iteration
   HostBuf<int32_t> act;
   if ((rc = act.alloc((size_t)P))) return rc;
   constexpr int kCheck = 4;  // iterations between host checks for an early end of the batch

@@ -224,7 +224,9 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
       d->count_cap = 0;
       int rc = dalloc(&d->count, (size_t)nc);
       if (rc) return rc;
-      CUDA_TRY(cudaMemset(d->count, 0, nc * sizeof(int)));
+      // zeroed on the caller's stream (ordered before the kernel that counts arrivals; the
+      // legacy-stream cudaMemset is not ordered against non-blocking streams)
+      CUDA_TRY(cudaMemsetAsync(d->count, 0, nc * sizeof(int), st));
       d->count_cap = nc;
     }
     a.count = d->count;

@@ -106,6 +106,10 @@ class System:
 
         if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
             raise ValueError("expected a contiguous float64 CUDA tensor")
+        if t.device.index != self.device:
+            # the C ABI takes device pointers on the handle's home device; a pointer on another
+            # GPU would fault inside the kernels (a sticky context error), so refuse it here
+            raise ValueError(f"tensor on cuda:{t.device.index}, the system's home device is cuda:{self.device}")
         if tuple(t.shape) != tuple(shape):
             raise ValueError(f"expected shape {tuple(shape)}, got {tuple(t.shape)}")
 
@@ -119,6 +123,8 @@ class System:
             f = torch.empty((self.n_eq, 2, L), dtype=torch.float64, device=x.device)
         if jac is None:
             jac = torch.empty((self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=x.device)
+        self._check(f, (self.n_eq, 2, L))
+        self._check(jac, (self.n_eq, self.n_var, 2, L))
         st = _stream_handle(stream, x.device)
         _lib.phc_eval_jacobian(self._h, _ptr(x), _ptr(f), _ptr(jac), ctypes.c_void_p(st))
         return f, jac
@@ -134,6 +140,8 @@ class System:
             F = torch.empty((P, self.n_eq, 2, L), dtype=torch.float64, device=X.device)
         if J is None:
             J = torch.empty((P, self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=X.device)
+        self._check(F, (P, self.n_eq, 2, L))
+        self._check(J, (P, self.n_eq, self.n_var, 2, L))
         st = _stream_handle(stream, X.device)
         if devices:
             dv = (ctypes.c_int32 * len(devices))(*devices)
@@ -153,6 +161,7 @@ class System:
         self._check(X, (P, self.n_var, 2, L))
         if X_new is None:
             X_new = torch.empty_like(X)
+        self._check(X_new, (P, self.n_var, 2, L))
         res = torch.empty(P, dtype=torch.float64, device=X.device)
         status = torch.empty(P, dtype=torch.int32, device=X.device)
         st = _stream_handle(stream, X.device)
@@ -172,6 +181,7 @@ class System:
             self._check(T, (P, L))
         if X_out is None:
             X_out = torch.empty_like(X)
+        self._check(X_out, (P, self.n_var, 2, L))
         res = torch.empty(P, dtype=torch.float64, device=X.device)
         its = torch.empty(P, dtype=torch.int32, device=X.device)
         status = torch.empty(P, dtype=torch.int32, device=X.device)
@@ -193,6 +203,8 @@ class System:
             F = torch.empty((P, self.n_eq, 2, L), dtype=torch.float64, device=X.device)
         if J is None:
             J = torch.empty((P, self.n_eq, self.n_var, 2, L), dtype=torch.float64, device=X.device)
+        self._check(F, (P, self.n_eq, 2, L))
+        self._check(J, (P, self.n_eq, self.n_var, 2, L))
         st = _stream_handle(stream, X.device)
         if devices:
             dv = (ctypes.c_int32 * len(devices))(*devices)
@@ -212,6 +224,7 @@ class System:
         self._check(T, (P, L))
         if X_new is None:
             X_new = torch.empty_like(X)
+        self._check(X_new, (P, self.n_var, 2, L))
         res = torch.empty(P, dtype=torch.float64, device=X.device)
         status = torch.empty(P, dtype=torch.int32, device=X.device)
         st = _stream_handle(stream, X.device)
@@ -250,6 +263,11 @@ class System:
             F = np.empty((P, self.n_eq, 2, L))
         if J is None:
             J = np.empty((P, self.n_eq, self.n_var, 2, L))
+        for a, shape in ((X, (P, self.n_var, 2, L)), (F, (P, self.n_eq, 2, L)), (J, (P, self.n_eq, self.n_var, 2, L))):
+            if not (isinstance(a, np.ndarray) and a.dtype == np.float64 and a.flags.c_contiguous):
+                raise ValueError("expected C-contiguous float64 numpy arrays (host memory)")
+            if a.shape != shape:
+                raise ValueError(f"expected shape {shape}, got {a.shape}")
         if devices:
             dv = (ctypes.c_int32 * len(devices))(*devices)
             nd = len(devices)

@@ -333,3 +333,71 @@ def test_newton_solve_edge_cases(phc):
     Xo, res, its, st = phc.System(s0).newton_solve(X0, 1e-25, 5)
     torch.cuda.synchronize()
     assert int(st[0]) == 2 and int(its[0]) == 1 and torch.equal(Xo, X0)
+
+
+def test_newton_solve_tol_at_least_one_runs_no_iteration(phc):
+    """Alg. 2 starts from ||h|| := 1 and loops while ||h|| > tol: with tol >= 1 the
+    loop body never runs, so x_out = x, iterations 0, residual 1, and fail := ||h|| >= tol
+    (status 1 for tol = 1, 0 for tol = 2)."""
+    L = 2
+    s = system_from_terms(1, 1, L, [[[(0, 2)], []]], limbs_from_values([1, -4], L))
+    h = phc.System(s)
+    X = torch.from_numpy(limbs_from_values([1.0], L)[None].copy()).cuda()
+    for tol, want in ((1.0, 1), (2.0, 0)):
+        Xo, res, its, st = h.newton_solve(X, tol, 5)
+        torch.cuda.synchronize()
+        assert torch.equal(Xo, X) and int(its[0]) == 0 and float(res[0]) == 1.0 and int(st[0]) == want, tol
+
+
+def _nan_f_finite_j_system(L):
+    """f(x) = x^3 - x^3 + x at x = 1e103: x^3 overflows in the evaluation (F = NaN), while
+    J = 3x^2 - 3x^2 + 1 = 1 stays finite."""
+    s = system_from_terms(1, 1, L, [[[(0, 3)], [(0, 3)], [(0, 1)]]], limbs_from_values([1, -1, 1], L))
+    X = limbs_from_values([1e103], L)[None].copy()
+    return s, X
+
+
+@pytest.mark.parametrize("regime", ["warp", "cta", "multi", "coop"])
+@pytest.mark.parametrize("L", [2, 4])
+def test_newton_nan_residual_is_reported(phc, monkeypatch, regime, L):
+    """A NaN in F with a finite J reaches the residual (not dropped by a max reduction) in every
+    elimination regime, and Alg. 2 to tolerance reports the point as failed (status 1)."""
+    env = {"warp": {"PHC_NEWTON_WARP": "1"}, "cta": {"PHC_NEWTON_WARP": "0"},
+           "multi": {"PHC_NEWTON_GLOBAL": "1", "PHC_NEWTON_COOP": "0"},
+           "coop": {"PHC_NEWTON_GLOBAL": "1", "PHC_NEWTON_COOP": "1"}}[regime]
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    s, X = _nan_f_finite_j_system(L)
+    h = phc.System(s)
+    Xd = torch.from_numpy(X).cuda()
+    F, J = h.eval_batch(Xd)
+    torch.cuda.synchronize()
+    assert torch.isnan(F).any() and bool(torch.isfinite(J).all())
+    Xn, res, status = h.newton_step(Xd)
+    torch.cuda.synchronize()
+    assert math.isnan(float(res[0])) and int(status[0]) == 0
+    Xo, res, its, st = h.newton_solve(Xd, 1e-20, 4)
+    torch.cuda.synchronize()
+    assert int(st[0]) == 1 and int(its[0]) == 1 and math.isnan(float(res[0]))
+
+
+def test_cooperative_elimination_singular_middle_column_repeated(phc, monkeypatch):
+    """Cooperative path, zero pivot in a MIDDLE column (variable 30 of 60 absent): CTA 0 finds it
+    in the look-ahead of iteration 29 while the other CTAs start that iteration; the per-column
+    flag slots keep every CTA on the same grid barrier count.  Repeated to give the race a
+    chance; every call ends (no hang) with status 1 and x unchanged."""
+    from synthetic import random_system
+    s, X = random_system(60, 6, 5, 2, 4, seed=14, points=2)
+    keep = s.var_idx != 30
+    counts = np.add.reduceat(keep.astype(np.int64), s.term_ptr[:-1])
+    counts[np.diff(s.term_ptr) == 0] = 0
+    s.term_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    s.var_idx, s.exponent = s.var_idx[keep].copy(), s.exponent[keep].copy()
+    monkeypatch.setenv("PHC_NEWTON_GLOBAL", "1")
+    monkeypatch.setenv("PHC_NEWTON_COOP", "1")
+    h = phc.System(s)
+    Xd = torch.from_numpy(X).cuda()
+    for _ in range(25):
+        Xn, res, status = h.newton_step(Xd)
+    torch.cuda.synchronize()
+    assert (status.cpu().numpy() == 1).all() and torch.equal(Xn, Xd)
