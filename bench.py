@@ -1,49 +1,78 @@
 #!/usr/bin/env python
-"""Benchmark: complex DD/QD polynomial system + Jacobian evaluations per second on B200.
+"""Benchmark: complex DD/QD polynomial system + Jacobian evaluations per second on B200
+(BASELINE.json metric: "complex DD/QD system+Jacobian evals/sec; achieved % of B200 FP64 peak").
 
 One "step" = one pass of the whole hot path (power table, Speelpenning monomial stage,
-coefficient product, reductions: SURVEY.md §8(a) rows a1-a8) over one batch of
-synthetic points resident in HBM.  Default workload: BASELINE.json configs[3]
-("batch": n=32, m=32, k=16, D=4, complex DD, 65,536 unit-circle points per GPU).
+coefficient product, reductions, writes of F and J: SURVEY.md §8(a) rows a1-a8) over one batch
+of synthetic points resident in HBM.
+
+Default workload: BASELINE.json configs[4] "large" as its 4,096-point batch (n = m = 256,
+k = 32, D = 8, complex QD -- the paper's tracking precision), the largest
+configuration that fits one GPU.  At N = 1 the same JSON line also carries nested records for
+the large single point ("large_single": median of >= 200 calls, L2 flushed before each) and for
+the DD batch config ("batch_dd": configs[3], 65,536 points), each with its own clocks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--workload NAME] [--impl ours|reference]
 
-Multi-GPU (torchrun, one process per GPU): every rank evaluates its own 65,536-point
-batch (weak scaling, no data-path collective); the timed region is bracketed by a
-barrier + synchronize and the max over ranks is taken.  `--impl reference` times the
-CPU oracle (oracle/, exact arithmetic) on the same workload.
+Multi-GPU (SURVEY.md §8(e), strong scaling of ONE fixed batch):
+  * under torchrun (WORLD_SIZE = N, one process per GPU): rank r evaluates the contiguous
+    shard [rP/N, (r+1)P/N) of the batch through phc_eval_jacobian_batch_range and its kernels
+    store F and J straight into rank 0's buffers, mapped with CUDA IPC -- the final gather is
+    fused into the evaluation (NVLink stores), no collective on the data path; NCCL
+    point-to-point copies are the fallback when IPC is refused;
+  * without torchrun, --gpus N > 1 runs one process calling phc_eval_jacobian_batch with the
+    device list 0..N-1 (the library's own sharded call, fused peer stores).
+  Timed region: barrier + synchronize on both sides, max over ranks of the device time.
+
+`--impl reference` times the CPU oracle (oracle/, the plain definition in exact rationals or
+mpmath at 512 bits) on the same workload, a bounded sample per step.
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import statistics
 import subprocess
 import sys
 import tempfile
-import threading
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-# SURVEY.md §8(d) frozen model (paper-faithful op counts, standard DD costs)
+DEFAULT_WORKLOAD = "large_batch"
+METRIC = "complex DD/QD system+Jacobian evals/sec"
+DATA = "synthetic (seeded unit-circle systems and points, BASELINE.json recipe; DESIGN.md §5)"
+# SURVEY.md §8(d) frozen model (paper-faithful op counts, standard DD costs): reported beside
+# the executed count, not the roofline numerator
 MODEL_FLOPS = {2: dict(cm=80, ca=40), 4: dict(cm=800, ca=200)}
+# nominal FP64 peak derived from the unit counts and the clock:
+# 148 SMs x 64 FP64 FMA/clk/SM x 2 flops x 1.965 GHz (clocks.max.sm)
+SMS, FMA_PER_SM_CLK, SM_MAX_MHZ = 148, 64, 1965.0
 
 
-def parse():
+def nominal_fp64_tflops(sm_mhz=SM_MAX_MHZ):
+    return SMS * FMA_PER_SM_CLK * 2 * sm_mhz * 1e6 / 1e12
+
+
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=None, help="timed steps (default: 10, batch DD 20)")
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--workload", default="batch")
-    ap.add_argument("--points", type=int, default=None, help="override points per GPU")
+    ap.add_argument("--workload", default=DEFAULT_WORKLOAD)
+    ap.add_argument("--points", type=int, default=None, help="override the batch size")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--single-calls", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-nested", action="store_true", help="skip the nested large_single / batch_dd records")
     ap.add_argument("--no-flush", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--ref-rows", type=int, default=None, help="reference arm: rows per step (QD configs)")
+    ap.add_argument("--verify", action="store_true",
+                    help="torchrun mode: rank 0 re-evaluates the whole batch alone and checks the gathered F, J bitwise")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -53,22 +82,17 @@ def dist_env():
     return rank, world, local
 
 
-def traffic_per_launch(workload, points):
-    """roofline.traffic: DRAM bytes per launch from the committed ncu capture (profiles/traffic.json)."""
-    try:
-        t = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[workload]
-        return t["bytes_per_point"] * points
-    except (OSError, KeyError, ValueError):
-        return None
+# ---------------------------------------------------------------------------------------
+# host-side plumbing (CPU-testable with gloo: tests/test_dist.py)
+# ---------------------------------------------------------------------------------------
 
-
-def rank_seed(rank):
-    """Weak scaling: every rank evaluates its own batch of the workload, drawn with seed 1 + rank."""
-    return 1 + rank
+def shard_range(rank, world, P):
+    """The batch call's sharding rule (include/phc.h): contiguous ranges [rP/N, (r+1)P/N)."""
+    return rank * P // world, (rank + 1) * P // world
 
 
 def max_over_ranks(value, world, device=None):
-    """The timing rule: the slowest rank defines the step time (all_reduce MAX)."""
+    """The timing rule: the slowest rank defines the time (all_reduce MAX)."""
     if world <= 1:
         return float(value)
     import torch
@@ -78,9 +102,33 @@ def max_over_ranks(value, world, device=None):
     return float(t.item())
 
 
-def aggregate_value(world, points_per_rank, steps, ms_max):
-    """Whole-job throughput: the units all ranks processed / the max-over-ranks time."""
-    return world * points_per_rank * steps / (ms_max * 1e-3)
+def aggregate_value(points_total, steps, ms_max):
+    """Whole-job throughput: every point of the batch, all steps, over the max-over-ranks time."""
+    return points_total * steps / (ms_max * 1e-3)
+
+
+def share_handles(rank, world, payload):
+    """Rank 0's IPC handles (bytes) to every rank (broadcast_object_list)."""
+    import torch.distributed as dist
+    obj = [payload if rank == 0 else None]
+    if world > 1:
+        dist.broadcast_object_list(obj, src=0)
+    return obj[0]
+
+
+def gather_to_rank0(rank, world, full, shard_rows):
+    """Fallback gather without IPC: rank r sends rows [p0, p1) of `full` to rank 0 (point to
+    point; NCCL on GPUs, gloo in the CPU test).  `full` has the batch as its leading axis."""
+    import torch.distributed as dist
+    if world <= 1:
+        return
+    if rank == 0:
+        for r in range(1, world):
+            a, b = shard_rows(r)
+            dist.recv(full[a:b], src=r)
+    else:
+        a, b = shard_rows(rank)
+        dist.send(full[a:b].contiguous(), dst=0)
 
 
 def host_cores():
@@ -90,13 +138,24 @@ def host_cores():
         return os.cpu_count() or 1
 
 
-def config_dict(name, c, P, flush):
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def config_dict(name, c, P, flush, parallelism):
     return {
         "workload": name,
         "n": c["n"], "m": c["m"], "k": c["k"], "D": c["D"],
         "precision": "complex DD" if c["limbs"] == 2 else "complex QD",
-        "points_per_gpu": P,
-        "l2": "flushed between timed steps (256 MiB write)" if flush else "outputs > L2",
+        "points": P,
+        "l2": "flushed before every timed step (256 MiB write)" if flush else "not flushed",
+        "parallelism": parallelism,
     }
 
 
@@ -104,7 +163,6 @@ def model_counts(s, st):
     """CM = T(6k-5) + n(D-2), CA = n(m-1) + T k - nnz(J) (paper-faithful)."""
     import numpy as np
     k = np.diff(s.term_ptr)
-    T = len(k)
     cm = int(np.sum(np.where(k >= 1, 6 * k - 5, 0))) + s.n_var * max(0, int(st["D"]) - 2)
     m = np.diff(s.poly_ptr)
     ca = int(np.sum(np.maximum(m - 1, 0))) + int(k.sum()) - int(st["nnz_J"])
@@ -117,17 +175,24 @@ def latency_regime(st, points):
     return st["latency_bound"] > 0 and points * st["n_terms"] <= st["latency_bound"]
 
 
-def exec_flops_per_point(s, st, points=None):
+def exec_flops_per_point(st, points):
     """Executed FP64 flops per point of the kernels' useful work, as counted by the library
-    (phc_system_stats out[8], or out[12] for the latency path; per-op costs from arith.cuh,
-    checked against ncu)."""
-    if points is not None and latency_regime(st, points):
+    (phc_system_stats; per-op costs from arith.cuh, checked against ncu)."""
+    if latency_regime(st, points):
         return int(st["latency_exec_flops_per_point"])
     return int(st["exec_flops_per_point"])
 
 
+def traffic_per_point(workload):
+    """DRAM bytes per point of the dominant kernel from the committed ncu capture (profiles/traffic.json)."""
+    try:
+        return json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[workload]["bytes_per_point"]
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 class ClockSampler:
-    """nvidia-smi clocks during the timed region (B200_PROFILING.md clocks line)."""
+    """nvidia-smi clocks during a timed region (B200_PROFILING.md clocks line)."""
 
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
@@ -141,7 +206,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
                                       stdout=self.f, stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.p = None
@@ -174,211 +239,503 @@ class ClockSampler:
         return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
 
 
+# ---------------------------------------------------------------------------------------
+# reference arm: the CPU oracle as it stands
+# ---------------------------------------------------------------------------------------
+
+def sample_rows(s, rows, terms_per_row):
+    """A bounded sample of the workload for the oracle: the first `terms_per_row` terms of each
+    polynomial in `rows`, as a system of len(rows) polynomials over the same n_var variables
+    (the same terms, so the same work per term as the full evaluation)."""
+    import numpy as np
+    from synthetic import SystemArrays
+    tsel = []
+    for i in rows:
+        a, b = int(s.poly_ptr[i]), int(s.poly_ptr[i + 1])
+        tsel.extend(range(a, min(b, a + terms_per_row)))
+    pp = [0]
+    for i in rows:
+        a, b = int(s.poly_ptr[i]), int(s.poly_ptr[i + 1])
+        pp.append(pp[-1] + min(b - a, terms_per_row))
+    tp = [0]
+    vi, ex = [], []
+    for t in tsel:
+        a, b = int(s.term_ptr[t]), int(s.term_ptr[t + 1])
+        vi.extend(s.var_idx[a:b].tolist())
+        ex.extend(s.exponent[a:b].tolist())
+        tp.append(len(vi))
+    return SystemArrays(n_eq=len(rows), n_var=s.n_var, limbs=s.limbs, poly_ptr=np.array(pp, np.int64),
+                        term_ptr=np.array(tp, np.int64), var_idx=np.array(vi, np.int32),
+                        exponent=np.array(ex, np.int32), coeff=np.ascontiguousarray(s.coeff[tsel])), len(tsel)
+
+
 def run_reference(args):
-    """--impl reference: the CPU oracle (exact arithmetic, all host cores over rows), as it stands."""
+    """--impl reference: the oracle (naive evaluator; exact rationals for the DD configs and c3,
+    mpmath 512 bits for the large QD config) on the host cores, a bounded sample per step: one
+    whole point for n <= 64; for the large config `cores` polynomials x 32 of their terms (one
+    polynomial per process), the value scaled by the fraction of the point's terms evaluated."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    from oracle import evaluate_system
+    from oracle import evaluate_rows
     from synthetic import CONFIGS, config_system
     c = CONFIGS[args.workload]
-    s, X = config_system(args.workload, seed=1, points=max(args.steps + args.warmup, 1))
-    arith = "exact" if c["limbs"] == 2 or c["n"] <= 64 else "mp"
+    npts = max(args.steps_eff + args.warmup, 1)
+    s, X = config_system(args.workload, seed=1, points=min(npts, c["points"]))
+    small = c["n"] <= 64
+    arith = "exact" if small else "mp"
     cores = host_cores()
+    tpr = 32
+    nrows = min(args.ref_rows or cores, s.n_eq)
+
+    def one(i):
+        if small:
+            evaluate_rows(s, X[i % X.shape[0]], None, arith)
+            return 1.0
+        rows = [(i * nrows + r) % s.n_eq for r in range(nrows)]
+        sub, nt = sample_rows(s, rows, tpr)
+        evaluate_rows(sub, X[i % X.shape[0]], None, arith)
+        return nt / s.n_terms
+
     for w in range(args.warmup):
-        evaluate_system(s, X[w % X.shape[0]], arith)
+        one(w)
     t = 0.0
-    for i in range(args.steps):
+    work = 0.0
+    for i in range(args.steps_eff):
         t0 = time.perf_counter()
-        evaluate_system(s, X[(args.warmup + i) % X.shape[0]], arith)
+        work += one(args.warmup + i)
         t += time.perf_counter() - t0
-    v = args.steps / t
+    v = work / t
+    sample = (f"each step = one full point ({arith} arithmetic, rows over {cores} processes)" if small else
+              f"each step = {tpr} terms of each of {nrows} polynomials of one point ({nrows * tpr} of "
+              f"{s.n_terms} terms, full Jacobian rows; mpmath 512 bits, one polynomial per process on "
+              f"{cores} processes); evals/s = evaluated fraction of the point / time")
     out = {
-        "metric": "complex DD/QD system+Jacobian evals/sec", "value": v, "unit": "evals/s", "impl": "reference",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (seeded unit-circle systems and points, BASELINE.json recipe)",
-        "config": dict(config_dict(args.workload, c, c["points"], False),
-                       sample=f"each step = 1 point of the workload (oracle, {arith} arithmetic)"),
-        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                         "sample": f"1 point per step, {args.steps} steps, {arith} arithmetic, rows over {cores} processes"},
+        "metric": METRIC, "value": v, "unit": "evals/s", "impl": "reference",
+        "n_gpus": args.gpus, "steps": args.steps_eff, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps_eff,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64 (exact / mp512 oracle)",
+        "data": DATA,
+        "config": config_dict(args.workload, c, c["points"], False, "host cores (oracle)"),
+        "cpu_baseline": {"value": v, "unit": "evals/s", "cores": cores, "cpu": cpu_model(), "kind": "oracle",
+                         "sample": sample},
         "e2e": {"value": v, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
     print(json.dumps(out), flush=True)
 
 
-def cpu_baseline(workload, budget_s=15.0):
-    """The oracle timed on this host's cores on a bounded sample (rank 0, N=1 only)."""
-    from oracle import evaluate_rows
-    from synthetic import CONFIGS, config_system
-    c = CONFIGS[workload]
-    s, X = config_system(workload, seed=1, points=min(c["points"], 64))
-    cores = host_cores()
-    arith = "exact" if c["limbs"] == 2 or c["n"] <= 64 else "mp"
-    if c["n"] <= 64:
-        t0 = time.perf_counter()
-        npts = 0
-        while time.perf_counter() - t0 < budget_s and npts < X.shape[0]:
-            evaluate_rows(s, X[npts], None, arith)
-            npts += 1
-        dt = time.perf_counter() - t0
-        return {"value": npts / dt, "unit": "evals/s", "cores": cores, "kind": "oracle",
-                "sample": f"{npts} full points of '{workload}' ({arith} arithmetic, rows over {cores} processes) in {dt:.1f} s"}
-    rows = list(range(min(cores, s.n_eq)))
-    t0 = time.perf_counter()
-    evaluate_rows(s, X[0], rows, arith)
-    dt = time.perf_counter() - t0
-    per_point = dt * s.n_eq / len(rows)
-    return {"value": 1.0 / per_point, "unit": "evals/s", "cores": cores, "kind": "oracle",
-            "sample": f"{len(rows)} of {s.n_eq} rows of one point ({arith}, 512 bits) in {dt:.1f} s, extrapolated to a full point"}
+def cpu_baseline(workload, steps=2):
+    """The oracle timed on this host's cores on a bounded sample (rank 0, N = 1 only): the
+    reference arm itself, run in a fresh subprocess (its process pool then forks from a
+    process without CUDA state, so the figure equals the --impl reference arm's)."""
+    cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--workload", workload,
+           "--steps", str(steps), "--warmup", "0"]
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    r = subprocess.run(cmd, capture_output=True, text=True, env=env, timeout=900)
+    for line in r.stdout.splitlines()[::-1]:
+        if line.startswith("{"):
+            cb = json.loads(line)["cpu_baseline"]
+            cb["sample"] = f"{steps} steps of the reference arm: " + cb["sample"]
+            return cb
+    return {"value": None, "unit": "evals/s", "cores": host_cores(), "kind": "oracle",
+            "sample": f"reference arm failed: {r.stderr[-300:]}"}
 
 
-def main():
-    args = parse()
-    if args.impl == "reference":
-        run_reference(args)
-        return
-    import numpy as np
+# ---------------------------------------------------------------------------------------
+# GPU measurements
+# ---------------------------------------------------------------------------------------
+
+def roofline(exec_pp, points_per_launch, ms_per_launch, peak_run, workload, kernel):
+    achieved = exec_pp * points_per_launch / (ms_per_launch * 1e-3) / 1e12 if ms_per_launch > 0 else 0.0
+    nominal = nominal_fp64_tflops()
+    tpp = traffic_per_point(workload)
+    return {
+        "bound": "alu",
+        "kernel": kernel,
+        "achieved": achieved,
+        "peak": nominal,
+        "unit": "TFLOP/s",
+        "frac": achieved / nominal,
+        "traffic": tpp * points_per_launch if tpp else None,
+        "peak_source": (f"nominal FP64: {SMS} SMs x {FMA_PER_SM_CLK} FMA/clk x 2 x {SM_MAX_MHZ:.0f} MHz "
+                        "(DESIGN.md §4; MEASURED_PEAKS.json has no FP64 entry)"),
+        "peak_measured_in_run": peak_run,
+        "frac_of_measured": achieved / peak_run if peak_run else None,
+        "peak_measured_source": "phc_fp64_peak: independent DFMA chains on this GPU in this run",
+        "flops": "executed FP64 flops (DADD = DMUL = 1, DFMA = 2) of the kernel's useful work per launch",
+        "traffic_source": "profiles/traffic.json (ncu --set full: dram read+write bytes per point x points)",
+    }
+
+
+def measure_batch(phc, h, Xd, F, J, steps, warmup, stream, scrub, local, devices=None):
+    """Per-step CUDA-event times of eval_batch (after `warmup` steps), the library's per-class
+    kernel times over the timed region, and the clocks during it."""
     import torch
-    import torch.distributed as dist
+    for _ in range(max(warmup, 0)):
+        h.eval_batch(Xd, F, J, devices=devices, stream=stream)
+    torch.cuda.synchronize()
+    phc.phc_profile_enable(h._h, True)
+    phc.phc_profile_read(h._h, reset=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for i in range(steps):
+            if scrub is not None:
+                scrub.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            h.eval_batch(Xd, F, J, devices=devices, stream=stream)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    kms, kn = phc.phc_profile_read(h._h, reset=True)
+    phc.phc_profile_enable(h._h, False)
+    return [a.elapsed_time(b) for a, b in ev], kms, kn, clk.summary()
 
+
+def measure_e2e(h, X, steps, devices=None):
+    """End to end through the host-pointer C-ABI call (phc_eval_jacobian_batch_host): pinned
+    host X in, pinned host F and J out, H2D + evaluation + D2H inside the timed region."""
+    import torch
+    P = X.shape[0]
+    Xh = torch.from_numpy(X).pin_memory()
+    Fh = torch.empty((P, h.n_eq, 2, h.limbs), dtype=torch.float64).pin_memory()
+    Jh = torch.empty((P, h.n_eq, h.n_var, 2, h.limbs), dtype=torch.float64).pin_memory()
+    h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy(), devices=devices)  # warm-up (allocates staging)
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy(), devices=devices)
+    dt = time.perf_counter() - t0
+    bi, bo = Xh.numel() * 8, (Fh.numel() + Jh.numel()) * 8
+    del Xh, Fh, Jh
+    return dt, bi, bo
+
+
+def measure_single(phc, h, x, calls, local, flush=True):
+    """Single-point latency: `calls` timed calls of phc_eval_jacobian (after 10 warm-ups), each
+    preceded by an L2 flush (256 MiB write) and bracketed by its own CUDA events; median."""
+    import torch
+    dev = x.device
+    f = torch.empty((h.n_eq, 2, h.limbs), dtype=torch.float64, device=dev)
+    j = torch.empty((h.n_eq, h.n_var, 2, h.limbs), dtype=torch.float64, device=dev)
+    scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    stream = torch.cuda.current_stream(dev)
+    for _ in range(10):
+        h.eval(x, f, j, stream=stream)
+    torch.cuda.synchronize()
+    phc.phc_profile_enable(h._h, True)
+    phc.phc_profile_read(h._h, reset=True)
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(calls)]
+    with ClockSampler(local) as clk:
+        for i in range(calls):
+            if scrub is not None:
+                scrub.fill_(i & 0xFF)
+            ev[i][0].record(stream)
+            h.eval(x, f, j, stream=stream)
+            ev[i][1].record(stream)
+        torch.cuda.synchronize()
+    _, kn = phc.phc_profile_read(h._h, reset=True)
+    phc.phc_profile_enable(h._h, False)
+    us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
+    return us, clk.summary(), int(sum(kn))
+
+
+def build_workload(workload, P, device):
     import paper_1109_0545_b200 as phc
     from synthetic import CONFIGS, config_system
+    c = CONFIGS[workload]
+    P = P or c["points"]
+    s, X = config_system(workload, seed=1, points=P)
+    return c, s, X, phc.System(s, device=device)
 
-    rank, world, local = dist_env()
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
+
+def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_run, devices=None, label=None,
+                 built=None):
+    """One batch workload on this process's device(s): the throughput line fields."""
+    import torch
     dev = torch.device("cuda", local)
-    c = CONFIGS[args.workload]
-    P = args.points or c["points"]
-    s, X = config_system(args.workload, seed=rank_seed(rank), points=P)
-    h = phc.System(s, device=local)
+    c, s, X, h = built or build_workload(workload, P, local)
+    P = X.shape[0]
     st = h.stats
     Xd = torch.from_numpy(X).to(dev)
     F = torch.empty((P, s.n_eq, 2, s.limbs), dtype=torch.float64, device=dev)
     J = torch.empty((P, s.n_eq, s.n_var, 2, s.limbs), dtype=torch.float64, device=dev)
     stream = torch.cuda.current_stream(dev)
+    scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
+    ms_list, kms, kn, clocks = measure_batch(phc, h, Xd, F, J, steps, warmup, stream, scrub, local, devices)
+    ms = sum(ms_list)
+    ok = bool(torch.isfinite(F).all().item()) and bool(torch.isfinite(J).all().item())
+    del Xd, F, J, scrub
+    torch.cuda.empty_cache()
+    e2e_s, bi, bo = measure_e2e(h, X, e2e_steps, devices)
+    cm_model, ca_model = model_counts(s, st)
+    mf = MODEL_FLOPS[s.limbs]
+    model_pp = cm_model * mf["cm"] + ca_model * mf["ca"]
+    exec_pp = exec_flops_per_point(st, P)
+    names = ["power_table", "term", "reduce", "poly_scan" if latency_regime(st, P) else "fused_block"]
+    dom = max(range(4), key=lambda i: kms[i])
+    dom_ms = kms[dom] / max(kn[dom], 1)
+    launches_dom_per_step = max(kn[dom] / steps, 1)
+    kernel = {3: f"block_kernel<{s.limbs},{st['K']},{st['layout']},0>" if not latency_regime(st, P)
+              else f"poly_scan_kernel<{s.limbs}>"}.get(dom, names[dom])
+    step_s = ms / steps * 1e-3
+    multi = devices is not None and len(devices) > 1
+    rl = roofline(exec_pp, P / launches_dom_per_step, dom_ms, peak_run, workload, kernel)
+    if multi:
+        rl["note"] = "kernel time of the home device's shard only; the step time covers every device"
+    rec = {
+        "value": aggregate_value(P, steps, ms),
+        "ms_per_step": ms / steps,
+        "ms_per_step_median": statistics.median(ms_list),
+        "config": config_dict(workload, c, P, flush,
+                              f"points sharded over devices {list(devices)} (one process)" if multi else "one GPU"),
+        "path": "latency (one warp per term)" if latency_regime(st, P) else "batch kernels",
+        "roofline": rl,
+        "fp64": {
+            "step_exec_tflops": exec_pp * P / step_s / 1e12,
+            "step_exec_frac": exec_pp * P / step_s / 1e12 / nominal_fp64_tflops(),
+            "step_model_tflops": model_pp * P / step_s / 1e12,
+            "model": "SURVEY.md §8(d): CM=T(6k-5)+n(D-2), CA=n(m-1)+Tk-nnz(J); DD 80/40, QD 800/200 flops per op",
+            "exec_flops_per_point": exec_pp,
+            "model_flops_per_point": model_pp,
+        },
+        "kernels_ms_per_step": {names[i]: kms[i] / steps for i in range(4) if kn[i]},
+        "clocks": clocks,
+        "e2e": {
+            "value": aggregate_value(P, e2e_steps, e2e_s * 1e3),
+            "unit": "evals/s",
+            "h2d_bytes_per_step": bi,
+            "d2h_bytes_per_step": bo,
+            "api": "phc_eval_jacobian_batch_host (pinned host buffers; H2D, evaluation, D2H timed)",
+        },
+        "gpu_launches": int(sum(kn)),
+        "outputs_finite": ok,
+    }
+    if label:
+        rec["label"] = label
+    return rec, h, X
+
+
+def run_one_process(args):
+    """N = 1 (or --gpus N > 1 without torchrun: the library's device-list call)."""
+    import torch
+
+    import paper_1109_0545_b200 as phc
+    local = 0
+    torch.cuda.set_device(local)
+    ngpu = args.gpus
+    devices = None
+    if ngpu > 1:
+        have = torch.cuda.device_count()
+        if have < ngpu:
+            raise SystemExit(f"--gpus {ngpu} but only {have} CUDA device(s) visible")
+        devices = list(range(ngpu))
+    peak_run = phc.phc_fp64_peak(local, 300.0)
     flush = not args.no_flush
+    built = build_workload(args.workload, args.points, local)
+    rec, h, X = batch_record(phc, args.workload, args.points, args.steps_eff, args.warmup, flush, local,
+                             args.e2e_steps, peak_run, devices, built=built)
+    out = {"metric": METRIC, "value": rec.pop("value"), "unit": "evals/s", "n_gpus": ngpu, "steps": args.steps_eff,
+           "warmup": args.warmup, "ms_per_step": rec.pop("ms_per_step"), "higher_is_better": True,
+           "scaling": "strong" if ngpu > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": DATA}
+    out.update(rec)
+    if ngpu == 1 and not args.no_nested and args.workload == "large_batch":
+        # the large single point (the same system; point 0 of the batch), L2 flushed per call
+        x0 = torch.from_numpy(X[0]).cuda(local)
+        us, clk, nl = measure_single(phc, h, x0, args.single_calls, local, flush=True)
+        st = h.stats
+        exec_pp = exec_flops_per_point(st, 1)
+        med = statistics.median(us)
+        tf = exec_pp / (med * 1e-6) / 1e12
+        out["large_single"] = {
+            "config": "BASELINE.json configs[4] large, single point (phc_eval_jacobian), point 0 of the batch",
+            "us_median": med, "us_p10": us[len(us) // 10], "us_p90": us[(9 * len(us)) // 10],
+            "calls": len(us), "evals_per_s": 1e6 / med, "l2": "flushed before every call (256 MiB write)",
+            "exec_flops_per_point": exec_pp, "exec_tflops": tf,
+            "frac": tf / nominal_fp64_tflops(), "frac_of_measured": tf / peak_run, "clocks": clk,
+            "gpu_launches": nl,
+        }
+        del x0
+    if ngpu == 1 and not args.no_nested and args.workload != "batch":
+        del h
+        torch.cuda.empty_cache()
+        rb, hb, _ = batch_record(phc, "batch", None, max(args.steps_eff, 10), max(args.warmup, 3), flush, local,
+                                 args.e2e_steps, peak_run, label="BASELINE.json configs[3] batch, complex DD")
+        out["batch_dd"] = rb
+    if ngpu == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(args.workload)
+    print(json.dumps(out), flush=True)
+
+
+def run_multiprocess(args):
+    """torchrun, one process per GPU: rank r evaluates its shard of ONE batch (strong scaling)
+    and its kernels store F, J into rank 0's buffers (CUDA IPC mapping, fused gather)."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_1109_0545_b200 as phc
+    rank, world, local = dist_env()
+    ndev = torch.cuda.device_count()
+    local = local % max(ndev, 1)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    dist.init_process_group("nccl", device_id=dev)
+    flush = not args.no_flush
+    c, s, X, h = build_workload(args.workload, args.points, local)
+    P = X.shape[0]
+    st = h.stats
+    p0, p1 = shard_range(rank, world, P)
+    Xd = torch.from_numpy(X).to(dev)  # inputs resident in HBM before the timed region
+    F = J = None
+    if rank == 0:
+        F = torch.empty((P, s.n_eq, 2, s.limbs), dtype=torch.float64, device=dev)
+        J = torch.empty((P, s.n_eq, s.n_var, 2, s.limbs), dtype=torch.float64, device=dev)
+    # rank 0 exports its F and J; every other rank maps them
+    gather = "fused NVLink stores into rank 0's IPC-mapped F/J"
+    payload = None
+    if rank == 0:
+        try:
+            payload = [phc.phc_ipc_get_handle(F.data_ptr()), phc.phc_ipc_get_handle(J.data_ptr())]
+        except Exception as e:  # noqa: BLE001
+            payload = ("error", str(e))
+    payload = share_handles(rank, world, payload)
+    fptr = jptr = None
+    bases = []
+    if rank == 0:
+        fptr, jptr = F.data_ptr(), J.data_ptr()
+    if isinstance(payload, tuple):
+        gather = f"NCCL point-to-point copies to rank 0 (IPC refused: {payload[1][:120]})"
+    elif rank != 0:
+        try:
+            for (hnd, off) in payload:
+                base = phc.phc_ipc_open(hnd, local)
+                bases.append(base)
+            fptr, jptr = bases[0] + payload[0][1], bases[1] + payload[1][1]
+        except Exception as e:  # noqa: BLE001
+            gather = f"NCCL point-to-point copies to rank 0 (IPC open failed: {str(e)[:120]})"
+    ok_flags = torch.tensor([1 if (fptr is not None or rank == 0) else 0], device=dev)
+    dist.all_reduce(ok_flags, op=dist.ReduceOp.MIN)
+    use_ipc = bool(ok_flags.item()) and not gather.startswith("NCCL")
+    if not use_ipc:
+        gather = gather if gather.startswith("NCCL") else "NCCL point-to-point copies to rank 0"
+        if rank != 0:
+            F = torch.empty((P, s.n_eq, 2, s.limbs), dtype=torch.float64, device=dev)
+            J = torch.empty((P, s.n_eq, s.n_var, 2, s.limbs), dtype=torch.float64, device=dev)
+        fptr, jptr = F.data_ptr(), J.data_ptr()
+    stream = torch.cuda.current_stream(dev)
     scrub = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if flush else None
 
-    peak_now = phc.phc_fp64_peak(local, 300.0)
+    def step():
+        h.eval_batch_range(Xd, p0, p1, fptr, jptr, stream=stream)
+        if not use_ipc:
+            gather_to_rank0(rank, world, F, lambda r: shard_range(r, world, P))
+            gather_to_rank0(rank, world, J, lambda r: shard_range(r, world, P))
 
     for _ in range(max(args.warmup, 0)):
-        h.eval_batch(Xd, F, J, stream=stream)
+        step()
     torch.cuda.synchronize()
+    dist.barrier()
     phc.phc_profile_enable(h._h, True)
     phc.phc_profile_read(h._h, reset=True)
-
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    if world > 1:
-        dist.barrier()
+    steps = args.steps_eff
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+    dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            if flush:
+        for i in range(steps):
+            if scrub is not None:
                 scrub.fill_(i & 0xFF)
             ev[i][0].record(stream)
-            h.eval_batch(Xd, F, J, stream=stream)
+            step()
             ev[i][1].record(stream)
         torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize()
-    ms = sum(a.elapsed_time(b) for a, b in ev)
+    ms_local = sum(a.elapsed_time(b) for a, b in ev)
     kms, kn = phc.phc_profile_read(h._h, reset=True)
     phc.phc_profile_enable(h._h, False)
-    ms = max_over_ranks(ms, world, dev)
+    ms = max_over_ranks(ms_local, world, dev)
+    kernel_ms = max_over_ranks(kms[3] / steps, world, dev)
+    launches = int(max_over_ranks(sum(kn), world, dev)) * world
     clocks = clk.summary()
-
-    # end to end through the C-ABI host call: pinned host buffers, H2D + eval + D2H every step
-    Xh = torch.from_numpy(X).pin_memory()
-    Fh = torch.empty((P, s.n_eq, 2, s.limbs), dtype=torch.float64).pin_memory()
-    Jh = torch.empty((P, s.n_eq, s.n_var, 2, s.limbs), dtype=torch.float64).pin_memory()
-    h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy())  # warm-up (allocates staging)
-    if world > 1:
-        dist.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        h.eval_batch_host(Xh.numpy(), Fh.numpy(), Jh.numpy())
-    e2e_s = time.perf_counter() - t0
-    e2e_s = max_over_ranks(e2e_s, world, dev)
-    ok = bool(torch.isfinite(F).all().item()) and bool(torch.isfinite(J).all().item())
-
+    # end to end: each rank copies its shard of X from pinned host memory, evaluates it into
+    # rank 0's buffers, and rank 0 reads F and J back to pinned host memory
+    Xh = torch.from_numpy(X[p0:p1]).pin_memory()
     if rank == 0:
-        cm_model, ca_model = model_counts(s, st)
-        mf = MODEL_FLOPS[s.limbs]
-        model_flops_pp = cm_model * mf["cm"] + ca_model * mf["ca"]
-        exec_pp = exec_flops_per_point(s, st, P)
-        value = aggregate_value(world, P, args.steps, ms)
-        peak = peak_now
-        # dominant kernel (largest summed time among the classes)
-        names = ["power_table", "term", "reduce", "poly_scan" if latency_regime(st, P) else "fused_block"]
-        dom = max(range(4), key=lambda i: kms[i])
-        dom_ms = kms[dom] / max(kn[dom], 1)
-        # the dominant kernel does (nearly) all of the step's FP64 work: the fused block
-        # kernel all of it, the generic term kernel all but the power table and sums
-        dom_flops = exec_pp * P / max(kn[dom] / args.steps, 1) if dom in (1, 3) else 0.0
-        achieved = dom_flops / (dom_ms * 1e-3) / 1e12 if dom_ms > 0 else 0.0
-        step_exec_tflops = exec_pp * P / (ms / args.steps * 1e-3) / 1e12
-        step_model_tflops = model_flops_pp * P / (ms / args.steps * 1e-3) / 1e12
-        launches = int(sum(kn))
-        bytes_in = X.nbytes
-        bytes_out = Fh.numel() * 8 + Jh.numel() * 8
+        Fh = torch.empty(tuple(F.shape), dtype=torch.float64).pin_memory()
+        Jh = torch.empty(tuple(J.shape), dtype=torch.float64).pin_memory()
+    e2e_steps = args.e2e_steps
+    torch.cuda.synchronize()
+    dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        Xd[p0:p1].copy_(Xh, non_blocking=True)
+        step()
+        torch.cuda.synchronize()
+        dist.barrier()
+        if rank == 0:
+            Fh.copy_(F, non_blocking=True)
+            Jh.copy_(J, non_blocking=True)
+            torch.cuda.synchronize()
+        dist.barrier()
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
+    ok = True
+    verified = None
+    if rank == 0:
+        ok = bool(torch.isfinite(F).all().item()) and bool(torch.isfinite(J).all().item())
+        if args.verify:
+            Fv, Jv = h.eval_batch(Xd)
+            torch.cuda.synchronize()
+            verified = bool(torch.equal(Fv, F)) and bool(torch.equal(Jv, J))
+            del Fv, Jv
+        exec_pp = exec_flops_per_point(st, P)
+        step_s = ms / steps * 1e-3
+        fj_bytes = (F.numel() + J.numel()) * 8
+        shard_pts = p1 - p0
         out = {
-            "metric": "complex DD/QD system+Jacobian evals/sec",
-            "value": value,
-            "unit": "evals/s",
-            "n_gpus": world,
-            "steps": args.steps,
-            "warmup": args.warmup,
-            "ms_per_step": ms / args.steps,
-            "higher_is_better": True,
-            "scaling": "weak",
-            "vs_baseline": None,
-            "dtype": "f64",
-            "data": "synthetic (seeded unit-circle systems and points, BASELINE.json recipe)",
-            "config": dict(config_dict(args.workload, c, P, flush), parallelism=f"dp{world} (points)",
-                           path="latency (one warp per term)" if latency_regime(st, P) else "batch kernels"),
-            "roofline": {
-                "bound": "alu",
-                "kernel": names[dom],
-                "achieved": achieved,
-                "peak": peak,
-                "unit": "TFLOP/s",
-                "frac": achieved / peak if peak else None,
-                "traffic": traffic_per_launch(args.workload, P / max(kn[dom] / args.steps, 1)),
-                "traffic_source": "profiles/traffic.json (ncu --set full, dram read+write per point x points per launch)",
-                "flops": "executed FP64 flops (DADD=DMUL=1, DFMA=2) per launch from the kernel op counts",
-                "peak_source": "phc_fp64_peak: DFMA chains measured in this run (profiles/fp64_peak_r01.jsonl: 34.2 sustained)",
+            "metric": METRIC, "value": aggregate_value(P, steps, ms), "unit": "evals/s", "n_gpus": world,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
+            "config": dict(config_dict(args.workload, c, P, flush, f"points sharded over {world} processes / GPUs"),
+                           gather=gather),
+            "roofline": roofline(exec_pp, shard_pts, kernel_ms, None, args.workload,
+                                 f"block_kernel<{s.limbs},{st['K']},{st['layout']},0>"),
+            "multi_gpu": {
+                "step_ms_max_over_ranks": ms / steps,
+                "kernel_ms_max_over_ranks": kernel_ms,
+                "gather_bytes_per_step": fj_bytes * (world - 1) // world,
+                "home_ingress_gbs": fj_bytes * (world - 1) / world / step_s / 1e9,
+                "home_ingress_reference_gbs": 770.0,
+                "shard_points": [shard_range(r, world, P) for r in range(world)],
             },
-            "fp64": {
-                "step_exec_tflops": step_exec_tflops,
-                "step_exec_frac": step_exec_tflops / peak,
-                "step_model_tflops": step_model_tflops,
-                "step_model_frac": step_model_tflops / peak,
-                "model": "SURVEY.md §8(d): CM=T(6k-5)+n(D-2), CA=n(m-1)+Tk-nnz(J); DD 80/40, QD 800/200 flops",
-                "exec_flops_per_point": exec_pp,
-                "model_flops_per_point": model_flops_pp,
-            },
-            "kernels_ms_per_step": {names[i]: kms[i] / args.steps for i in range(4) if kn[i]},
+            "fp64": {"step_exec_tflops": exec_pp * P / step_s / 1e12,
+                     "step_exec_frac_of_n_gpus_nominal": exec_pp * P / step_s / 1e12 / (world * nominal_fp64_tflops())},
             "clocks": clocks,
-            "e2e": {
-                "value": aggregate_value(world, P, args.e2e_steps, e2e_s * 1e3),
-                "unit": "evals/s",
-                "h2d_bytes_per_step": bytes_in,
-                "d2h_bytes_per_step": bytes_out,
-                "api": "phc_eval_jacobian_batch_host (pinned host buffers)",
-            },
+            "e2e": {"value": aggregate_value(P, e2e_steps, e2e_s * 1e3), "unit": "evals/s",
+                    "h2d_bytes_per_step": X.nbytes, "d2h_bytes_per_step": fj_bytes,
+                    "api": "per rank: H2D of its shard of X, phc_eval_jacobian_batch_range into rank 0's F/J; "
+                           "rank 0: D2H of F and J (pinned)"},
             "gpu_launches": launches,
             "outputs_finite": ok,
         }
-        if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline(args.workload)
+        if verified is not None:
+            out["verified_bitwise_vs_one_process"] = verified
         print(json.dumps(out), flush=True)
+    dist.barrier()
+    for b in bases:
+        phc.phc_ipc_close(b, local)
+    dist.destroy_process_group()
+
+
+def main(argv=None):
+    args = parse(argv)
+    args.steps_eff = args.steps if args.steps is not None else 10
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    _, world, _ = dist_env()
     if world > 1:
-        dist.destroy_process_group()
+        run_multiprocess(args)
+    else:
+        run_one_process(args)
 
 
 if __name__ == "__main__":

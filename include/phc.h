@@ -99,6 +99,32 @@ int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* j
 int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double* x, double* f, double* jac,
                             const int32_t* devices, int32_t n_devices, void* stream);
 
+/* Points [p_begin, p_end) of an n_points-point batch call, evaluated on the handle's home
+ * device and written into the FULL output arrays: x [n_points][n_var][2][L] (only rows
+ * p_begin .. p_end-1 are read), f [n_points][n_eq][2][L], jac [n_points][n_eq][n_var][2][L]
+ * (only those rows are written).  The evaluation regime is that of the whole n_points call,
+ * so the rows are bitwise those phc_eval_jacobian_batch writes for all n_points: a batch
+ * split over processes (one per GPU, BASELINE.json configs[3] "points sharded across
+ * 1/2/4/8 GPUs") gives the unsharded result.  f and jac may be peer memory
+ * of another device or process (phc_ipc_open): the kernels then store the rows straight into
+ * that device's buffers over NVLink -- the final gather fused into the evaluation.  x must be
+ * readable from the home device.  Asynchronous on `stream`; PHC_EINVAL unless
+ * 0 <= p_begin <= p_end <= n_points. */
+int phc_eval_jacobian_batch_range(const phc_system* s, int64_t n_points, int64_t p_begin, int64_t p_end,
+                                  const double* x, double* f, double* jac, void* stream);
+
+/* CUDA IPC for the multi-process gather (one process per GPU).  phc_ipc_get_handle describes
+ * the device allocation containing dev_ptr: a PHC_IPC_HANDLE_BYTES-byte handle to send to
+ * another process, and the byte offset of dev_ptr inside that allocation.  phc_ipc_open maps
+ * the allocation on CUDA device `device` of the calling process (peer access enabled
+ * lazily) and returns its base (add the offset); phc_ipc_close unmaps it.  The exporting
+ * process owns the memory and must keep it alive until every importer closed it.
+ * PHC_ECUDA when the runtime refuses (e.g. memory not from cudaMalloc). */
+#define PHC_IPC_HANDLE_BYTES 64
+int phc_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset);
+int phc_ipc_open(const void* handle, int32_t device, void** base);
+int phc_ipc_close(void* base, int32_t device);
+
 /* End-to-end convenience: x, f, jac are HOST pointers (pinned or pageable); copies in,
  * evaluates n_points points on the home device (or sharded as above) and copies out.
  * On one device the call is a pipeline over chunks of points: the output copies of chunk c

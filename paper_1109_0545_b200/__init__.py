@@ -13,6 +13,10 @@ from ._lib import (  # noqa: F401
     phc_eval_jacobian,
     phc_eval_jacobian_batch,
     phc_eval_jacobian_batch_host,
+    phc_eval_jacobian_batch_range,
+    phc_ipc_get_handle,
+    phc_ipc_open,
+    phc_ipc_close,
     phc_fp64_peak,
     phc_last_error,
     phc_newton_step_batch,

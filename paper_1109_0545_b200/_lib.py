@@ -26,6 +26,10 @@ EXPORTED = (
     "phc_eval_jacobian",
     "phc_eval_jacobian_batch",
     "phc_eval_jacobian_batch_host",
+    "phc_eval_jacobian_batch_range",
+    "phc_ipc_get_handle",
+    "phc_ipc_open",
+    "phc_ipc_close",
     "phc_newton_step_batch",
     "phc_system_set_target",
     "phc_system_create_common",
@@ -77,6 +81,14 @@ def _load():
     lib.phc_eval_jacobian_batch.restype = ctypes.c_int
     lib.phc_eval_jacobian_batch_host.argtypes = [P, i64, P, P, P, P, i32]
     lib.phc_eval_jacobian_batch_host.restype = ctypes.c_int
+    lib.phc_eval_jacobian_batch_range.argtypes = [P, i64, i64, i64, P, P, P, P]
+    lib.phc_eval_jacobian_batch_range.restype = ctypes.c_int
+    lib.phc_ipc_get_handle.argtypes = [P, P, ctypes.POINTER(i64)]
+    lib.phc_ipc_get_handle.restype = ctypes.c_int
+    lib.phc_ipc_open.argtypes = [P, i32, ctypes.POINTER(P)]
+    lib.phc_ipc_open.restype = ctypes.c_int
+    lib.phc_ipc_close.argtypes = [P, i32]
+    lib.phc_ipc_close.restype = ctypes.c_int
     lib.phc_newton_step_batch.argtypes = [P, i64, P, P, P, P, P]
     lib.phc_newton_step_batch.restype = ctypes.c_int
     lib.phc_system_create_common.argtypes = [ctypes.POINTER(P), i32, i32, i32, i64, P, P, P, P, i32]
@@ -144,6 +156,35 @@ def phc_eval_jacobian_batch(h, n_points, x, f, jac, devices, n_devices, stream):
 
 def phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices):
     return check(lib.phc_eval_jacobian_batch_host(h, n_points, x, f, jac, devices, n_devices))
+
+
+def phc_eval_jacobian_batch_range(h, n_points, p_begin, p_end, x, f, jac, stream):
+    return check(lib.phc_eval_jacobian_batch_range(h, n_points, p_begin, p_end, x, f, jac, stream))
+
+
+PHC_IPC_HANDLE_BYTES = 64
+
+
+def phc_ipc_get_handle(dev_ptr):
+    """-> (handle bytes, offset of dev_ptr inside its allocation)"""
+    buf = ctypes.create_string_buffer(PHC_IPC_HANDLE_BYTES)
+    off = ctypes.c_int64()
+    check(lib.phc_ipc_get_handle(dev_ptr, buf, ctypes.byref(off)))
+    return buf.raw, off.value
+
+
+def phc_ipc_open(handle, device):
+    """-> base device pointer (int) of the exported allocation, mapped on `device`"""
+    if len(handle) != PHC_IPC_HANDLE_BYTES:
+        raise ValueError(f"IPC handle must be {PHC_IPC_HANDLE_BYTES} bytes")
+    base = ctypes.c_void_p()
+    check(lib.phc_ipc_open(ctypes.create_string_buffer(bytes(handle), PHC_IPC_HANDLE_BYTES), device,
+                           ctypes.byref(base)))
+    return base.value
+
+
+def phc_ipc_close(base, device):
+    return check(lib.phc_ipc_close(base, device))
 
 
 def phc_newton_step_batch(h, n_points, x, x_new, residual, status, stream):

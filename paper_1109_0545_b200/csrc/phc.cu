@@ -703,6 +703,70 @@ int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double*
   return eval_batch_impl(s, n_points, x, nullptr, f, jac, devices, n_devices, stream);
 }
 
+int phc_eval_jacobian_batch_range(const phc_system* cs, int64_t n_points, int64_t p_begin, int64_t p_end,
+                                  const double* x, double* f, double* jac, void* stream) {
+  g_err.clear();
+  phc_system* s = const_cast<phc_system*>(cs);
+  if (!s) return fail(PHC_EINVAL, "NULL system");
+  if (n_points < 0 || p_begin < 0 || p_end < p_begin || p_end > n_points)
+    return fail(PHC_EINVAL, "need 0 <= p_begin <= p_end <= n_points (got %lld, %lld, %lld)", (long long)p_begin,
+                (long long)p_end, (long long)n_points);
+  if (p_end == p_begin) return PHC_OK;
+  if (!x || !f || !jac) return fail(PHC_EINVAL, "NULL x/f/jac");
+  if ((((uintptr_t)x) | ((uintptr_t)f) | ((uintptr_t)jac)) & 31) return fail(PHC_EINVAL, "x/f/jac must be 32-byte aligned");
+  const int64_t cd = 2 * s->L;
+  DeviceGuard g(s->home);
+  DeviceState* d;
+  int rc = get_device_state(s, s->home, &d);
+  if (rc) return rc;
+  // call_points = n_points: the regime of the whole call, so the rows are bitwise those of
+  // phc_eval_jacobian_batch over all n_points (determinism, phc.h)
+  return run_on_device(s, d, p_end - p_begin, x + p_begin * s->n_var * cd, nullptr, f + p_begin * s->n_eq * cd,
+                       jac + p_begin * (int64_t)s->n_eq * s->n_var * cd, (cudaStream_t)stream, n_points);
+}
+
+// cuMemGetAddressRange through the runtime's driver entry point (no link-time libcuda, so the
+// library still loads on hosts without a driver)
+typedef int (*phc_get_range_fn)(unsigned long long*, size_t*, unsigned long long);
+
+int phc_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset) {
+  g_err.clear();
+  if (!dev_ptr || !handle || !offset) return fail(PHC_EINVAL, "NULL argument");
+  static phc_get_range_fn range = [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (phc_get_range_fn)fn;
+  }();
+  if (!range) return fail(PHC_ECUDA, "cuMemGetAddressRange not available");
+  unsigned long long base = 0;
+  size_t size = 0;
+  if (range(&base, &size, (unsigned long long)(uintptr_t)dev_ptr) != 0) return fail(PHC_EINVAL, "not a device allocation");
+  CUDA_TRY(cudaIpcGetMemHandle(reinterpret_cast<cudaIpcMemHandle_t*>(handle), (void*)(uintptr_t)base));
+  *offset = (int64_t)((uintptr_t)dev_ptr - (uintptr_t)base);
+  return PHC_OK;
+}
+
+int phc_ipc_open(const void* handle, int32_t device, void** base) {
+  g_err.clear();
+  if (!handle || !base) return fail(PHC_EINVAL, "NULL argument");
+  DeviceGuard g(device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof(h));
+  CUDA_TRY(cudaIpcOpenMemHandle(base, h, cudaIpcMemLazyEnablePeerAccess));
+  return PHC_OK;
+}
+
+int phc_ipc_close(void* base, int32_t device) {
+  g_err.clear();
+  if (!base) return PHC_OK;
+  DeviceGuard g(device);
+  CUDA_TRY(cudaIpcCloseMemHandle(base));
+  return PHC_OK;
+}
+
 int phc_eval_homotopy_batch(const phc_system* s, int64_t n_points, const double* x, const double* t, double* f,
                             double* jac, const int32_t* devices, int32_t n_devices, void* stream) {
   g_err.clear();

@@ -151,6 +151,27 @@ class System:
         _lib.phc_eval_jacobian_batch(self._h, P, _ptr(X), _ptr(F), _ptr(J), dv, nd, ctypes.c_void_p(st))
         return F, J
 
+    def eval_batch_range(self, X, p_begin, p_end, F, J, stream=None):
+        """Points [p_begin, p_end) of the len(X)-point batch call (phc_eval_jacobian_batch_range):
+        X [P, n_var, 2, L] on the home device (only those rows are read); F [P, n_eq, 2, L] and
+        J [P, n_eq, n_var, 2, L] receive those rows, bitwise what eval_batch writes for all P.
+        F and J are tensors on the home device or raw device pointers (int) to such arrays,
+        e.g. another process's buffers mapped with phc_ipc_open (the gather fused into the
+        kernels' stores)."""
+        L = self.limbs
+        P = int(X.shape[0])
+        self._check(X, (P, self.n_var, 2, L))
+        ptrs = []
+        for a, shape in ((F, (P, self.n_eq, 2, L)), (J, (P, self.n_eq, self.n_var, 2, L))):
+            if isinstance(a, int):
+                ptrs.append(ctypes.c_void_p(a))
+            else:
+                self._check(a, shape)
+                ptrs.append(_ptr(a))
+        st = _stream_handle(stream, X.device)
+        _lib.phc_eval_jacobian_batch_range(self._h, P, int(p_begin), int(p_end), _ptr(X), ptrs[0], ptrs[1],
+                                           ctypes.c_void_p(st))
+
     def newton_step(self, X, X_new=None, stream=None):
         """One Newton iteration per point (NEXT-1): X [P, n, 2, L] on the home device ->
         (X_new, residual [P] float64, status [P] int32).  X_new may be X (in place)."""

@@ -5,6 +5,7 @@ reals into DD/QD limbs.  It holds none of the method's arithmetic: no
 monomial, derivative, Speelpenning or DD/QD arithmetic lives here.
 """
 from .systems import (  # noqa: F401
+    config_point_rows,
     CONFIGS,
     SystemArrays,
     config_system,

@@ -161,6 +161,22 @@ def config_system(name: str, seed: int = 1, points: int | None = None, workers=N
     return random_system(c["n"], c["m"], c["k"], c["D"], c["limbs"], seed, P, workers)
 
 
+def config_point_rows(name: str, seed: int, rows, points: int | None = None):
+    """Rows ``rows`` of the point batch ``config_system(name, seed, points)`` draws, without
+    converting the other points' angles (the same generator stream: the system's draws, then
+    the (points, n) angle matrix).  Returns float64 [len(rows)][n][2][limbs]."""
+    c = CONFIGS[name]
+    P = c["points"] if points is None else points
+    n, m, k, D, limbs = c["n"], c["m"], c["k"], c["D"], c["limbs"]
+    rng = np.random.Generator(np.random.PCG64(seed))
+    for _ in range(n * m):
+        rng.choice(n, k, replace=False)
+        rng.integers(1, D + 1, k)
+        rng.uniform(0.0, 2.0 * math.pi)
+    thetas_x = rng.uniform(0.0, 2.0 * math.pi, size=(P, n))
+    return unit_circle_limbs(thetas_x[list(rows)], limbs)
+
+
 def limbs_from_values(values, limbs: int) -> np.ndarray:
     """Exact small complex values (Python complex / int / Fraction pairs) → [..][2][limbs] limbs.
 
