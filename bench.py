@@ -435,7 +435,9 @@ def measure_single(phc, h, x, calls, local, flush=True):
     _, kn = phc.phc_profile_read(h._h, reset=True)
     phc.phc_profile_enable(h._h, False)
     us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
-    return us, clk.summary(), int(sum(kn))
+    st = h.stats
+    nl = max(int(sum(kn)), int(st["launches"]) * calls if not latency_regime(st, 1) else 0)
+    return us, clk.summary(), nl
 
 
 def build_workload(workload, P, device):
@@ -506,7 +508,9 @@ def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_
             "d2h_bytes_per_step": bo,
             "api": "phc_eval_jacobian_batch_host (pinned host buffers; H2D, evaluation, D2H timed)",
         },
-        "gpu_launches": int(sum(kn)),
+        # the profile records the block kernel; the power-table kernel of layout 0 (a
+        # programmatic dependent launch) is counted from the plan's launches per call
+        "gpu_launches": max(int(sum(kn)), int(st["launches"]) * steps if not latency_regime(st, P) else 0),
         "outputs_finite": ok,
     }
     if label:
@@ -535,7 +539,7 @@ def run_one_process(args):
                              args.e2e_steps, peak_run, devices, built=built)
     out = {"metric": METRIC, "value": rec.pop("value"), "unit": "evals/s", "n_gpus": ngpu, "steps": args.steps_eff,
            "warmup": args.warmup, "ms_per_step": rec.pop("ms_per_step"), "higher_is_better": True,
-           "scaling": "strong" if ngpu > 1 else "weak", "vs_baseline": None, "dtype": "f64", "data": DATA}
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA}
     out.update(rec)
     if ngpu == 1 and not args.no_nested and args.workload == "large_batch":
         # the large single point (the same system; point 0 of the batch), L2 flushed per call
@@ -577,7 +581,15 @@ def run_multiprocess(args):
     local = local % max(ndev, 1)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    dist.init_process_group("nccl", device_id=dev)
+    # NCCL needs one GPU per rank; ranks sharing a GPU (a test of the IPC path on a one-GPU
+    # box) use gloo for the control plane (barriers, handle broadcast, timing reductions) --
+    # the data path is the same IPC-mapped stores either way
+    backend = "nccl" if ndev >= world else "gloo"
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    cdev = dev if backend == "nccl" else None
     flush = not args.no_flush
     c, s, X, h = build_workload(args.workload, args.points, local)
     P = X.shape[0]
@@ -611,10 +623,12 @@ def run_multiprocess(args):
             fptr, jptr = bases[0] + payload[0][1], bases[1] + payload[1][1]
         except Exception as e:  # noqa: BLE001
             gather = f"NCCL point-to-point copies to rank 0 (IPC open failed: {str(e)[:120]})"
-    ok_flags = torch.tensor([1 if (fptr is not None or rank == 0) else 0], device=dev)
+    ok_flags = torch.tensor([1 if (fptr is not None or rank == 0) else 0], device=cdev)
     dist.all_reduce(ok_flags, op=dist.ReduceOp.MIN)
     use_ipc = bool(ok_flags.item()) and not gather.startswith("NCCL")
     if not use_ipc:
+        if backend != "nccl":
+            raise SystemExit(f"ranks share a GPU and IPC failed ({gather}); no NCCL fallback")
         gather = gather if gather.startswith("NCCL") else "NCCL point-to-point copies to rank 0"
         if rank != 0:
             F = torch.empty((P, s.n_eq, 2, s.limbs), dtype=torch.float64, device=dev)
@@ -652,9 +666,9 @@ def run_multiprocess(args):
     ms_local = sum(a.elapsed_time(b) for a, b in ev)
     kms, kn = phc.phc_profile_read(h._h, reset=True)
     phc.phc_profile_enable(h._h, False)
-    ms = max_over_ranks(ms_local, world, dev)
-    kernel_ms = max_over_ranks(kms[3] / steps, world, dev)
-    launches = int(max_over_ranks(sum(kn), world, dev)) * world
+    ms = max_over_ranks(ms_local, world, cdev)
+    kernel_ms = max_over_ranks(kms[3] / steps, world, cdev)
+    launches = int(max_over_ranks(st["launches"] * steps, world, cdev)) * world
     clocks = clk.summary()
     # end to end: each rank copies its shard of X from pinned host memory, evaluates it into
     # rank 0's buffers, and rank 0 reads F and J back to pinned host memory
@@ -676,7 +690,7 @@ def run_multiprocess(args):
             Jh.copy_(J, non_blocking=True)
             torch.cuda.synchronize()
         dist.barrier()
-    e2e_s = max_over_ranks(time.perf_counter() - t0, world, dev)
+    e2e_s = max_over_ranks(time.perf_counter() - t0, world, cdev)
     ok = True
     verified = None
     if rank == 0:
@@ -695,7 +709,8 @@ def run_multiprocess(args):
             "steps": steps, "warmup": args.warmup, "ms_per_step": ms / steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": DATA,
             "config": dict(config_dict(args.workload, c, P, flush, f"points sharded over {world} processes / GPUs"),
-                           gather=gather),
+                           gather=gather, control_plane=backend,
+                           gpus_visible=ndev),
             "roofline": roofline(exec_pp, shard_pts, kernel_ms, None, args.workload,
                                  f"block_kernel<{s.limbs},{st['K']},{st['layout']},0>"),
             "multi_gpu": {
