@@ -346,38 +346,6 @@ PHC_DEV qd qd_div(const qd& a, const qd& b) {
   return renorm5(q[0], q[1], q[2], q[3], q[4]);
 }
 
-// Reciprocals by Newton's iteration y <- y + y (1 - d y), which doubles the number of correct
-// bits per step (53 -> 106 -> 212), from y0 = 1 / d0 correctly rounded.  Each step forms the
-// residual 1 - d y to the precision the next step needs (1 - d0 y0 is exact: d0 y0 is within
-// an ulp of 1, so both the subtraction and the FMA error term are exact), then adds the
-// correction y (1 - d y), which only needs the relative precision already gained.
-// Relative error ~2^-104 (DD) / ~2^-208 (QD), like the long divisions, in a dependency chain
-// of ~25 instead of ~160 operations (the pivot reciprocal is on every elimination column's
-// critical path).
-PHC_DEV dd dd_recip(const dd& d) {
-  const double y0 = __ddiv_rn(1.0, d.x[0]);
-  const double p = mul_(d.x[0], y0);
-  const double pe = fma_(d.x[0], y0, -p);
-  // e0 = 1 - (d0 + d1) y0, to ~2^-106 absolute
-  const double e0 = fma_(-d.x[1], y0, sub_(sub_(1.0, p), pe));
-  dd r;
-  quick_two_sum(y0, mul_(y0, e0), r.x[0], r.x[1]);
-  return r;
-}
-PHC_DEV qd qd_recip(const qd& d) {
-  const dd y1 = dd_recip(dd_make(d.x[0], d.x[1]));  // |1 - d y1| <~ 2^-104
-  qd y;
-  y.x[0] = y1.x[0];
-  y.x[1] = y1.x[1];
-  y.x[2] = y.x[3] = 0.0;
-  // e = 1 - d y1 in full QD (the leading parts cancel exactly), then f = e + e^2: the
-  // iteration's own error y1 e^2 (~2^-208 here) is part of the correction, so
-  // y = y1 + y1 f = y1 (1 + e + e^2) leaves y1 e^3 (~2^-312)
-  qd f = qd_sub(qd_from_d(1.0), qd_mul(d, y));
-  f.x[2] = add_(f.x[2], mul_(f.x[0], f.x[0]));
-  return qd_add(y, qd_mul(y, f));
-}
-
 // ---------------------------------------------------------------------------
 // complex values, templated on the real type; Prec<L> traits below
 // ---------------------------------------------------------------------------
@@ -494,15 +462,11 @@ template <> struct Prec<2> {
   // 1 / a = conj(a) / |a|^2
   // |a|^2 (the denominator of the reciprocal)
   PHC_DEV static real abs2(const C& a) { return dd_add(dd_mul(a.re, a.re), dd_mul(a.im, a.im)); }
-  // 1 / d for a positive DD d by one Newton step from the double reciprocal (dd_recip)
-  PHC_DEV static real rrecip(const real& d) { return dd_recip(d); }
-  // 1 / a = conj(a) * (1 / |a|^2): the real reciprocal by Newton's iteration instead of two
-  // long divisions (the pivot reciprocal is the serial step of every elimination column)
   PHC_DEV static C recip(const C& a) {
-    const dd y = dd_recip(abs2(a));
+    const dd d = abs2(a);
     C r;
-    r.re = dd_mul(a.re, y);
-    r.im = dd_neg(dd_mul(a.im, y));
+    r.re = dd_div(a.re, d);
+    r.im = dd_neg(dd_div(a.im, d));
     return r;
   }
   // |a|^2 from the leading limbs (pivot selection only)
@@ -554,12 +518,11 @@ template <> struct Prec<4> {
   PHC_DEV static C neg(const C& a) { C r; r.re = qd_neg(a.re); r.im = qd_neg(a.im); return r; }
   PHC_DEV static C sub(const C& a, const C& b) { return add(a, neg(b)); }
   PHC_DEV static real abs2(const C& a) { return qd_dot2(a.re, a.re, a.im, a.im); }
-  PHC_DEV static real rrecip(const real& d) { return qd_recip(d); }
   PHC_DEV static C recip(const C& a) {
-    const qd y = qd_recip(abs2(a));
+    const qd d = abs2(a);
     C r;
-    r.re = qd_mul(a.re, y);
-    r.im = qd_neg(qd_mul(a.im, y));
+    r.re = qd_div(a.re, d);
+    r.im = qd_neg(qd_div(a.im, d));
     return r;
   }
   PHC_DEV static double abs2_hi(const C& a) { return a.re.x[0] * a.re.x[0] + a.im.x[0] * a.im.x[0]; }

@@ -31,16 +31,16 @@ __device__ __forceinline__ double nan_max(double a, double b) { return (b != b |
 
 
 // The pivot reciprocal (the serial step of every elimination column) computed by a whole
-// warp: every lane forms y = 1 / |a|^2 (Newton's iteration, P::rrecip), lane 0 the real part
-// a.re y, lane 1 the imaginary part -a.im y -- P::recip's own operations, so the value is
-// bitwise P::recip(a) -- and every lane receives the result.  The two final products run side
-// by side instead of one after the other in one thread.  Call with the full warp converged.
+// warp: lane 0 divides the real part by |a|^2, lane 1 the imaginary part -- P::recip's own
+// operations, so the value is bitwise P::recip(a) -- and every lane receives the result.  The
+// two long divisions then run side by side instead of interleaved in one thread.
+// Call with the full warp converged.
 template <int L>
 PHC_DEV typename Prec<L>::C recip_warp(const typename Prec<L>::C& a, int lane) {
   using P = Prec<L>;
   typename P::C r;
-  const typename P::real y = P::rrecip(P::abs2(a));
-  const typename P::real q = P::rmul((lane & 1) ? a.im : a.re, y);
+  const typename P::real d = P::abs2(a);
+  const typename P::real q = P::rdiv((lane & 1) ? a.im : a.re, d);
 #pragma unroll
   for (int i = 0; i < L; ++i) {
     r.re.x[i] = __shfl_sync(0xffffffffu, q.x[i], 0);
@@ -776,227 +776,6 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
     }
     grid.sync();  // perm_g, red_g and flag_g are reused by the next point
   }
-}
-
-
-// ---------------------------------------------------------------------------------------
-// Few points of a mid-size system (n beyond the warp kernel, [J | -F] up to ~half a cluster's
-// shared memory): one THREAD-BLOCK CLUSTER of CS CTAs (CS SMs) per point, [J | -F] distributed
-// over the CTAs' shared memory by columns (column j lives in CTA j % CS, local slot j / CS).
-// The single-CTA kernel runs the trailing update of all columns on one SM (c3: ~100 us of
-// FP64 work at full rate); here every CTA updates its own columns, reading the multipliers
-// of the pivot column from the owner's shared memory (distributed shared memory), and the
-// look-ahead of column k+1 -- update, pivot search, row exchange, reciprocal, multipliers --
-// runs on warp 0 of the CTA that owns column k+1, entirely on local data, while the other
-// warps of the cluster do the trailing update of step k.  One cluster barrier per column.
-// The CTA owning the right-hand side gathers U and the pivot reciprocals and back-substitutes
-// as newton_solve_kernel does.  Same pivot rule, same operations per entry in the same order
-// as the other eliminations: bitwise the same step (tested).
-// ---------------------------------------------------------------------------------------
-constexpr int kClusterThreads = 256;
-struct ClusterLayout {
-  int W;            // local column slots per CTA
-  size_t mat, mloc, inv, ug, perm, piv, bytes;  // offsets: doubles for mat..ug, bytes from perm on
-};
-__host__ __device__ inline ClusterLayout cluster_layout(int n, int L, int CS) {
-  ClusterLayout c;
-  const size_t cd = 2 * L;
-  c.W = (n + 1 + CS - 1) / CS;
-  c.mat = 0;
-  c.mloc = c.mat + (size_t)n * c.W * cd;         // [J | -F] local columns (two planes)
-  c.inv = c.mloc + (size_t)2 * n * cd;           // [2][n] multipliers of columns of each parity (by physical row)
-  c.ug = c.inv + (size_t)c.W * cd;               // reciprocals of this CTA's pivot columns
-  const size_t tri = (size_t)n * (n - 1) / 2;    // RHS owner: U above the diagonal (packed rows), b, 1/U_ii
-  const size_t perm_d = c.ug + (tri + 2 * (size_t)n) * cd;
-  c.perm = perm_d * sizeof(double);              // [2][n] permutations
-  c.piv = c.perm + (size_t)2 * n * sizeof(int);  // [n] pivot row per column, then [2] zero-column flags
-  c.bytes = c.piv + (size_t)(n + 2) * sizeof(int);
-  return c;
-}
-
-template <int L>
-__global__ void __launch_bounds__(kClusterThreads) newton_cluster_kernel(const NewtonArgs a) {
-  namespace cg = cooperative_groups;
-  using P = Prec<L>;
-  using C = typename P::C;
-  cg::cluster_group cl = cg::this_cluster();
-  const int CS = (int)cl.num_blocks();
-  const int me = (int)cl.block_rank();
-  const int64_t p = blockIdx.x / CS;
-  const int n = a.n, cols = n + 1, cd = 2 * L;
-  const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
-  const ClusterLayout lay = cluster_layout(n, L, CS);
-  const int W = lay.W;
-  extern __shared__ __align__(16) double ksm[];
-  char* base = reinterpret_cast<char*>(ksm);
-  double* Mre = ksm + lay.mat;
-  double* Mim = Mre + (size_t)n * W * L;
-  double* mloc = ksm + lay.mloc;  // [2][n][cd]: pushed by the owner of each pivot column
-  double* invd = ksm + lay.inv;
-  double* Ug = ksm + lay.ug;
-  int* perm = reinterpret_cast<int*>(base + lay.perm);  // [2][n]: after the exchange of column c: perm[c & 1]
-  int* pivs = reinterpret_cast<int*>(base + lay.piv);   // [n]: pivot row of column c (pushed by its owner)
-  int* bad = pivs + n;                                  // [2]: column c's zero-column flag at bad[c & 1]
-  auto ldE = [&](int r, int jl) { return plane_ld<L>(Mre, Mim, ((size_t)r * W + jl) * L); };
-  auto stE = [&](int r, int jl, const C& v) { plane_st<L>(Mre, Mim, ((size_t)r * W + jl) * L, v); };
-  auto owner = [&](int j) { return j % CS; };
-  const double* Fp = a.F + (size_t)p * n * cd;
-  const double* Jp = a.J + (size_t)p * n * n * cd;
-  // the local columns of [J | -F]; identity permutation in buffer 1 (the "column -1" state)
-  for (int e = tid; e < n * W; e += T) {
-    const int i = e / W, jl = e % W, j = me + CS * jl;
-    if (j < n) stE(i, jl, cload<L>(Jp + ((size_t)i * n + j) * cd));
-    else if (j == n) stE(i, jl, P::neg(cload<L>(Fp + (size_t)i * cd)));
-  }
-  for (int i = tid; i < n; i += T) perm[n + i] = i;
-  // residual max_i |F_i| (rank 0)
-  if (me == 0) {
-    __shared__ double red_v[32];
-    double rmax = 0.0;
-    for (int i = tid; i < n; i += T) rmax = nan_max(rmax, sqrt(P::abs2_hi(cload<L>(Fp + (size_t)i * cd))));
-    for (int o = 16; o; o >>= 1) rmax = nan_max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
-    if (lane == 0) red_v[wid] = rmax;
-    __syncthreads();
-    if (tid == 0) {
-      double r = 0.0;
-      for (int w = 0; w < nwarp; ++w) r = nan_max(r, red_v[w]);
-      a.resid[p] = r;
-    }
-  }
-  __syncthreads();
-  // look-ahead of column c by warp 0 of its owner: pivot among logical rows c.. of the local
-  // column (updated through step c-1), exchange into perm[c & 1] (from perm[(c-1) & 1]),
-  // reciprocal; the multipliers, the pivot row and the zero-column flag are PUSHED into every
-  // CTA's shared memory (distributed-shared-memory stores), so after the cluster barrier each
-  // CTA reads them locally.
-  auto pivot_column = [&](int c) {
-    const int jl = c / CS;
-    const int* src = perm + ((c + 1) & 1) * n;
-    int* dst = perm + (c & 1) * n;
-    double best = -1.0;
-    int bi = n;
-    for (int i = c + lane; i < n; i += 32) {
-      const double v = P::abs2_hi(ldE(src[i], jl));
-      if (v > best) { best = v; bi = i; }
-    }
-    for (int o = 16; o; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, best, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
-    }
-    const int zero = !(best > 0.0);
-    if (lane < CS) {
-      *cl.map_shared_rank(bad + (c & 1), (unsigned)lane) = zero;
-      *cl.map_shared_rank(pivs + c, (unsigned)lane) = bi;
-    }
-    if (zero) return;
-    for (int i = lane; i < n; i += 32) dst[i] = (i == c) ? src[bi] : (i == bi ? src[c] : src[i]);
-    __syncwarp();
-    const C inv = recip_warp<L>(ldE(dst[c], jl), lane);
-    if (lane == 0) sstore<L>(invd + (size_t)jl * cd, inv);
-    double* ml = mloc + (size_t)(c & 1) * n * cd;
-    for (int i = c + 1 + lane; i < n; i += 32) {
-      const int r = dst[i];
-      const C l = P::mul(ldE(r, jl), inv);
-      for (int q = 0; q < CS; ++q) sstore<L>(cl.map_shared_rank(ml, (unsigned)q) + (size_t)r * cd, l);
-    }
-  };
-  if (me == 0 && wid == 0) pivot_column(0);
-  cl.sync();
-  int k = 0;
-  bool stop = false;
-  for (;; ++k) {
-    stop = bad[k & 1] != 0;  // column k, pushed before the barrier (cluster-uniform)
-    if (stop || k == n - 1) break;
-    const int* pk = perm + (k & 1) * n;
-    if (me != owner(k)) {
-      // perm[k & 1] from perm[(k-1) & 1] and column k's pivot row
-      const int bi = pivs[k];
-      const int* src = perm + ((k + 1) & 1) * n;
-      int* dst = perm + (k & 1) * n;
-      for (int i = tid; i < n; i += T) dst[i] = (i == k) ? src[bi] : (i == bi ? src[k] : src[i]);
-      __syncthreads();
-    }
-    const double* ml = mloc + (size_t)(k & 1) * n * cd;
-    const int pr = pk[k];
-    const bool ahead = (owner(k + 1) == me);
-    if (ahead && wid == 0) {
-      // look-ahead: column k+1 of the rows below k, then its pivot, exchange, multipliers
-      const int jl = (k + 1) / CS;
-      const C u = ldE(pr, jl);
-      for (int i = k + 1 + lane; i < n; i += 32) {
-        const int r = pk[i];
-        stE(r, jl, P::sub(ldE(r, jl), P::mul(sload<L>(ml + (size_t)r * cd), u)));
-      }
-      __syncwarp();
-      pivot_column(k + 1);
-    } else {
-      // trailing update M[i][j] -= l_i M[k][j], i > k, local columns j >= k + 2
-      const int worker = ahead ? tid - 32 : tid;
-      const int nworker = ahead ? T - 32 : T;
-      const int jl0 = (k + 2 - me + CS - 1) / CS;  // first local slot with j >= k + 2
-      const int ncl = (cols - me + CS - 1) / CS - jl0;
-      const int rows = n - k - 1;
-      for (int e = worker; e < rows * ncl; e += nworker) {
-        const int i = k + 1 + e / ncl, jl = jl0 + e % ncl;
-        const int r = pk[i];
-        stE(r, jl, P::sub(ldE(r, jl), P::mul(sload<L>(ml + (size_t)r * cd), ldE(pr, jl))));
-      }
-    }
-    cl.sync();
-  }
-  if (stop) {
-    if (me == 0) {
-      if (tid == 0) a.status[p] = 1;
-      for (int e = tid; e < n; e += T)
-        cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
-    }
-    return;  // no CTA reads another's shared memory after the last barrier
-  }
-  // k == n - 1: the final permutation (column n-1's exchange) in every CTA
-  const int* pf = perm + ((n - 1) & 1) * n;
-  if (me != owner(n - 1)) {
-    const int bi = pivs[n - 1];
-    const int* src = perm + (n & 1) * n;
-    int* dst = perm + ((n - 1) & 1) * n;
-    for (int i = tid; i < n; i += T) dst[i] = (i == n - 1) ? src[bi] : (i == bi ? src[n - 1] : src[i]);
-  }
-  __syncthreads();
-  const int R = owner(n);
-  double* bv = Ug + (size_t)n * (n - 1) / 2 * cd;
-  double* iv = bv + (size_t)n * cd;
-  if (me == R) {
-    // gather U (logical rows, packed above the diagonal), b and the pivot reciprocals
-    const int tri = n * (n - 1) / 2;
-    for (int q = tid; q < tri; q += T) {
-      // row i holds entries j = i+1 .. n-1 from offset i (2n - i - 1) / 2
-      int i = 0;
-      while ((i + 1) * (2 * n - i - 2) / 2 <= q) ++i;
-      const int j = i + 1 + (q - i * (2 * n - i - 1) / 2);
-      const int o = owner(j);
-      sstore<L>(Ug + (size_t)q * cd, plane_ld<L>(cl.map_shared_rank(Mre, (unsigned)o), cl.map_shared_rank(Mim, (unsigned)o),
-                                                 ((size_t)pf[i] * W + j / CS) * L));
-    }
-    for (int i = tid; i < n; i += T) {
-      sstore<L>(bv + (size_t)i * cd, ldE(pf[i], n / CS));
-      sstore<L>(iv + (size_t)i * cd, sload<L>(cl.map_shared_rank(invd, (unsigned)owner(i)) + (size_t)(i / CS) * cd));
-    }
-  }
-  cl.sync();  // the gather is complete: the other CTAs may leave
-  if (me != R) return;
-  auto U = [&](int i, int j) { return sload<L>(Ug + ((size_t)i * (2 * n - i - 1) / 2 + (j - i - 1)) * cd); };
-  for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) sstore<L>(bv + (size_t)i * cd, P::mul(sload<L>(bv + (size_t)i * cd), sload<L>(iv + (size_t)i * cd)));
-    __syncthreads();
-    const C xi = sload<L>(bv + (size_t)i * cd);
-    for (int r = tid; r < i; r += T) sstore<L>(bv + (size_t)r * cd, P::sub(sload<L>(bv + (size_t)r * cd), P::mul(U(r, i), xi)));
-    __syncthreads();
-  }
-  for (int e = tid; e < n; e += T) {
-    const double* xp = a.X + ((size_t)p * n + e) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), sload<L>(bv + (size_t)e * cd)));
-  }
-  if (tid == 0) a.status[p] = 0;
 }
 
 }  // namespace phc

@@ -6,7 +6,6 @@
 namespace phc_rt {
 
 constexpr int64_t kCoopMaxPoints = 4;  // cooperative elimination up to this many points per call
-constexpr int64_t kClusterMaxPoints = 8;  // cluster elimination up to this many points per call
 
 // Multi-kernel elimination (kernels_newton.cuh) for matrices beyond shared memory.
 template <int L>
@@ -19,38 +18,6 @@ void newton_multi(const phc::NewtonArgs& a, int64_t np, cudaStream_t st) {
     if (work > 0) phc::newton_update_kernel<L><<<dim3((unsigned)((work + 255) / 256), (unsigned)np), 256, 0, st>>>(a, k);
   }
   phc::newton_backsub_kernel<L><<<(unsigned)np, 256, 0, st>>>(a);
-}
-
-// One thread-block cluster of CS CTAs per point (kernels_newton.cuh newton_cluster_kernel).
-template <int L>
-int newton_cluster(const phc::NewtonArgs& a, int64_t np, int CS, cudaStream_t st) {
-  const phc::ClusterLayout lay = phc::cluster_layout(a.n, L, CS);
-  auto kern = phc::newton_cluster_kernel<L>;
-  if (lay.bytes > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)kern, lay.bytes));
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(np * CS));
-  cfg.blockDim = dim3(phc::kClusterThreads);
-  cfg.dynamicSmemBytes = lay.bytes;
-  cfg.stream = st;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = (unsigned)CS;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a));
-  return PHC_OK;
-}
-
-// Cluster regime: few points of a mid-size system (beyond the warp kernel) whose [J | -F] and
-// back-substitution gather fit the cluster's shared memory.  PHC_NEWTON_CLUSTER=0|1 forces it
-// off / on where it fits, PHC_NEWTON_CLUSTER_SIZE the CTAs per cluster (A/B and test hooks).
-inline int cluster_size_for(int n, int L) {
-  const char* e = getenv("PHC_NEWTON_CLUSTER_SIZE");
-  int CS = e ? atoi(e) : (n <= 48 ? 4 : 8);
-  CS = std::max(1, std::min(8, CS));
-  return phc::cluster_layout(n, L, CS).bytes <= (size_t)220 * 1024 ? CS : 0;
 }
 
 // One cooperative launch per chunk (kernels_newton.cuh newton_coop_kernel): one CTA per SM.
@@ -151,17 +118,6 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
     a.n = n;
     a.n_points = np;
     ProfScope ps(s, d->dev, 2, st);
-    // few points, mid-size systems: one thread-block cluster per point (bitwise the same step)
-    {
-      const int cl_env = getenv("PHC_NEWTON_CLUSTER") ? atoi(getenv("PHC_NEWTON_CLUSTER")) : -1;  // A/B hook
-      const int CS = cluster_size_for(n, L);
-      const bool use = CS > 0 && !getenv("PHC_NEWTON_GLOBAL") &&
-                       (cl_env >= 0 ? cl_env == 1 : (np <= kClusterMaxPoints && n > 32));
-      if (use) {
-        if ((rc = (L == 2 ? newton_cluster<2>(a, np, CS, st) : newton_cluster<4>(a, np, CS, st)))) return rc;
-        continue;
-      }
-    }
     // small systems: one warp per point (bitwise the same step as the CTA kernel)
     const size_t per_warp = (size_t)n * (n + 1) * cd * sizeof(double);
     const int warp_env = getenv("PHC_NEWTON_WARP") ? atoi(getenv("PHC_NEWTON_WARP")) : -1;  // A/B hook

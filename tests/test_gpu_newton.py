@@ -401,72 +401,3 @@ def test_cooperative_elimination_singular_middle_column_repeated(phc, monkeypatc
         Xn, res, status = h.newton_step(Xd)
     torch.cuda.synchronize()
     assert (status.cpu().numpy() == 1).all() and torch.equal(Xn, Xd)
-
-
-def _step_env(phc, monkeypatch, s, X, env):
-    for k in ("PHC_NEWTON_CLUSTER", "PHC_NEWTON_CLUSTER_SIZE", "PHC_NEWTON_WARP", "PHC_NEWTON_GLOBAL",
-              "PHC_NEWTON_COOP"):
-        monkeypatch.delenv(k, raising=False)
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
-    h = phc.System(s)
-    Xd = torch.from_numpy(np.ascontiguousarray(X)).cuda()
-    out = h.newton_step(Xd)
-    torch.cuda.synchronize()
-    return [t.cpu().numpy() for t in out]
-
-
-@pytest.mark.parametrize("n,L,points,CS", [(40, 4, 1, 4), (40, 4, 3, 2), (40, 4, 2, 8), (33, 2, 1, 4),
-                                           (64, 4, 1, 8), (64, 2, 2, 3), (20, 2, 1, 1), (5, 4, 2, 4),
-                                           (2, 2, 1, 2), (1, 4, 1, 2)])
-def test_cluster_elimination_bitwise(phc, monkeypatch, n, L, points, CS):
-    """The thread-block-cluster elimination ([J | -F] distributed over CS CTAs by columns,
-    distributed-shared-memory multipliers, one cluster barrier per column) makes the same pivot
-    choices and the same operations per entry as the one-CTA shared-memory kernel (or, beyond
-    its shared memory, the cooperative global-memory kernel): bitwise equal steps."""
-    from synthetic import random_system
-    k = min(n, 6)
-    s, X = random_system(n, max(4, min(n, 12)), k, 3, L, seed=100 + n + CS, points=points)
-    big = (n * (n + 1) + n) * 2 * L * 8 + 2 * n * 4 > 200 * 1024
-    ref_env = {"PHC_NEWTON_GLOBAL": "1", "PHC_NEWTON_COOP": "1"} if big else {"PHC_NEWTON_CLUSTER": "0",
-                                                                            "PHC_NEWTON_WARP": "0"}
-    ref = _step_env(phc, monkeypatch, s, X, ref_env)
-    got = _step_env(phc, monkeypatch, s, X, {"PHC_NEWTON_CLUSTER": "1", "PHC_NEWTON_CLUSTER_SIZE": str(CS)})
-    for a, b in zip(ref, got):
-        assert np.array_equal(a.view(np.uint8), b.view(np.uint8))
-    if n >= 8:
-        assert (ref[2] == 0).all()
-
-
-def test_cluster_elimination_vs_oracle_c3(phc, monkeypatch):
-    """The c3 single point (n = 40, QD) takes the cluster elimination by default; its step
-    matches the oracle step within the error budget."""
-    s, X = config_system("c3", seed=1)
-    xn, res, status = _step_env(phc, monkeypatch, s, X, {})
-    h = phc.System(s)
-    F, Jd = h.eval_batch(torch.from_numpy(X).cuda())
-    Jc = Jd.cpu().numpy()[0][..., 0, 0] + 1j * Jd.cpu().numpy()[0][..., 1, 0]
-    err = _check_point(s, X[0], xn[0], res[0])
-    assert err <= _tol(4, 40, np.linalg.cond(Jc)), err
-
-
-@pytest.mark.parametrize("col", [0, 17, 39])
-def test_cluster_elimination_singular_column(phc, monkeypatch, col):
-    """Cluster path: a variable absent from the system gives a zero pivot column (first, middle,
-    last): status 1 and x unchanged, every CTA of the cluster leaving together."""
-    from synthetic import random_system
-    s, X = random_system(40, 6, 5, 2, 4, seed=20 + col, points=2)
-    keep = s.var_idx != col
-    counts = np.add.reduceat(keep.astype(np.int64), s.term_ptr[:-1])
-    counts[np.diff(s.term_ptr) == 0] = 0
-    s.term_ptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
-    s.var_idx, s.exponent = s.var_idx[keep].copy(), s.exponent[keep].copy()
-    for _ in range(5):
-        xn, res, status = _step_env(phc, monkeypatch, s, X, {"PHC_NEWTON_CLUSTER": "1"})
-    assert (status == 1).all() and np.array_equal(xn, X)
-
-
-def test_cluster_elimination_nan_residual(phc, monkeypatch):
-    s, X = _nan_f_finite_j_system(4)
-    xn, res, status = _step_env(phc, monkeypatch, s, X, {"PHC_NEWTON_CLUSTER": "1", "PHC_NEWTON_CLUSTER_SIZE": "2"})
-    assert math.isnan(float(res[0])) and int(status[0]) == 0
