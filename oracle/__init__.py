@@ -17,6 +17,6 @@ from .naive import (  # noqa: F401
     derivative_monomial,
 )
 from .compare import rel_errors, exact_equal_limbs  # noqa: F401
-from .newton import newton_step, solve_exact  # noqa: F401
+from .newton import newton_step, solve_exact, solve_step_mp  # noqa: F401
 from .homotopy import evaluate_homotopy_rows, evaluate_homotopy_dt  # noqa: F401
 from .predictor import lagrange_value, predict_point  # noqa: F401

@@ -92,6 +92,16 @@ def newton_step(system, X_point, arith="exact", prec=512, workers=None):
     ar = MPArith(prec)
     with mpmath.workprec(prec):
         z = [ar.from_limbs(X_point[v, 0], X_point[v, 1]) for v in range(n)]
+    return solve_step_mp(F, J, z, prec)
+
+
+def solve_step_mp(F, J, z, prec=512):
+    """The solve and update of one Newton step from evaluated F [n] and J [n][n]
+    (mpmath complex values) at the point z [n]: residual max_i |F_i|, dz = J^{-1} (-F) by
+    mpmath.lu_solve at `prec` bits, z_new = z + dz.  (newton_step's mp mode after the
+    evaluation; separate so stored oracle values of F and J can be reused.)"""
+    n = len(F)
+    with mpmath.workprec(prec):
         res = float(max(abs(f) for f in F))
         A = mpmath.matrix([[J[i][v] for v in range(n)] for i in range(n)])
         b = mpmath.matrix([-F[i] for i in range(n)])

@@ -171,3 +171,33 @@ def test_range_call_keeps_the_regime_of_the_whole_call(phc):
         h.eval_batch_range(Xd, 10, 5, Fr, Jr)
     with pytest.raises(phc.PhcError):
         h.eval_batch_range(Xd, 0, 1001, Fr, Jr)
+
+
+def test_large_newton_step_vs_oracle(phc, golden):
+    """NEXT-1 at the largest config (n = 256, QD, single point: the cooperative global-memory
+    elimination): the GPU's step dz = x_new - x against the oracle's (golden newton_dz0:
+    mpmath.lu_solve at 512 bits on the oracle's F and J), within the error budget
+    64 n u cond(J) of a backward-stable elimination; the residual max_i |F_i| as the oracle's."""
+    import mpmath
+    from fractions import Fraction
+    if "newton_dz0" not in golden:
+        pytest.skip("golden file without the Newton step (tools/make_golden_large.py --add-newton)")
+    s, X = config_system("large", seed=1)
+    h = phc.System(s, device=0)
+    Xd = torch.from_numpy(X).cuda()
+    Xn, res, status = h.newton_step(Xd)
+    F, J = h.eval_batch(Xd)
+    torch.cuda.synchronize()
+    assert int(status[0]) == 0
+    assert float(res[0]) == pytest.approx(float(golden["newton_residual0"]), rel=1e-12)
+    xn = Xn.cpu().numpy()[0]
+    ref = to_mpc(golden["newton_dz0"])
+    ex = lambda r: sum(Fraction(float(d)) for d in r)  # noqa: E731
+    with mpmath.workprec(1100):
+        got = [mpmath.mpc(mpmath.mpf(ex(xn[v, 0]) - ex(X[0, v, 0])), mpmath.mpf(ex(xn[v, 1]) - ex(X[0, v, 1])))
+               for v in range(s.n_var)]
+        num = max(abs(a - b) for a, b in zip(got, ref))
+        den = max(abs(b) for b in ref)
+    Jc = J.cpu().numpy()[0][..., 0, 0] + 1j * J.cpu().numpy()[0][..., 1, 0]
+    budget = 64 * s.n_var * 2.0 ** -209 * np.linalg.cond(Jc)
+    assert float(num / den) <= max(budget, 1e-60), (float(num / den), budget)

@@ -50,12 +50,25 @@ def child():
     b.record()
     b.synchronize()
     eps = 3 * X.shape[0] / (a.elapsed_time(b) * 1e-3)
+    sb, Xb = config_system("batch", seed=1)
+    hb = phc.System(sb)
+    Xbd = torch.from_numpy(Xb).cuda()
+    Fb, Jb = hb.eval_batch(Xbd)
+    torch.cuda.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(10):
+        hb.eval_batch(Xbd, Fb, Jb)
+    b.record()
+    b.synchronize()
+    dd_eps = 10 * Xb.shape[0] / (a.elapsed_time(b) * 1e-3)
+    del Fb, Jb, Xbd
     g = load()
     ar = MPArith(512)
     ef, _, _ = rel_errors(ar, to_mpc(g["F0"]), f.cpu().numpy())
     ej, _, _ = rel_errors(ar, to_mpc(g["J0"]), j.cpu().numpy().reshape(-1, 2, 4))
     print(json.dumps(dict(lib=os.environ.get("PHC_LIB", "libphc.so"), single_us_median=statistics.median(us),
-                          single_us_min=min(us), batch_evals_per_s=eps, err_F=ef, err_J=ej,
+                          single_us_min=min(us), batch_evals_per_s=eps, batch_dd_evals_per_s=dd_eps, err_F=ef, err_J=ej,
                           exec_flops_per_point=h.stats["exec_flops_per_point"])), flush=True)
 
 

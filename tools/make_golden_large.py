@@ -10,7 +10,11 @@ bits, >= 530 bits kept: the oracle's 512-bit values are stored without loss).  A
 input arrays (system tables and the points used) is stored beside them; the tests refuse a golden
 file whose inputs no longer match the generator.
 
-    python tools/make_golden_large.py            # ~5 min on 8 cores
+    python tools/make_golden_large.py            # ~11 min on 8 cores
+    python tools/make_golden_large.py --add-newton   # + the Newton step at point 0 (~min)
+
+`--add-newton` adds the oracle's Newton step at point 0 (Alg. 2: dz = J^{-1}(-F) by
+mpmath.lu_solve at 512 bits, oracle.solve_step_mp) computed from the stored oracle F and J.
 """
 import hashlib
 import os
@@ -22,7 +26,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
-from oracle import evaluate_rows  # noqa: E402
+from oracle import evaluate_rows, solve_step_mp  # noqa: E402
 from synthetic import config_system  # noqa: E402
 from synthetic.systems import split_limbs  # noqa: E402
 
@@ -54,7 +58,38 @@ def to_limbs(values):
     return out
 
 
+def from_limbs(limbs):
+    out = []
+    with mpmath.workprec(1100):
+        for v in limbs.reshape(-1, 2, LIMBS):
+            out.append(mpmath.mpc(mpmath.fsum(mpmath.mpf(float(d)) for d in v[0]),
+                                  mpmath.fsum(mpmath.mpf(float(d)) for d in v[1])))
+    return out
+
+
+def add_newton():
+    t0 = time.time()
+    g = dict(np.load(OUT))
+    s, X = config_system("large", seed=1)
+    n = s.n_var
+    F = from_limbs(g["F0"])
+    Jf = from_limbs(g["J0"])
+    J = [Jf[i * n:(i + 1) * n] for i in range(n)]
+    with mpmath.workprec(PREC):
+        z = [mpmath.mpc(mpmath.fsum(mpmath.mpf(float(d)) for d in X[0, v, 0]),
+                        mpmath.fsum(mpmath.mpf(float(d)) for d in X[0, v, 1])) for v in range(n)]
+    out = solve_step_mp(F, J, z, PREC)
+    assert not out["singular"]
+    g["newton_dz0"] = to_limbs(out["dz"])
+    g["newton_residual0"] = np.float64(out["residual"])
+    np.savez(OUT, **g)
+    print(f"Newton step at point 0 added in {time.time() - t0:.0f} s")
+
+
 def main():
+    if "--add-newton" in sys.argv:
+        add_newton()
+        return
     t0 = time.time()
     s, X = config_system("large_batch", seed=1)
     n = s.n_eq
