@@ -44,6 +44,9 @@
 namespace phc {
 
 constexpr int kWarp = 32;
+#ifndef PHC_DD_DEFER_RMW
+#define PHC_DD_DEFER_RMW 1
+#endif
 // Warps per CTA (NW); the other layouts run 8 warps in one CTA per SM.
 // Layout 2 runs 4-warp CTAs, two per SM (252 registers x 128 threads x 2 fits the register
 // file, 2 x ~99 KB shared memory), each CTA covering a whole point's polynomials
@@ -321,9 +324,36 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   if constexpr (L == 2) {
 #pragma unroll
     for (int t = 1; t <= H; ++t) phase1(t, word_at(t), word_at(K - t + 1));
+#if PHC_DD_DEFER_RMW
+    // the accumulator updates of step t are issued after the products of step t+1 (same
+    // updates in the same order, so the same bits): the shared-memory read-modify-write
+    // latency of a step overlaps the next step's arithmetic instead of stalling the warp
+    uint32_t dwa = 0, dwb = 0;
+    C dga, dgb;
+#pragma unroll
+    for (int t = 1; t <= H; ++t) {
+      const uint32_t wa = word_at(H + t), wb = word_at(H - t + 1);
+      const C pk = Pk[H - t], sk = t < H ? Sk[H - t] : P::one();
+      const int ea = entry(wa), eb = entry(wb);
+      C ga = P::mul_lazy(p, ld(ea + a.E));
+      if (t < H) ga = P::mul_lazy(ga, sk);
+      C gb = P::mul_lazy(pk, ld(eb + a.E));
+      gb = P::mul_lazy(gb, q);
+      p = P::mul_lazy(p, ld(ea));
+      if (t < H) q = P::mul_lazy(q, ld(eb));
+      if (t > 1) {
+        rmw(dwa, dga);
+        rmw(dwb, dgb);
+      }
+      dwa = wa, dwb = wb, dga = ga, dgb = gb;
+    }
+    rmw(dwa, dga);
+    rmw(dwb, dgb);
+#else
 #pragma unroll
     for (int t = 1; t <= H; ++t)
       phase2(t, Pk[H - t], t < H ? Sk[H - t] : P::one(), word_at(H + t), word_at(H - t + 1));
+#endif
   } else {
     // rolled loops (the QD body is thousands of instructions): the factor words are
     // fetched one step ahead, so the table gathers of a step do not wait on them

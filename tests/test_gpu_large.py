@@ -193,8 +193,12 @@ def test_large_newton_step_vs_oracle(phc, golden):
     xn = Xn.cpu().numpy()[0]
     ref = to_mpc(golden["newton_dz0"])
     ex = lambda r: sum(Fraction(float(d)) for d in r)  # noqa: E731
+
+    def mpq(fr):
+        return mpmath.mpf(fr.numerator) / fr.denominator
+
     with mpmath.workprec(1100):
-        got = [mpmath.mpc(mpmath.mpf(ex(xn[v, 0]) - ex(X[0, v, 0])), mpmath.mpf(ex(xn[v, 1]) - ex(X[0, v, 1])))
+        got = [mpmath.mpc(mpq(ex(xn[v, 0]) - ex(X[0, v, 0])), mpq(ex(xn[v, 1]) - ex(X[0, v, 1])))
                for v in range(s.n_var)]
         num = max(abs(a - b) for a, b in zip(got, ref))
         den = max(abs(b) for b in ref)
