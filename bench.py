@@ -591,8 +591,22 @@ def run_multiprocess(args):
         dist.init_process_group("gloo")
     cdev = dev if backend == "nccl" else None
     flush = not args.no_flush
-    c, s, X, h = build_workload(args.workload, args.points, local)
-    P = X.shape[0]
+    # rank 0 draws the batch and broadcasts it (every rank evaluates part of the SAME batch;
+    # the system itself is cheap to draw and identical on every rank)
+    import numpy as np
+    from synthetic import CONFIGS, config_system
+    c = CONFIGS[args.workload]
+    P = args.points or c["points"]
+    if rank == 0:
+        s, X = config_system(args.workload, seed=1, points=P)
+    else:
+        s, _ = config_system(args.workload, seed=1, points=1)
+        X = np.empty((P, s.n_var, 2, s.limbs), dtype=np.float64)
+    Xt = torch.from_numpy(X).to(dev) if backend == "nccl" else torch.from_numpy(X)
+    dist.broadcast(Xt, src=0)
+    X = Xt.cpu().numpy() if backend == "nccl" else Xt.numpy()
+    del Xt
+    h = phc.System(s, device=local)
     st = h.stats
     p0, p1 = shard_range(rank, world, P)
     Xd = torch.from_numpy(X).to(dev)  # inputs resident in HBM before the timed region
