@@ -119,6 +119,7 @@ int phc_eval_jacobian_batch_range(const phc_system* s, int64_t n_points, int64_t
  * the allocation on CUDA device `device` of the calling process (peer access enabled
  * lazily) and returns its base (add the offset); phc_ipc_close unmaps it.  The exporting
  * process owns the memory and must keep it alive until every importer closed it.
+ * Open a handle once per importing process (CUDA maps an allocation once per context).
  * PHC_ECUDA when the runtime refuses (e.g. memory not from cudaMalloc). */
 #define PHC_IPC_HANDLE_BYTES 64
 int phc_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset);
