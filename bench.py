@@ -151,6 +151,7 @@ def cpu_model():
 def config_dict(name, c, P, flush, parallelism):
     return {
         "workload": name,
+        "seed": 1,
         "n": c["n"], "m": c["m"], "k": c["k"], "D": c["D"],
         "precision": "complex DD" if c["limbs"] == 2 else "complex QD",
         "points": P,
@@ -437,7 +438,45 @@ def measure_single(phc, h, x, calls, local, flush=True):
     us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
     st = h.stats
     nl = max(int(sum(kn)), int(st["launches"]) * calls if not latency_regime(st, 1) else 0)
-    return us, clk.summary(), nl
+    return us, clk.summary(), nl, f.cpu().numpy(), j.cpu().numpy()
+
+
+def _exact_ints(limbs, scale=1300):
+    """[N][2][L] float64 limbs -> (re, im) exact integer multiples of 2^-scale (Python ints)."""
+    out = []
+    for v in limbs:
+        parts = []
+        for part in v:
+            acc = 0
+            for d in part:
+                num, den = float(d).as_integer_ratio()
+                acc += num << (scale - (den.bit_length() - 1))
+            parts.append(acc)
+        out.append(parts)
+    return out
+
+
+def parity_vs_golden(f, j):
+    """Normwise relative errors (reading C9) of the large point 0's F and J against the
+    committed oracle values (tests/golden/large_seed1.npz, written by tools/make_golden_large.py
+    from the mp512 oracle): exact integer arithmetic on the limbs, no oracle code executed."""
+    import numpy as np
+    g = np.load(os.path.join(ROOT, "tests", "golden", "large_seed1.npz"))
+
+    def err(gpu, ref):
+        # max(||d||_inf / ||ref||_inf, ||d||_F / ||ref||_F) with entries as complex moduli,
+        # from exact squared moduli (integers); only the final ratio is rounded
+        from fractions import Fraction
+        a, b = _exact_ints(np.asarray(gpu).reshape(-1, 2, gpu.shape[-1])), _exact_ints(ref.reshape(-1, 2, ref.shape[-1]))
+        d2 = [(x[0] - y[0]) ** 2 + (x[1] - y[1]) ** 2 for x, y in zip(a, b)]
+        r2 = [y[0] ** 2 + y[1] ** 2 for y in b]
+        if max(r2) == 0:
+            return 0.0 if max(d2) == 0 else float("inf")
+        return float(max(Fraction(max(d2), max(r2)), Fraction(sum(d2), sum(r2)))) ** 0.5
+
+    return {"err_F": err(f, g["F0"]), "err_J": err(j, g["J0"]), "tolerance": 1e-60,
+            "checked": f"all {f.shape[0]} F and {j.shape[0] * j.shape[1]} J entries of point 0 against the "
+                       "committed mp512 oracle values (tests/golden/large_seed1.npz)"}
 
 
 def build_workload(workload, P, device):
@@ -544,7 +583,7 @@ def run_one_process(args):
     if ngpu == 1 and not args.no_nested and args.workload == "large_batch":
         # the large single point (the same system; point 0 of the batch), L2 flushed per call
         x0 = torch.from_numpy(X[0]).cuda(local)
-        us, clk, nl = measure_single(phc, h, x0, args.single_calls, local, flush=True)
+        us, clk, nl, f0, j0 = measure_single(phc, h, x0, args.single_calls, local, flush=True)
         st = h.stats
         exec_pp = exec_flops_per_point(st, 1)
         med = statistics.median(us)
@@ -556,6 +595,7 @@ def run_one_process(args):
             "exec_flops_per_point": exec_pp, "exec_tflops": tf,
             "frac": tf / nominal_fp64_tflops(), "frac_of_measured": tf / peak_run, "clocks": clk,
             "gpu_launches": nl,
+            "parity": parity_vs_golden(f0, j0),
         }
         del x0
     if ngpu == 1 and not args.no_nested and args.workload != "batch":
