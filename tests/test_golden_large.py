@@ -47,3 +47,15 @@ def test_golden_zero_pattern_is_the_structure():
     zero = np.all(g["J0"] == 0, axis=(2, 3))
     assert np.array_equal(zero, ~nz)
     assert np.all(np.abs(g["F0"][:, :, 0]).max(axis=1) > 0)
+
+
+def test_bench_parity_check_against_golden():
+    """bench.py's in-line parity record (exact integer arithmetic on the limbs) sees QD
+    rounding of the oracle values as ~1e-65 and a perturbed entry as an error."""
+    import bench
+    g = load()
+    f, j = g["F0"][..., :4].copy(), g["J0"][..., :4].copy()
+    r = bench.parity_vs_golden(f, j)
+    assert r["err_F"] < 1e-63 and r["err_J"] < 1e-63
+    j[7, 9, 1, 1] += 1e-25
+    assert bench.parity_vs_golden(f, j)["err_J"] > 1e-30
