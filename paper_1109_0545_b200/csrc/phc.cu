@@ -913,7 +913,11 @@ int phc_eval_jacobian_batch_host(const phc_system* cs, int64_t n_points, const d
   DeviceState* d;
   int rc = get_device_state(s, s->home, &d);
   if (rc) return rc;
-  const int64_t chunks = n_points >= 8192 ? 8 : (n_points >= 1024 ? 4 : 1);
+  // chunks of ~128 MiB of output (the last chunk's copy is the exposed tail), at least 256
+  // points each (a chunk must still fill the GPU), at most 64
+  const int64_t out_bytes = n_points * (int64_t)s->n_eq * (s->n_var + 1) * cd * 8;
+  int64_t chunks = std::min<int64_t>(64, std::max<int64_t>(1, out_bytes >> 27));
+  chunks = std::max<int64_t>(1, std::min<int64_t>(chunks, n_points / 256));
   std::vector<cudaEvent_t> evs;
   for (int64_t c = 0; c < chunks; ++c) {
     const int64_t p0 = c * n_points / chunks, p1 = (c + 1) * n_points / chunks, np = p1 - p0;

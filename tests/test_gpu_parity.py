@@ -232,8 +232,8 @@ def test_latency_path_vs_batch_path(phc, name):
 
 
 def test_host_pipeline_equals_device_call(phc):
-    """phc_eval_jacobian_batch_host pipelines 8 chunks (output copies overlapping the next
-    chunk's evaluation) at >= 8192 points: bitwise the device call's results."""
+    """phc_eval_jacobian_batch_host pipelines chunks of ~128 MiB of output (output copies
+    overlapping the next chunk's evaluation; 2 chunks here): bitwise the device call's results."""
     s, X = config_system("batch", seed=6, points=8200)
     F, J, h = gpu_eval(phc, s, X)
     Fh = torch.empty((X.shape[0], s.n_eq, 2, 2), dtype=torch.float64).pin_memory()
