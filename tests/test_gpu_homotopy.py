@@ -51,7 +51,7 @@ def test_homotopy_vs_oracle(phc, name, seed):
     assert limbs_normalised(F) and limbs_normalised(J)
 
 
-@pytest.mark.parametrize("name", ["c2", "c3"])
+@pytest.mark.parametrize("name", ["c2", "c3", "batch", "large"])
 def test_t0_t1_equal_plain_evaluations(phc, name):
     """c(0) = c_s and c(1) = c_f exactly in the blend ((1 - t) and t are exactly 1 and 0),
     so the homotopy at t = 0 / 1 is bitwise the plain evaluation of the start / target system."""
