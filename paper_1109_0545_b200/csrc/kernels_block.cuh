@@ -44,6 +44,12 @@
 namespace phc {
 
 constexpr int kWarp = 32;
+// Layout 2: factor words pre-decoded on the host, word = e | row << 16 with e the power-table
+// entry of (var, exp) (the dummy variable's U(1) entry for padding) and row the accumulator row
+// (the spare row n_var for padding): no index arithmetic or dummy test per factor on the device
+#ifndef PHC_L2_PREDECODE
+#define PHC_L2_PREDECODE 1
+#endif
 #ifndef PHC_DD_DEFER_RMW
 #define PHC_DD_DEFER_RMW 1
 #endif
@@ -253,6 +259,10 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   const uint32_t* fw = a.fac + (size_t)b * K * kWarp + lane;
   // entry index of U(var, exp) in the power table; Dd is E entries further
   auto entry = [&](uint32_t word) {
+    if constexpr (LAYOUT == 2 && PHC_L2_PREDECODE) {
+      PHC_CHECK((word & 0xffffu) < (uint32_t)((a.n_var + 1) * twoE));
+      return (int)(word & 0xffffu);
+    }
     uint32_t v = word & 0xffffu;
     v = (v == kDummyVar) ? (uint32_t)a.n_var : v;
     const uint32_t ex = (word >> 16) & 0xffu;
@@ -274,7 +284,7 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   auto rmw = [&](uint32_t word, const C& g) {
     const uint32_t v = word & 0xffffu;
     if constexpr (junk) {
-      const int vr = (v == kDummyVar) ? a.n_var : (int)v;
+      const int vr = PHC_L2_PREDECODE ? (int)(word >> 16) : ((v == kDummyVar) ? a.n_var : (int)v);
       PHC_CHECK(vr <= a.n_var);
       double2* rw = reinterpret_cast<double2*>(rows);
       cls_store<L>(rw, RS, vr, cls, P::add_lazy(cls_load<L>(rw, RS, vr, cls), g));
@@ -765,13 +775,17 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       } else if (!colour_block(terms, s.n_var, K, R, &slot, &rep)) {
         return false;
       }
+      const bool predecode = PHC_L2_PREDECODE && layout == 2 && PHC_JUNK_ROW;
       for (int l = 0; l < kWarp; ++l) {
-        for (int q = 0; q < K; ++q) fac[((size_t)b * K + q) * kWarp + l] = kDummyVar | (1u << 16);
+        for (int q = 0; q < K; ++q)
+          fac[((size_t)b * K + q) * kWarp + l] =
+              predecode ? (uint32_t)(s.n_var * 2 * E) | ((uint32_t)s.n_var << 16) : kDummyVar | (1u << 16);
         if (l >= (int)terms.size()) continue;
         for (size_t j = 0; j < terms[l].size(); ++j) {
           const int q = slot[l][j];
+          const uint32_t v = (uint32_t)terms[l][j].first, ex = (uint32_t)terms[l][j].second;
           fac[((size_t)b * K + q) * kWarp + l] =
-              (uint32_t)terms[l][j].first | ((uint32_t)terms[l][j].second << 16) | ((uint32_t)rep[l][j] << 24);
+              predecode ? (v * 2 * E + ex - 1) | (v << 16) : v | (ex << 16) | ((uint32_t)rep[l][j] << 24);
         }
         const int64_t t = bterms[b][l];
         slot_term[(size_t)b * kWarp + l] = t;
