@@ -456,6 +456,22 @@ def _exact_ints(limbs, scale=1300):
     return out
 
 
+def _golden_err(gpu, ref):
+    """max(||d||_inf / ||ref||_inf, ||d||_F / ||ref||_F), entries as complex moduli, from exact
+    squared moduli (integers); only the final ratio is rounded.  gpu [..][2][L], ref [..][2][10]."""
+    import numpy as np
+    from fractions import Fraction
+    a = _exact_ints(np.asarray(gpu).reshape(-1, 2, np.asarray(gpu).shape[-1]))
+    b = _exact_ints(np.asarray(ref).reshape(-1, 2, np.asarray(ref).shape[-1]))
+    if len(a) != len(b):
+        raise ValueError(f"{len(a)} GPU values against {len(b)} oracle values")
+    d2 = [(x[0] - y[0]) ** 2 + (x[1] - y[1]) ** 2 for x, y in zip(a, b)]
+    r2 = [y[0] ** 2 + y[1] ** 2 for y in b]
+    if max(r2) == 0:
+        return 0.0 if max(d2) == 0 else float("inf")
+    return float(max(Fraction(max(d2), max(r2)), Fraction(sum(d2), sum(r2)))) ** 0.5
+
+
 def parity_vs_golden(f, j):
     """Normwise relative errors (reading C9) of the large point 0's F and J against the
     committed oracle values (tests/golden/large_seed1.npz, written by tools/make_golden_large.py
@@ -463,20 +479,43 @@ def parity_vs_golden(f, j):
     import numpy as np
     g = np.load(os.path.join(ROOT, "tests", "golden", "large_seed1.npz"))
 
-    def err(gpu, ref):
-        # max(||d||_inf / ||ref||_inf, ||d||_F / ||ref||_F) with entries as complex moduli,
-        # from exact squared moduli (integers); only the final ratio is rounded
-        from fractions import Fraction
-        a, b = _exact_ints(np.asarray(gpu).reshape(-1, 2, gpu.shape[-1])), _exact_ints(ref.reshape(-1, 2, ref.shape[-1]))
-        d2 = [(x[0] - y[0]) ** 2 + (x[1] - y[1]) ** 2 for x, y in zip(a, b)]
-        r2 = [y[0] ** 2 + y[1] ** 2 for y in b]
-        if max(r2) == 0:
-            return 0.0 if max(d2) == 0 else float("inf")
-        return float(max(Fraction(max(d2), max(r2)), Fraction(sum(d2), sum(r2)))) ** 0.5
-
-    return {"err_F": err(f, g["F0"]), "err_J": err(j, g["J0"]), "tolerance": 1e-60,
+    return {"err_F": _golden_err(f, g["F0"]), "err_J": _golden_err(j, g["J0"]), "tolerance": 1e-60,
             "checked": f"all {f.shape[0]} F and {j.shape[0] * j.shape[1]} J entries of point 0 against the "
                        "committed mp512 oracle values (tests/golden/large_seed1.npz)"}
+
+
+def parity_batch(workload, F, J):
+    """The batch line's own parity: GPU rows at the committed oracle points (batch: every entry
+    of 16 points, exact-rational oracle; large_batch: 8 rows at each of 8 points, mp512 oracle)
+    against tests/golden/*_seed1.npz, normwise per point (reading C9); the worst point reported."""
+    import numpy as np
+    if workload == "batch":
+        g = np.load(os.path.join(ROOT, "tests", "golden", "batch_seed1.npz"))
+        pts = [int(p) for p in g["points"]]
+        cases = [(F[p].cpu().numpy(), J[p].cpu().numpy(), g["F"][q], g["J"][q]) for q, p in enumerate(pts)]
+        what, tol = f"every entry of F and J at {len(pts)} points (first and last of each 8-way shard)", 1e-28
+    elif workload == "large_batch":
+        g = np.load(os.path.join(ROOT, "tests", "golden", "large_seed1.npz"))
+        pts = [int(p) for p in g["batch_points"]]
+        cases = []
+        for q, p in enumerate(pts):
+            rows = [int(r) for r in g["batch_rows"][q]]
+            cases.append((F[p].cpu().numpy()[rows], J[p].cpu().numpy()[rows], g["Fb"][q], g["Jb"][q]))
+        what, tol = f"8 rows of F and J at each of {len(pts)} points", 1e-60
+    else:
+        return None
+    ef = ej = 0.0
+    for f, j, gf, gj in cases:
+        ef = max(ef, _golden_err(f, gf))
+        ej = max(ej, _golden_err(j, gj))
+    return {"err_F": ef, "err_J": ej, "tolerance": tol,
+            "checked": what + f" against the committed oracle values (tests/golden/, {workload})"}
+
+
+def built_points(workload):
+    """The full batch size of a workload (the golden points index into it)."""
+    from synthetic import CONFIGS
+    return CONFIGS[workload]["points"]
 
 
 def build_workload(workload, P, device):
@@ -504,6 +543,7 @@ def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_
     ms_list, kms, kn, clocks = measure_batch(phc, h, Xd, F, J, steps, warmup, stream, scrub, local, devices)
     ms = sum(ms_list)
     ok = bool(torch.isfinite(F).all().item()) and bool(torch.isfinite(J).all().item())
+    parity = parity_batch(workload, F, J) if P == built_points(workload) else None
     del Xd, F, J, scrub
     torch.cuda.empty_cache()
     e2e_s, bi, bo = measure_e2e(h, X, e2e_steps, devices)
@@ -552,6 +592,8 @@ def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_
         "gpu_launches": max(int(sum(kn)), int(st["launches"]) * steps if not latency_regime(st, P) else 0),
         "outputs_finite": ok,
     }
+    if parity:
+        rec["parity"] = parity
     if label:
         rec["label"] = label
     return rec, h, X
