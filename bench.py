@@ -646,6 +646,22 @@ def run_one_process(args):
         rb, hb, _ = batch_record(phc, "batch", None, max(args.steps_eff, 10), max(args.warmup, 3), flush, local,
                                  args.e2e_steps, peak_run, label="BASELINE.json configs[3] batch, complex DD")
         out["batch_dd"] = rb
+    if ngpu == 1 and not args.no_nested:
+        # the three small single-point configs (BASELINE.json configs[0..2]): latency-bound
+        # calls, reported as the median of single calls with the L2 flushed before each
+        small = {}
+        for name in ("tiny", "c2", "c3"):
+            _, ss, Xs, hs = build_workload(name, None, local)
+            xs = torch.from_numpy(Xs[0]).cuda(local)
+            us, clk, nl, _, _ = measure_single(phc, hs, xs, args.single_calls, local, flush=True)
+            st = hs.stats
+            med = statistics.median(us)
+            small[name] = {"us_median": med, "us_p10": us[len(us) // 10], "us_p90": us[(9 * len(us)) // 10],
+                           "evals_per_s": 1e6 / med, "calls": len(us),
+                           "path": "latency (one warp per term)" if latency_regime(st, 1) else "batch kernels",
+                           "gpu_launches": nl, "clocks": clk}
+            del hs, xs
+        out["small_single"] = small
     if ngpu == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(args.workload)
     print(json.dumps(out), flush=True)
