@@ -44,11 +44,13 @@
 namespace phc {
 
 constexpr int kWarp = 32;
-// Layout 2: factor words pre-decoded on the host, word = e | row << 16 with e the power-table
-// entry of (var, exp) (the dummy variable's U(1) entry for padding) and row the accumulator row
-// (the spare row n_var for padding): no index arithmetic or dummy test per factor on the device
+// Layout 2: factor words pre-decoded on the host: the power-table entry e of (var, exp) (the
+// dummy variable's U(1) entry for padding) and the accumulator row (the spare row n_var for
+// padding), as e | row << 16 (1) or as the byte offset e * 128 | row << 24 (2: the offset is
+// added to per-lane chunk-plane pointers; layout 2 implies (n_var + 1) 2E <= 800, n_var < 100):
+// no index arithmetic or dummy test per factor on the device
 #ifndef PHC_L2_PREDECODE
-#define PHC_L2_PREDECODE 1
+#define PHC_L2_PREDECODE 2
 #endif
 #ifndef PHC_DD_DEFER_RMW
 #define PHC_DD_DEFER_RMW 1
@@ -258,8 +260,17 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   const int NE = (a.n_var + 1) * twoE;
   const uint32_t* fw = a.fac + (size_t)b * K * kWarp + lane;
   // entry index of U(var, exp) in the power table; Dd is E entries further
+  // PHC_L2_PREDECODE == 2: word = (entry * 128) | row << 24, the entry's byte offset within a
+  // chunk plane of the class-interleaved table (8 classes x 16 bytes per entry)
+  constexpr bool L2B = (LAYOUT == 2 && PHC_L2_PREDECODE == 2);
+  const int dd_off = L2B ? a.E * 128 : a.E;  // U -> Dd entry (index or byte offset)
+  const char* ptc0 = L2B ? reinterpret_cast<const char*>(pt) + cls * 16 : nullptr;
+  const char* ptc1 = L2B ? ptc0 + (size_t)NE * 128 : nullptr;
   auto entry = [&](uint32_t word) {
-    if constexpr (LAYOUT == 2 && PHC_L2_PREDECODE) {
+    if constexpr (L2B) {
+      PHC_CHECK((word & 0x1ffffu) < (uint32_t)((a.n_var + 1) * twoE * 128));
+      return (int)(word & 0x1ffffu);
+    } else if constexpr (LAYOUT == 2 && PHC_L2_PREDECODE) {
       PHC_CHECK((word & 0xffffu) < (uint32_t)((a.n_var + 1) * twoE));
       return (int)(word & 0xffffu);
     }
@@ -270,7 +281,13 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
     return (int)(v * twoE + ex - 1);
   };
   auto ld = [&](int e) -> C {
-    if constexpr (LAYOUT == 2) return cls_load<L>(reinterpret_cast<const double2*>(pt), NE, e, cls);
+    if constexpr (L2B) {
+      const double2 q0 = *reinterpret_cast<const double2*>(ptc0 + e);
+      const double2 q1 = *reinterpret_cast<const double2*>(ptc1 + e);
+      C v;
+      v.re.x[0] = q0.x; v.re.x[1] = q0.y; v.im.x[0] = q1.x; v.im.x[1] = q1.y;
+      return v;
+    } else if constexpr (LAYOUT == 2) return cls_load<L>(reinterpret_cast<const double2*>(pt), NE, e, cls);
     else if constexpr (LAYOUT == 1) return row_ld<L>(pt, (size_t)e);
     else return cload<L>(pt + (size_t)e * 2 * L);
   };
@@ -283,7 +300,19 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   const int RS = a.n_var + (junk ? 1 : 0);  // row stride (per class / per replica)
   auto rmw = [&](uint32_t word, const C& g) {
     const uint32_t v = word & 0xffffu;
-    if constexpr (junk) {
+    if constexpr (junk && L2B) {
+      const int ro = (int)(word >> 24) * 128;  // byte offset of the row entry within a chunk plane
+      PHC_CHECK((word >> 24) <= (uint32_t)a.n_var);
+      char* r0 = reinterpret_cast<char*>(rows) + cls * 16 + ro;
+      char* r1 = r0 + (size_t)RS * 128;
+      const double2 q0 = *reinterpret_cast<const double2*>(r0);
+      const double2 q1 = *reinterpret_cast<const double2*>(r1);
+      C acc;
+      acc.re.x[0] = q0.x; acc.re.x[1] = q0.y; acc.im.x[0] = q1.x; acc.im.x[1] = q1.y;
+      acc = P::add_lazy(acc, g);
+      *reinterpret_cast<double2*>(r0) = make_double2(acc.re.x[0], acc.re.x[1]);
+      *reinterpret_cast<double2*>(r1) = make_double2(acc.im.x[0], acc.im.x[1]);
+    } else if constexpr (junk) {
       const int vr = PHC_L2_PREDECODE ? (int)(word >> 16) : ((v == kDummyVar) ? a.n_var : (int)v);
       PHC_CHECK(vr <= a.n_var);
       double2* rw = reinterpret_cast<double2*>(rows);
@@ -322,9 +351,9 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
   // pk = P_{H-t}, sk = S_{H-t}; wa = word_at(H + t), wb = word_at(H - t + 1)
   auto phase2 = [&](int t, const C& pk, const C& sk, uint32_t wa, uint32_t wb) {
     const int ea = entry(wa), eb = entry(wb);
-    C ga = P::mul_lazy(p, ld(ea + a.E));
+    C ga = P::mul_lazy(p, ld(ea + dd_off));
     if (t < H) ga = P::mul_lazy(ga, sk);
-    C gb = P::mul_lazy(pk, ld(eb + a.E));
+    C gb = P::mul_lazy(pk, ld(eb + dd_off));
     gb = P::mul_lazy(gb, q);
     p = P::mul_lazy(p, ld(ea));
     if (t < H) q = P::mul_lazy(q, ld(eb));
@@ -345,9 +374,9 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
       const uint32_t wa = word_at(H + t), wb = word_at(H - t + 1);
       const C pk = Pk[H - t], sk = t < H ? Sk[H - t] : P::one();
       const int ea = entry(wa), eb = entry(wb);
-      C ga = P::mul_lazy(p, ld(ea + a.E));
+      C ga = P::mul_lazy(p, ld(ea + dd_off));
       if (t < H) ga = P::mul_lazy(ga, sk);
-      C gb = P::mul_lazy(pk, ld(eb + a.E));
+      C gb = P::mul_lazy(pk, ld(eb + dd_off));
       gb = P::mul_lazy(gb, q);
       p = P::mul_lazy(p, ld(ea));
       if (t < H) q = P::mul_lazy(q, ld(eb));
@@ -779,13 +808,16 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
       for (int l = 0; l < kWarp; ++l) {
         for (int q = 0; q < K; ++q)
           fac[((size_t)b * K + q) * kWarp + l] =
-              predecode ? (uint32_t)(s.n_var * 2 * E) | ((uint32_t)s.n_var << 16) : kDummyVar | (1u << 16);
+              predecode ? (PHC_L2_PREDECODE == 2 ? ((uint32_t)(s.n_var * 2 * E) << 7) | ((uint32_t)s.n_var << 24)
+                                                 : (uint32_t)(s.n_var * 2 * E) | ((uint32_t)s.n_var << 16))
+                        : kDummyVar | (1u << 16);
         if (l >= (int)terms.size()) continue;
         for (size_t j = 0; j < terms[l].size(); ++j) {
           const int q = slot[l][j];
           const uint32_t v = (uint32_t)terms[l][j].first, ex = (uint32_t)terms[l][j].second;
           fac[((size_t)b * K + q) * kWarp + l] =
-              predecode ? (v * 2 * E + ex - 1) | (v << 16) : v | (ex << 16) | ((uint32_t)rep[l][j] << 24);
+              predecode ? (PHC_L2_PREDECODE == 2 ? ((v * 2 * E + ex - 1) << 7) | (v << 24) : (v * 2 * E + ex - 1) | (v << 16))
+                        : v | (ex << 16) | ((uint32_t)rep[l][j] << 24);
         }
         const int64_t t = bterms[b][l];
         slot_term[(size_t)b * kWarp + l] = t;
