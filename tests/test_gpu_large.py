@@ -205,3 +205,20 @@ def test_large_newton_step_vs_oracle(phc, golden):
     Jc = J.cpu().numpy()[0][..., 0, 0] + 1j * J.cpu().numpy()[0][..., 1, 0]
     budget = 64 * s.n_var * 2.0 ** -209 * np.linalg.cond(Jc)
     assert float(num / den) <= max(budget, 1e-60), (float(num / den), budget)
+
+
+@pytest.mark.parametrize("points,shards", [(2000, 5), (5, 5)])
+def test_range_call_common_support(phc, points, shards):
+    """phc_eval_jacobian_batch_range on a common-support handle (the two-stage path, NEXT-2):
+    shards of a batch call and of a few-point call (latency regime, chosen from the whole
+    call's point count) are bitwise the unsharded call."""
+    from synthetic import common_config
+    c, X = common_config("common_dd", seed=4, points=points)
+    h = phc.System(c, device=0)
+    Xd = torch.from_numpy(X).cuda()
+    F, J = h.eval_batch(Xd)
+    Fr, Jr = torch.zeros_like(F), torch.zeros_like(J)
+    for r in range(shards):
+        h.eval_batch_range(Xd, r * points // shards, (r + 1) * points // shards, Fr, Jr)
+    torch.cuda.synchronize()
+    assert torch.equal(Fr, F) and torch.equal(Jr, J)
