@@ -36,6 +36,7 @@ int newton_coop(const phc::NewtonArgs& a, DeviceState* d, cudaStream_t st) {
     }
     G = it->second;
   }
+  if (const char* e = getenv("PHC_NEWTON_COOP_CTAS")) G = std::max(2, std::min(G, atoi(e)));  // A/B hook
   const size_t smem = phc::coop_smem_bytes(a.n, L);
   if (smem > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)phc::newton_coop_kernel<L>, smem));
   int nb = 0;
