@@ -749,9 +749,17 @@ int phc_ipc_get_handle(const void* dev_ptr, void* handle, int64_t* offset) {
   return PHC_OK;
 }
 
+static int check_device(int32_t device) {
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) return fail(PHC_ECUDA, "cudaGetDeviceCount failed");
+  if (device < 0 || device >= c) return fail(PHC_EINVAL, "device %d out of range (%d devices)", device, c);
+  return PHC_OK;
+}
+
 int phc_ipc_open(const void* handle, int32_t device, void** base) {
   g_err.clear();
   if (!handle || !base) return fail(PHC_EINVAL, "NULL argument");
+  if (int rc = check_device(device)) return rc;
   DeviceGuard g(device);
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof(h));
@@ -762,6 +770,7 @@ int phc_ipc_open(const void* handle, int32_t device, void** base) {
 int phc_ipc_close(void* base, int32_t device) {
   g_err.clear();
   if (!base) return PHC_OK;
+  if (int rc = check_device(device)) return rc;
   DeviceGuard g(device);
   CUDA_TRY(cudaIpcCloseMemHandle(base));
   return PHC_OK;

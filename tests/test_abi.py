@@ -121,3 +121,18 @@ def test_next_row_entry_points_validate_without_device():
     assert lib.phc_homotopy_old_create(ctypes.byref(h), 0, 1, 2, 0, None, None, None, None, None, None, 0) == L.PHC_EINVAL
     assert lib.phc_system_create_common(ctypes.byref(h), 2, 2, 2, 0, None, None, None, None, 0) == L.PHC_EINVAL
     assert "NULL" in L.phc_last_error() or L.phc_last_error() != ""
+
+
+def test_range_and_ipc_entry_points_validate_without_device():
+    """The multi-process entry points reject bad arguments before touching a device."""
+    import ctypes
+    import paper_1109_0545_b200._lib as L
+    lib = L.lib
+    P = ctypes.c_void_p
+    assert lib.phc_eval_jacobian_batch_range(None, 10, 0, 5, None, None, None, None) == L.PHC_EINVAL
+    off = ctypes.c_int64()
+    assert lib.phc_ipc_get_handle(None, None, ctypes.byref(off)) == L.PHC_EINVAL
+    base = P()
+    assert lib.phc_ipc_open(None, 0, ctypes.byref(base)) == L.PHC_EINVAL
+    assert lib.phc_ipc_close(None, 0) == L.PHC_OK  # NULL mapping: no-op
+    assert "NULL" in L.phc_last_error() or L.phc_last_error() == ""
