@@ -104,7 +104,8 @@ int newton_impl(const phc_system* cs, int64_t n_points, const double* x, const d
   }
   // few points: 512 threads spread one elimination over the whole SM; batches: 128-256 per point
   const char* th_env = getenv("PHC_NEWTON_THREADS");  // A/B hook (CTA eliminations)
-  const int threads = th_env ? atoi(th_env) : (n_points < 148 ? 512 : (n <= 48 ? 128 : 256));
+  const int threads = th_env ? std::max(64, std::min(512, atoi(th_env) / 32 * 32))  // the kernels' launch bounds
+                             : (n_points < 148 ? 512 : (n <= 48 ? 128 : 256));
   for (int64_t p0 = 0; p0 < n_points; p0 += chunk) {
     const int64_t np = std::min(chunk, n_points - p0);
     if ((rc = run_on_device(s, d, np, x + p0 * n * cd, T ? T + p0 * L : nullptr, d->nF, d->nJ, st, n_points)))
