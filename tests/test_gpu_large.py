@@ -222,3 +222,18 @@ def test_range_call_common_support(phc, points, shards):
         h.eval_batch_range(Xd, r * points // shards, (r + 1) * points // shards, Fr, Jr)
     torch.cuda.synchronize()
     assert torch.equal(Fr, F) and torch.equal(Jr, J)
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_large_other_seeds_sampled_rows(phc, seed):
+    """Two more random systems of the large shape (seeds 2, 3; single point): 3 rows of F and J
+    against the mp512 oracle computed here (the committed values cover seed 1 in full)."""
+    from _parity import compare_point, oracle_point
+    s, X = config_system("large", seed=seed)
+    h = phc.System(s, device=0)
+    f, j = h.eval(torch.from_numpy(X[0]).cuda())
+    torch.cuda.synchronize()
+    rows = [0, 100 + seed, 255]
+    ar, Fr, Jr = oracle_point(s, X[0], rows=rows, arith="mp")
+    ef, ej = compare_point(ar, Fr, Jr, f.cpu().numpy(), j.cpu().numpy(), 4, rows)
+    assert ef <= TOL[4] and ej <= TOL[4], (ef, ej)
