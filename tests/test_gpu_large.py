@@ -237,3 +237,18 @@ def test_large_other_seeds_sampled_rows(phc, seed):
     ar, Fr, Jr = oracle_point(s, X[0], rows=rows, arith="mp")
     ef, ej = compare_point(ar, Fr, Jr, f.cpu().numpy(), j.cpu().numpy(), 4, rows)
     assert ef <= TOL[4] and ej <= TOL[4], (ef, ej)
+
+
+@pytest.mark.parametrize("seed", [2, 3])
+def test_batch_other_seeds_sampled_points(phc, seed):
+    """The batch shape on two more random systems (seeds 2, 3; all 65,536 points in one call,
+    the bench configuration): 4 points against the exact oracle, every entry."""
+    from _parity import compare_point, oracle_point
+    s, X = config_system("batch", seed=seed)
+    h = phc.System(s, device=0)
+    F, J = h.eval_batch(torch.from_numpy(X).cuda())
+    torch.cuda.synchronize()
+    for p in (0, 777 * seed, 40000 + seed, 65535):
+        ar, Fr, Jr = oracle_point(s, X[p], arith="exact")
+        ef, ej = compare_point(ar, Fr, Jr, F[p].cpu().numpy(), J[p].cpu().numpy(), 2)
+        assert ef <= TOL[2] and ej <= TOL[2], (p, ef, ej)
