@@ -99,8 +99,9 @@ int phc_eval_jacobian(const phc_system* s, const double* x, double* f, double* j
 int phc_eval_jacobian_batch(const phc_system* s, int64_t n_points, const double* x, double* f, double* jac,
                             const int32_t* devices, int32_t n_devices, void* stream);
 
-/* Points [p_begin, p_end) of an n_points-point batch call, evaluated on the handle's home
- * device and written into the FULL output arrays: x [n_points][n_var][2][L] (only rows
+/* Points [p_begin, p_end) of an n_points-point batch call -- the same Y (the polynomials and
+ * all partial derivatives) as phc_eval_jacobian_batch -- evaluated on the handle's
+ * home device and written into the FULL output arrays: x [n_points][n_var][2][L] (only rows
  * p_begin .. p_end-1 are read), f [n_points][n_eq][2][L], jac [n_points][n_eq][n_var][2][L]
  * (only those rows are written).  The evaluation regime is that of the whole n_points call,
  * so the rows are bitwise those phc_eval_jacobian_batch writes for all n_points: a batch
