@@ -170,6 +170,21 @@ def model_counts(s, st):
     return cm, ca
 
 
+def latency_kernel_name(st):
+    return f"poly_seg_kernel<4,{st['latency_G']}>" if st["latency_kernel"] == 2 else "poly_scan_kernel"
+
+
+def latency_path_name(st):
+    if st["latency_kernel"] == 2:
+        return f"latency (segmented: {st['latency_G']} lanes per term, power table + kernel)"
+    return "latency (one warp per term)"
+
+
+def launches_per_call(st, points):
+    """kernel launches of one eval call with `points` points (phc_system_stats)"""
+    return int(st["latency_launches"] if latency_regime(st, points) else st["launches"])
+
+
 def latency_regime(st, points):
     """True when a call with `points` points takes the latency path (phc.h: n_points * n_terms
     <= the bound in phc_system_stats out[13])."""
@@ -437,7 +452,7 @@ def measure_single(phc, h, x, calls, local, flush=True):
     phc.phc_profile_enable(h._h, False)
     us = sorted(a.elapsed_time(b) * 1e3 for a, b in ev)
     st = h.stats
-    nl = max(int(sum(kn)), int(st["launches"]) * calls if not latency_regime(st, 1) else 0)
+    nl = max(int(sum(kn)), launches_per_call(st, 1) * calls)
     return us, clk.summary(), nl, f.cpu().numpy(), j.cpu().numpy()
 
 
@@ -551,12 +566,12 @@ def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_
     mf = MODEL_FLOPS[s.limbs]
     model_pp = cm_model * mf["cm"] + ca_model * mf["ca"]
     exec_pp = exec_flops_per_point(st, P)
-    names = ["power_table", "term", "reduce", "poly_scan" if latency_regime(st, P) else "fused_block"]
+    names = ["power_table", "term", "reduce", latency_kernel_name(st) if latency_regime(st, P) else "fused_block"]
     dom = max(range(4), key=lambda i: kms[i])
     dom_ms = kms[dom] / max(kn[dom], 1)
     launches_dom_per_step = max(kn[dom] / steps, 1)
     kernel = {3: f"block_kernel<{s.limbs},{st['K']},{st['layout']},0>" if not latency_regime(st, P)
-              else f"poly_scan_kernel<{s.limbs}>"}.get(dom, names[dom])
+              else latency_kernel_name(st)}.get(dom, names[dom])
     step_s = ms / steps * 1e-3
     multi = devices is not None and len(devices) > 1
     rl = roofline(exec_pp, P / launches_dom_per_step, dom_ms, peak_run, workload, kernel)
@@ -568,7 +583,7 @@ def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_
         "ms_per_step_median": statistics.median(ms_list),
         "config": config_dict(workload, c, P, flush,
                               f"points sharded over devices {list(devices)} (one process)" if multi else "one GPU"),
-        "path": "latency (one warp per term)" if latency_regime(st, P) else "batch kernels",
+        "path": latency_path_name(st) if latency_regime(st, P) else "batch kernels",
         "roofline": rl,
         "fp64": {
             "step_exec_tflops": exec_pp * P / step_s / 1e12,
@@ -589,7 +604,7 @@ def batch_record(phc, workload, P, steps, warmup, flush, local, e2e_steps, peak_
         },
         # the profile records the block kernel; the power-table kernel of layout 0 (a
         # programmatic dependent launch) is counted from the plan's launches per call
-        "gpu_launches": max(int(sum(kn)), int(st["launches"]) * steps if not latency_regime(st, P) else 0),
+        "gpu_launches": max(int(sum(kn)), launches_per_call(st, P) * steps),
         "outputs_finite": ok,
     }
     if parity:
@@ -658,7 +673,7 @@ def run_one_process(args):
             med = statistics.median(us)
             small[name] = {"us_median": med, "us_p10": us[len(us) // 10], "us_p90": us[(9 * len(us)) // 10],
                            "evals_per_s": 1e6 / med, "calls": len(us),
-                           "path": "latency (one warp per term)" if latency_regime(st, 1) else "batch kernels",
+                           "path": latency_path_name(st) if latency_regime(st, 1) else "batch kernels",
                            "gpu_launches": nl, "clocks": clk}
             del hs, xs
         out["small_single"] = small

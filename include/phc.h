@@ -290,10 +290,12 @@ int phc_track_paths(const phc_system* s, int64_t n_paths, double* x, const phc_t
  * point of the kernels' useful work (DADD = DMUL = 1, DFMA = 2; padding lanes/slots not
  * counted), out[9] = path (0 generic, 1 fused block), out[10] = block layout,
  * out[11] = slots per lane K, out[12] = executed FP64 flops per point on the latency path
- * (one warp per term; includes its redundant products; 0 if the system never takes it),
+ * (includes its redundant products; 0 if the system never takes it),
  * out[13] = the latency-path bound: calls with n_points * n_terms <= out[13] take it,
- * out[14] = 1 for a common-support handle. */
-#define PHC_STATS_LEN 15
+ * out[14] = 1 for a common-support handle, out[15] = the latency-path kernel (0 none,
+ * 1 one warp per term, 2 segmented: G lanes per term), out[16] = its G (0 unless segmented),
+ * out[17] = kernel launches per latency-path call. */
+#define PHC_STATS_LEN 18
 int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]);
 
 /* FP64 pipe peak of `device` in TFLOP/s (2 flops per DFMA), measured with independent

@@ -235,7 +235,7 @@ def phc_homotopy_old_create(n_eq, n_var, limbs, n_terms, poly_ptr, term_ptr, var
 
 
 def phc_system_stats(h):
-    out = (ctypes.c_int64 * 15)()
+    out = (ctypes.c_int64 * 18)()
     check(lib.phc_system_stats(h, out))
     return list(out)
 

@@ -182,6 +182,8 @@ int run_generic(const phc_system* s, DeviceState* d, int64_t n_points, const dou
 }
 
 // Latency path (kernels_scan.cuh) for calls with few points: one warp per term.
+int split_scratch(const phc_system* s, DeviceState* d, int64_t n_points, int S, int64_t cd, cudaStream_t st,
+                  phc::ScanArgs* a);
 
 template <int L>
 int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
@@ -204,8 +206,23 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
   a.n_points = n_points;
   a.part = nullptr;
   a.count = nullptr;
-  if (s->scan_S > 1) {
-    const int64_t need = n_points * s->n_eq * s->scan_S * (int64_t)(s->n_var + 1) * cd;
+  int rc = split_scratch(s, d, n_points, s->scan_S, cd, st, &a);
+  if (rc) return rc;
+  ProfScope ps(s, d->dev, 3, st);
+  auto kern = phc::poly_scan_kernel<L>;
+  if (s->scan_smem > 48 * 1024)
+    CUDA_TRY(phc::ensure_smem((const void*)kern, s->scan_smem));
+  const int64_t ctas = n_points * s->n_eq * s->scan_S;
+  kern<<<(unsigned)ctas, s->scan_W * 32, s->scan_smem, st>>>(a);
+  CUDA_TRY(cudaGetLastError());
+  return PHC_OK;
+}
+
+// partial rows and arrival counters of an S-way split (latency paths)
+int split_scratch(const phc_system* s, DeviceState* d, int64_t n_points, int S, int64_t cd, cudaStream_t st,
+                  phc::ScanArgs* a) {
+  if (S > 1) {
+    const int64_t need = n_points * s->n_eq * S * (int64_t)(s->n_var + 1) * cd;
     if (need > d->part_cap) {
       cudaStreamSynchronize(st);
       if (d->part) cudaFree(d->part);
@@ -215,7 +232,7 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
       if (rc) return rc;
       d->part_cap = need;
     }
-    a.part = d->part;
+    a->part = d->part;
     const int64_t nc = n_points * s->n_eq;
     if (nc > d->count_cap) {
       cudaStreamSynchronize(st);
@@ -229,16 +246,79 @@ int run_scan(const phc_system* s, DeviceState* d, int64_t n_points, const double
       CUDA_TRY(cudaMemsetAsync(d->count, 0, nc * sizeof(int), st));
       d->count_cap = nc;
     }
-    a.count = d->count;
+    a->count = d->count;
+  }
+  return PHC_OK;
+}
+
+// Segmented latency path (kernels_scan.cuh poly_seg_kernel): the power table of the call's
+// points (block_power_table_kernel, global), then the segmented kernel as its programmatic
+// dependent launch.
+template <int L, int G>
+int launch_seg(const phc_system* s, const phc::ScanArgs& a, const double* PT, int64_t n_points, cudaStream_t st) {
+  auto kern = phc::poly_seg_kernel<L, G>;
+  if (s->seg_smem > 48 * 1024) CUDA_TRY(phc::ensure_smem((const void*)kern, s->seg_smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(n_points * s->n_eq * s->seg_S));
+  cfg.blockDim = dim3(s->seg_W * 32);
+  cfg.dynamicSmemBytes = s->seg_smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, a, PT));
+  return PHC_OK;
+}
+
+// segment widths G compiled for the segmented path (two factors per lane: k <= 2G);
+// phc_system_create picks one
+#define PHC_SEG_SHAPES(X) X(4) X(8) X(10) X(12) X(16)
+
+template <int L>
+int run_seg(const phc_system* s, DeviceState* d, int64_t n_points, const double* x, const double* T, double* f,
+            double* jac, cudaStream_t st) {
+  const int64_t cd = 2 * L;
+  phc::ScanArgs a;
+  a.poly_ptr = d->poly_ptr;
+  a.term_ptr = d->term_ptr;
+  a.fac = d->fac;
+  a.coeff = d->coeff;
+  a.coeff2 = T ? d->coeff2 : nullptr;
+  a.T = T;
+  a.X = x;
+  a.F = f;
+  a.J = jac;
+  a.n_eq = s->n_eq;
+  a.n_var = s->n_var;
+  a.E = s->E;
+  a.S = s->seg_S;
+  a.n_points = n_points;
+  a.part = nullptr;
+  a.count = nullptr;
+  int rc = split_scratch(s, d, n_points, s->seg_S, cd, st, &a);
+  if (rc) return rc;
+  const int64_t per_point = (int64_t)(s->n_var + 1) * 2 * s->E * cd;
+  if (n_points * per_point > d->segPT_cap) {
+    cudaStreamSynchronize(st);
+    if (d->segPT) cudaFree(d->segPT);
+    d->segPT = nullptr;
+    d->segPT_cap = 0;
+    rc = dalloc(&d->segPT, (size_t)(n_points * per_point));
+    if (rc) return rc;
+    d->segPT_cap = n_points * per_point;
   }
   ProfScope ps(s, d->dev, 3, st);
-  auto kern = phc::poly_scan_kernel<L>;
-  if (s->scan_smem > 48 * 1024)
-    CUDA_TRY(phc::ensure_smem((const void*)kern, s->scan_smem));
-  const int64_t ctas = n_points * s->n_eq * s->scan_S;
-  kern<<<(unsigned)ctas, s->scan_W * 32, s->scan_smem, st>>>(a);
+  const int64_t nth = n_points * (s->n_var + 1) * s->E;
+  phc::block_power_table_kernel<L><<<(unsigned)((nth + 127) / 128), 128, 0, st>>>(x, s->n_var, s->E, n_points,
+                                                                                 d->segPT);
   CUDA_TRY(cudaGetLastError());
-  return PHC_OK;
+#define PHC_SEG_CASE(G_) \
+  if (s->seg_G == G_) return launch_seg<L, G_>(s, a, d->segPT, n_points, st);
+  PHC_SEG_SHAPES(PHC_SEG_CASE)
+#undef PHC_SEG_CASE
+  return fail(PHC_EUNSUPPORTED, "segmented latency path: no kernel for G = %d", s->seg_G);
 }
 
 // NEXT-2 two-stage path: power table, monomial stage V (the term kernel with unit
@@ -320,7 +400,9 @@ int run_on_device(const phc_system* s, DeviceState* d, int64_t n_points, const d
   }
   static const bool no_latency = getenv("PHC_DEBUG_NO_LATENCY_PATH") != nullptr;  // A/B hook
   if (s->scan_ok && !no_latency && (call_points < 0 ? n_points : call_points) * s->n_terms <= kScanMaxTerms)
-    return s->L == 2 ? run_scan<2>(s, d, n_points, x, T, f, jac, st) : run_scan<4>(s, d, n_points, x, T, f, jac, st);
+    return s->seg_ok ? run_seg<4>(s, d, n_points, x, T, f, jac, st)
+           : s->L == 2 ? run_scan<2>(s, d, n_points, x, T, f, jac, st)
+                       : run_scan<4>(s, d, n_points, x, T, f, jac, st);
   if (d->have_block) {
     ProfScope ps(s, d->dev, 3, st);
     int rc = s->L == 2 ? phc::run_block<2>(s->plan, d->bt, s->n_eq, s->n_var, n_points, x, T, f, jac, st)
@@ -590,6 +672,46 @@ int phc_system_create(phc_system** out, int32_t n_eq, int32_t n_var, int32_t lim
     // c2 (k = 10) 12.6 vs 12.5, c3 (k = 20) 75 vs 47 (tools/regime_ab.sh); k <= 2 tracker
     // systems: the block path is as fast or faster and steadier (tools/track_regime.py)
     s->scan_ok = kmax >= 12 && kmax <= 32 && s->scan_smem <= (size_t)200 * 1024 && max_terms > 0;
+    // segmented latency path (QD): the segment width G (lanes per term, two factors per lane)
+    // with the fewest products on the busiest scheduler, 8 + 2 ceil(log2 G) per lane times the
+    // warp-tasks per scheduler (592 on a B200); W = 2 warps per CTA (more when the CTA count
+    // would exceed two per SM), S splits so that each warp takes about one task
+    if (s->scan_ok && limbs == 4) {  // DD: the warp-scan kernel is faster (batch config 13.0 vs 16.3 us)
+      static const int widths[] = {4, 8, 10, 12, 16};
+      int bestG = 0;
+      double best = 1e300;
+      const char* env = getenv("PHC_SEG");  // A/B hook: "G" forces a width, "0" the warp-scan path
+      const int eg = env ? atoi(env) : -1;
+      for (int G : widths) {
+        if (2 * G < kmax) continue;
+        if (eg >= 0 && G != eg) continue;
+        int lg = 0;
+        while ((1 << lg) < G) ++lg;
+        int64_t tasks = 0;
+        for (int i = 0; i < n_eq; ++i) tasks += (poly_ptr[i + 1] - poly_ptr[i] + 32 / G - 1) / (32 / G);
+        const double est = (8.0 + 2 * lg) * std::max<double>(1.0, std::ceil(tasks / 592.0));
+        if (est < best) best = est, bestG = G;
+      }
+      if (bestG > 0) {
+        const int TPW = 32 / bestG;
+        int W = 2;
+        int64_t S = (max_terms + W * TPW - 1) / (W * TPW);
+        while (n_eq * S > 2 * 148 && W < phc::kSegMaxWarps) {
+          W *= 2;
+          S = (max_terms + W * TPW - 1) / (W * TPW);
+        }
+        if (const char* ew = getenv("PHC_SEG_W")) {  // A/B hook: warps per CTA
+          W = std::max(1, std::min(phc::kSegMaxWarps, atoi(ew)));
+          S = (max_terms + W * TPW - 1) / (W * TPW);
+        }
+        if (const char* es = getenv("PHC_SEG_S")) S = std::max(1, atoi(es));  // test hook: splits
+        s->seg_G = bestG;
+        s->seg_W = W;
+        s->seg_S = (int)std::max<int64_t>(1, S);
+        s->seg_smem = (size_t)W * TPW * (n_var + 1) * 2 * limbs * sizeof(double);
+        s->seg_ok = s->seg_smem <= (size_t)200 * 1024;
+      }
+    }
   }
   s->ca_per_point = s->plan.usable ? s->plan.ca_per_point : s->ca_per_point;
   DeviceState* d;
@@ -1014,7 +1136,23 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
     // one integer scaling per entry), n_eq * S CTAs per point
     const phc::OpFlops f = phc::op_flops(s->L);
     int64_t fl = 0;
-    if (s->scan_ok && !s->common) {
+    if (s->seg_ok && !s->common) {
+      // segmented path: per warp-task (32 / G terms) 8 + 2 ceil(log2 G) products on all
+      // 32 lanes, one addition per factor and per term; the global power table once per point
+      // (<= 2 log2(E) + 1 products and one integer scaling per entry); the epilogue's additions
+      int lg = 0, lgE = 0;
+      while ((1 << lg) < s->seg_G) ++lg;
+      while ((1 << lgE) < s->E) ++lgE;
+      const int TPW = 32 / s->seg_G;
+      for (int i = 0; i < s->n_eq; ++i) {
+        const int64_t nt = s->poly_ptr[i + 1] - s->poly_ptr[i];
+        fl += (nt + TPW - 1) / TPW * 32 * (8 + 2 * lg) * (int64_t)f.cm;
+      }
+      fl += (s->n_factors + s->n_terms) * (int64_t)f.ca;
+      fl += (int64_t)(s->n_var + 1) * s->E * ((2 * lgE + 1) * (int64_t)f.cm + f.ci);
+      fl += (int64_t)s->n_eq * s->seg_S * (s->n_var + 1) * (s->seg_W * TPW - 1) * (int64_t)f.ca;
+      fl += (int64_t)s->n_eq * (s->seg_S - 1) * (s->n_var + 1) * (int64_t)f.ca;
+    } else if (s->scan_ok && !s->common) {
       for (int64_t t = 0; t < s->n_terms; ++t) {
         const int64_t k = s->term_ptr[t + 1] - s->term_ptr[t];
         fl += 32 * 13 * (int64_t)f.cm + (k + 1) * f.ca;
@@ -1027,8 +1165,23 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
     out[12] = fl;
     out[13] = s->scan_ok && !s->common ? kScanMaxTerms : 0;
     out[14] = s->common ? 1 : 0;
+    const bool lat = s->scan_ok && !s->common;
+    out[15] = !lat ? 0 : s->seg_ok ? 2 : 1;
+    out[16] = lat && s->seg_ok ? s->seg_G : 0;
+    out[17] = !lat ? 0 : s->seg_ok ? 2 : 1;  // segmented: the power table, then the kernel
   }
   return PHC_OK;
 }
+
+#if PHC_SEG_TRACE
+// diagnostic builds only (PHC_SEG_TRACE): the per-CTA phase stamps of the last segmented call
+int phc_debug_seg_trace(unsigned long long* out, int n_ctas) {
+  if (cudaDeviceSynchronize() != cudaSuccess) return PHC_ECUDA;
+  n_ctas = std::min(n_ctas, 4096);
+  if (cudaMemcpyFromSymbol(out, phc::g_seg_trace, (size_t)n_ctas * 8 * sizeof(unsigned long long)) != cudaSuccess)
+    return PHC_ECUDA;
+  return PHC_OK;
+}
+#endif
 
 }  // extern "C"

@@ -95,6 +95,9 @@ struct DeviceState {
   int64_t part_cap = 0;
   int* count = nullptr;  // arrival counters (zeroed at allocation; each call leaves them zero)
   int64_t count_cap = 0;
+  // segmented latency path: the global power table of the call's points
+  double* segPT = nullptr;
+  int64_t segPT_cap = 0;
   // staging buffers for remote shards
   double* xs = nullptr;
   double* fs = nullptr;
@@ -107,7 +110,7 @@ struct DeviceState {
                     (void*)Y, (void*)G, (void*)xs, (void*)fs, (void*)js, (void*)ts, (void*)bt.fac, (void*)bt.coeff,
                     (void*)bt.blk, (void*)bt.PT, (void*)coeff2, (void*)bt.coeff2, (void*)cl_ptr, (void*)cl_j,
                     (void*)cl_q, (void*)cT, (void*)part, (void*)count, (void*)cT2, (void*)nF, (void*)nJ,
-                    (void*)nM, (void*)nAux})
+                    (void*)nM, (void*)nAux, (void*)segPT})
       if (p) cudaFree(p);
     if (stream) cudaStreamDestroy(stream);
     if (stream2) cudaStreamDestroy(stream2);
@@ -139,6 +142,12 @@ struct phc_system {
   bool scan_ok = false;
   int scan_S = 1, scan_W = 8;
   size_t scan_smem = 0;
+  // segmented latency path (kernels_scan.cuh poly_seg_kernel, QD): G lanes per term (two
+  // factors per lane), W warps per CTA, S splits per polynomial; takes the place of the
+  // warp-scan path when seg_ok
+  bool seg_ok = false;
+  int seg_G = 0, seg_W = 2, seg_S = 1;
+  size_t seg_smem = 0;
   std::vector<int64_t> cl_ptr, cl_q;
   std::vector<int32_t> cl_j;
   std::vector<double> cT;

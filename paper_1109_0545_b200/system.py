@@ -98,7 +98,7 @@ class System:
     def stats(self):
         keys = ("n_terms", "n_factors", "kmax", "D", "nnz_J", "cm_per_point", "ca_per_point", "launches",
                 "exec_flops_per_point", "path", "layout", "K", "latency_exec_flops_per_point", "latency_bound",
-                "common")
+                "common", "latency_kernel", "latency_G", "latency_launches")
         return dict(zip(keys, _lib.phc_system_stats(self._h)))
 
     def _check(self, t, shape):
