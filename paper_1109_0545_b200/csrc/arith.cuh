@@ -197,7 +197,11 @@ PHC_DEV qd renorm4_robust(double a0, double a1, double a2, double a3) {
 // order-3 products by FMA; level l collects the order-l terms with exact two_sum chains
 // whose errors move to level l+1; level 3 is a plain sum.  Normwise error ~2^-208
 // relative to |x||y| + |z||w| (checked in exact emulation).
-PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
+// The levels' sums (a0, a1, a2, o) whose exact sum is x*y + z*w to ~2^-208 normwise, not yet
+// renormalised: the "lazy" QD product (PHC_QD_LAZY) feeds them straight into the next product,
+// whose limb levels only need |level l| <~ u^l N (N = |x0 y0| + |z0 w0|), which they satisfy by
+// construction even after cancellation in a0; renorm4_robust makes them non-overlapping.
+PHC_DEV qd qd_dot2_parts(const qd& x, const qd& y, const qd& z, const qd& w) {
   double p0, q0, r0, t0;
   two_prod(x.x[0], y.x[0], p0, q0);
   two_prod(z.x[0], w.x[0], r0, t0);
@@ -266,7 +270,12 @@ PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
     const double hs = add_(add_(h0, h1), add_(h2, h3));
     o = add_(o, add_(add_(gs, hs), add_(add_(k0, k1), k2)));
   }
-  return renorm4_robust(a0, a1, a2, o);
+  qd r;
+  r.x[0] = a0;
+  r.x[1] = a1;
+  r.x[2] = a2;
+  r.x[3] = o;
+  return r;
 #else
   // level 1: e, q0, t0, p1, p2, r1, r2 -> a1, errors f1..f6 (order 2)
   double a1 = e, f1, f2, f3, f4, f5, f6;
@@ -293,8 +302,18 @@ PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
   two_sum(a2, r3, a2, g); o = add_(o, g);
   two_sum(a2, r4, a2, g); o = add_(o, g);
   two_sum(a2, r5, a2, g); o = add_(o, g);
-  return renorm4_robust(a0, a1, a2, o);
+  qd r;
+  r.x[0] = a0;
+  r.x[1] = a1;
+  r.x[2] = a2;
+  r.x[3] = o;
+  return r;
 #endif
+}
+
+PHC_DEV qd qd_dot2(const qd& x, const qd& y, const qd& z, const qd& w) {
+  const qd t = qd_dot2_parts(x, y, z, w);
+  return renorm4_robust(t.x[0], t.x[1], t.x[2], t.x[3]);
 }
 
 // ---------------------------------------------------------------------------
@@ -440,6 +459,8 @@ template <> struct Prec<2> {
     r.im.x[1] = add_(add_(a.im.x[1], b.im.x[1]), e);
     return r;
   }
+  // accumulator update with a lazy product (the lazy sum takes unnormalised operands)
+  PHC_DEV static C accum(const C& acc, const C& g) { return add_lazy(acc, g); }
   // renormalise a lazy value: (hi, lo) -> two_sum(hi, lo)
   PHC_DEV static C norm(const C& a) {
     C r;
@@ -498,9 +519,31 @@ template <> struct Prec<4> {
     r.im = qd_dot2(a.re, b.im, a.im, b.re);
     return r;
   }
+#ifndef PHC_QD_LAZY
+#define PHC_QD_LAZY 1
+#endif
+#if PHC_QD_LAZY
+  // lazy product: the dot products' level sums without the final renormalisation (qd_dot2_parts);
+  // a lazy value may only feed another product, norm() or accum()
+  PHC_DEV static C mul_lazy(const C& a, const C& b) {
+    C r;
+    r.re = qd_dot2_parts(a.re, b.re, qd_neg(a.im), b.im);
+    r.im = qd_dot2_parts(a.re, b.im, a.im, b.re);
+    return r;
+  }
+  PHC_DEV static C norm(const C& a) {
+    C r;
+    r.re = renorm4_robust(a.re.x[0], a.re.x[1], a.re.x[2], a.re.x[3]);
+    r.im = renorm4_robust(a.im.x[0], a.im.x[1], a.im.x[2], a.im.x[3]);
+    return r;
+  }
+#else
   PHC_DEV static C mul_lazy(const C& a, const C& b) { return mul(a, b); }
-  PHC_DEV static C add_lazy(const C& a, const C& b) { return add(a, b); }
   PHC_DEV static C norm(const C& a) { return a; }
+#endif
+  PHC_DEV static C add_lazy(const C& a, const C& b) { return add(a, b); }
+  // accumulator update with a (possibly lazy) product: qd_add needs normalised operands
+  PHC_DEV static C accum(const C& acc, const C& g) { return add(acc, norm(g)); }
   PHC_DEV static real mul_int_real(const real& a, double s) {
     // a_j * s = p_j + e_j exactly; collect by order of magnitude
     double p0, p1, p2, p3, e0, e1, e2;

@@ -108,10 +108,12 @@ struct HostBlockPlan {
 // counted from arith.cuh (and checked against ncu's sm__sass_thread_inst_executed_op_d*):
 // complex mul, lazy complex mul, complex add, lazy complex add, renormalisation,
 // complex times small integer.
-struct OpFlops { int cm, cm_lazy, ca, ca_lazy, norm, ci; };
+// complex times small integer, renormalisation of a lazy product inside an accumulator update.
+struct OpFlops { int cm, cm_lazy, ca, ca_lazy, norm, ci, acc_norm; };
 inline OpFlops op_flops(int L) {
-  if (L == 2) return {50, 44, 22, 16, 12, 16};
-  return {468, 468, 183, 183, 0, 130};
+  if (L == 2) return {50, 44, 22, 16, 12, 16, 0};
+  if (PHC_QD_LAZY) return {468, 408, 183, 183, 60, 130, 60};
+  return {468, 468, 183, 183, 0, 130, 0};
 }
 
 struct BlockArgs {
@@ -309,22 +311,22 @@ PHC_DEV typename Prec<L>::C do_block(const BlockArgs& a, int64_t b, const double
       const double2 q1 = *reinterpret_cast<const double2*>(r1);
       C acc;
       acc.re.x[0] = q0.x; acc.re.x[1] = q0.y; acc.im.x[0] = q1.x; acc.im.x[1] = q1.y;
-      acc = P::add_lazy(acc, g);
+      acc = P::accum(acc, g);
       *reinterpret_cast<double2*>(r0) = make_double2(acc.re.x[0], acc.re.x[1]);
       *reinterpret_cast<double2*>(r1) = make_double2(acc.im.x[0], acc.im.x[1]);
     } else if constexpr (junk) {
       const int vr = PHC_L2_PREDECODE ? (int)(word >> 16) : ((v == kDummyVar) ? a.n_var : (int)v);
       PHC_CHECK(vr <= a.n_var);
       double2* rw = reinterpret_cast<double2*>(rows);
-      cls_store<L>(rw, RS, vr, cls, P::add_lazy(cls_load<L>(rw, RS, vr, cls), g));
+      cls_store<L>(rw, RS, vr, cls, P::accum(cls_load<L>(rw, RS, vr, cls), g));
     } else if (v != kDummyVar) {
       PHC_CHECK(v < (uint32_t)a.n_var && (LAYOUT == 2 || (word >> 24) < (uint32_t)a.R));
       if constexpr (LAYOUT == 2) {
         double2* rw = reinterpret_cast<double2*>(rows);
-        cls_store<L>(rw, RS, (int)v, cls, P::add_lazy(cls_load<L>(rw, RS, (int)v, cls), g));
+        cls_store<L>(rw, RS, (int)v, cls, P::accum(cls_load<L>(rw, RS, (int)v, cls), g));
       } else {
         const size_t idx = (size_t)(word >> 24) * a.n_var + v;
-        row_st<L>(rows, idx, P::add_lazy(row_ld<L>(rows, idx), g));
+        row_st<L>(rows, idx, P::accum(row_ld<L>(rows, idx), g));
       }
     }
     __syncwarp();
@@ -875,7 +877,7 @@ void plan_blocks(const S& s, HostBlockPlan* plan) {
     int64_t fl = (int64_t)s.n_var * std::max(0, E - 1) * (f.cm + f.ci);  // power table
     for (int64_t t = 0; t < s.n_terms; ++t) {
       const int64_t k = s.term_ptr[t + 1] - s.term_ptr[t];
-      if (k >= 1) fl += (4 * k - 3) * f.cm_lazy + k * f.ca_lazy;
+      if (k >= 1) fl += (4 * k - 3) * f.cm_lazy + k * (f.ca_lazy + f.acc_norm);
     }
     fl += nb * kWarp * (2 * f.norm + 5 * f.ca_lazy);  // warp shuffle tree of each block's term values
     const int parts = plan->layout == 2 ? kClasses : R;

@@ -62,7 +62,7 @@ __global__ void coef_product_kernel(const int64_t* __restrict__ cl_ptr, const in
         C c = cload<L>(crow + u * cd);
         if (cT2)  // homotopy (NEXT-3): c(t) = (1 - t) c_s + t c_f
           c = P::add(P::mul_real(c, omt), P::mul_real(cload<L>(cT2 + ((int64_t)j * n_eq + i0 + u) * cd), tt));
-        acc[u] = P::add_lazy(acc[u], P::mul_lazy(c, val));
+        acc[u] = P::accum(acc[u], P::mul_lazy(c, val));
       }
   }
 #pragma unroll
@@ -165,7 +165,7 @@ __global__ void coef_product_pt_kernel(const int64_t* __restrict__ cl_ptr, const
       if (i0 + u < n_eq) {
         C cf = cload<L>(crow + u * cd);
         if (cT2) cf = P::add(P::mul_real(cf, omt), P::mul_real(cload<L>(cT2 + ((int64_t)j * n_eq + i0 + u) * cd), tt));
-        acc[u] = P::add_lazy(acc[u], P::mul_lazy(cf, val));
+        acc[u] = P::accum(acc[u], P::mul_lazy(cf, val));
       }
   }
 #pragma unroll
@@ -215,7 +215,7 @@ __global__ void coef_product_split_kernel(const int64_t* __restrict__ cl_ptr, co
     const C val = (c == 0) ? cload<L>(Yp + (int64_t)j * cd) : cload<L>(Gp + cl_q[e] * cd);
     C cf = cload<L>(cT + ((int64_t)j * n_eq + i) * cd);
     if (cT2) cf = P::add(P::mul_real(cf, omt), P::mul_real(cload<L>(cT2 + ((int64_t)j * n_eq + i) * cd), tt));
-    acc = P::add_lazy(acc, P::mul_lazy(cf, val));
+    acc = P::accum(acc, P::mul_lazy(cf, val));
   }
 #pragma unroll
   for (int d = 16; d >= 1; d >>= 1) {

@@ -1121,7 +1121,7 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
   } else if (s->common) {
     const phc::OpFlops f = phc::op_flops(s->L);
     const int64_t mono_cm = s->cm_per_point - s->ca_per_point;  // monomial stage + power table products
-    out[8] = mono_cm * f.cm + (int64_t)s->n_var * std::max(0, s->E - 1) * f.ci + s->ca_per_point * (f.cm_lazy + f.ca_lazy) +
+    out[8] = mono_cm * f.cm + (int64_t)s->n_var * std::max(0, s->E - 1) * f.ci + s->ca_per_point * (f.cm_lazy + f.ca_lazy + f.acc_norm) +
              (int64_t)s->n_eq * (s->n_var + 1) * f.norm;
   } else {
     const phc::OpFlops f = phc::op_flops(s->L);
