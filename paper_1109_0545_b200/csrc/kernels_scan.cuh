@@ -73,6 +73,16 @@ __device__ __noinline__ CPair<L> cmul2_ool(const typename Prec<L>::C a1, const t
   r.b = Prec<L>::mul(a2, b2);
   return r;
 }
+// the same with lazy products (QD: the level sums, not renormalised; arith.cuh) for chains
+// whose values only feed further products -- the segmented kernel renormalises what it stores
+template <int L>
+__device__ __noinline__ CPair<L> cmul2l_ool(const typename Prec<L>::C a1, const typename Prec<L>::C b1,
+                                            const typename Prec<L>::C a2, const typename Prec<L>::C b2) {
+  CPair<L> r;
+  r.a = Prec<L>::mul_lazy(a1, b1);
+  r.b = Prec<L>::mul_lazy(a2, b2);
+  return r;
+}
 template <int L>
 PHC_DEV typename Prec<L>::C smul(const typename Prec<L>::C& a, const typename Prec<L>::C& b) {
   if constexpr (L == 4) return cmul_ool<L>(a, b);
@@ -377,10 +387,10 @@ __global__ void __launch_bounds__(kSegMaxWarps * 32) poly_seg_kernel(const ScanA
     }
     const C u0 = cload<L>(pt + (size_t)eu[0] * cd), u1 = cload<L>(pt + (size_t)eu[1] * cd);
     const C d0 = cload<L>(pt + (size_t)(eu[0] + a.E) * cd), d1 = cload<L>(pt + (size_t)(eu[1] + a.E) * cd);
-    // every product goes through the one out-of-line pair product: its code (~14 KB) stays in
-    // the 32 KB L1.5 instruction cache, where a three-product function (~22 KB) next to it
-    // missed on every call (ncu: no_instruction 463 of its 820 stall samples)
-    CPair<L> r = cmul2_ool<L>(u0, u1, d0, u1);
+    // every product goes through the one out-of-line (lazy) pair product: its code (~12 KB)
+    // stays in the 32 KB L1.5 instruction cache, where a three-product function (~22 KB) next
+    // to it missed on every call (ncu: no_instruction 463 of its 820 stall samples)
+    CPair<L> r = cmul2l_ool<L>(u0, u1, d0, u1);
     const C T = r.a, Q0 = r.b;  // T = u0 u1, Q0 = d0 u1
     // inclusive scans of the shifted values: the prefix of (c, T_0, .., T_{G-2}) over the
     // segment is M = c * (product of the factors before the lane), the suffix of
@@ -391,16 +401,16 @@ __global__ void __launch_bounds__(kSegMaxWarps * 32) poly_seg_kernel(const ScanA
 #pragma unroll 1
     for (int off = 1; off < G; off <<= 1) {
       const C x1 = shfl_c<L>(pre, off, true), x2 = shfl_c<L>(suf, off, false);
-      r = cmul2_ool<L>(g >= off ? x1 : P::one(), pre, suf, g + off < G ? x2 : P::one());
+      r = cmul2l_ool<L>(g >= off ? x1 : P::one(), pre, suf, g + off < G ? x2 : P::one());
       pre = r.a;
       suf = r.b;
     }
     const C M = pre;
-    r = cmul2_ool<L>(Q0, suf, d1, suf);  // R0 = Q0 after, X1 = d1 after
-    r = cmul2_ool<L>(M, r.a, u0, r.b);   // g0 = M R0, R1 = u0 X1
-    const C g0 = r.a;
-    r = cmul2_ool<L>(M, r.b, M, T);      // g1 = M R1, y = M T (the term's value on the last lane)
-    const C g1 = r.a, y = r.b;
+    r = cmul2l_ool<L>(Q0, suf, d1, suf);  // R0 = Q0 after, X1 = d1 after
+    r = cmul2l_ool<L>(M, r.a, u0, r.b);   // g0 = M R0, R1 = u0 X1
+    const C g0 = P::norm(r.a);
+    r = cmul2l_ool<L>(M, r.b, M, T);      // g1 = M R1, y = M T (the term's value on the last lane)
+    const C g1 = P::norm(r.a), y = P::norm(r.b);
     PHC_SEG_STAMP(2)
     // accumulate the gradients into the slot's rows (entry index relative to `rows`: the
     // swizzle depends on it)

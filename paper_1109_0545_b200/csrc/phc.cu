@@ -1137,16 +1137,17 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
     const phc::OpFlops f = phc::op_flops(s->L);
     int64_t fl = 0;
     if (s->seg_ok && !s->common) {
-      // segmented path: per warp-task (32 / G terms) 8 + 2 ceil(log2 G) products on all
-      // 32 lanes, one addition per factor and per term; the global power table once per point
-      // (<= 2 log2(E) + 1 products and one integer scaling per entry); the epilogue's additions
+      // segmented path: per warp-task (32 / G terms) 8 + 2 ceil(log2 G) lazy products and three
+      // renormalisations on all 32 lanes, one addition per factor and per term; the global
+      // power table once per point (<= 2 log2(E) + 1 products and one integer scaling per
+      // entry); the epilogue's additions
       int lg = 0, lgE = 0;
       while ((1 << lg) < s->seg_G) ++lg;
       while ((1 << lgE) < s->E) ++lgE;
       const int TPW = 32 / s->seg_G;
       for (int i = 0; i < s->n_eq; ++i) {
         const int64_t nt = s->poly_ptr[i + 1] - s->poly_ptr[i];
-        fl += (nt + TPW - 1) / TPW * 32 * (8 + 2 * lg) * (int64_t)f.cm;
+        fl += (nt + TPW - 1) / TPW * 32 * ((8 + 2 * lg) * (int64_t)f.cm_lazy + 3 * (int64_t)f.norm);
       }
       fl += (s->n_factors + s->n_terms) * (int64_t)f.ca;
       fl += (int64_t)(s->n_var + 1) * s->E * ((2 * lgE + 1) * (int64_t)f.cm + f.ci);
