@@ -112,6 +112,7 @@ struct HostBlockPlan {
 struct OpFlops { int cm, cm_lazy, ca, ca_lazy, norm, ci, acc_norm; };
 inline OpFlops op_flops(int L) {
   if (L == 2) return {50, 44, 22, 16, 12, 16, 0};
+  if (PHC_QD_LAZY && PHC_QD_LAZY_ACC) return {468, 408, 183, 82, 60, 130, 0};
   if (PHC_QD_LAZY) return {468, 408, 183, 183, 60, 130, 60};
   return {468, 468, 183, 183, 0, 130, 0};
 }
