@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
 //        (inclusive scans of the shifted T: ceil(log2 G) steps of 2 products)
 //   g_0 = M (Q_0 after),  g_1 = M (u_0 (d_1 after)),  y = M T   (6 products; y on the
 //   segment's last lane is the term's value)
+// Products and sums are lazy QD values (arith.cuh qd_dot2_parts / qd_add_levels), renormalised
+// when F and J are stored.
 // The prefix/suffix products are the paper's psi/phi (§6) over the segment's
 // lanes, the lane's own factors combined as in a two-factor Speelpenning product, the
 // coefficient folded into the prefix (reading C3): 8 + 2 ceil(log2 G) products per lane in
@@ -294,18 +296,19 @@ PHC_DEV typename Prec<L>::C shfl_idx(const typename Prec<L>::C& v, int src) {
   }
   return r;
 }
-// one out-of-line complex addition (the kernel adds in several places; one copy of the code),
-// and two independent ones in one call
+// one out-of-line lazy complex addition (QD: level-wise, arith.cuh qd_add_levels; the kernel
+// adds in several places, one copy of the code), and two independent ones in one call; sums are
+// renormalised when they are stored
 template <int L>
 __device__ __noinline__ typename Prec<L>::C cadd_ool(const typename Prec<L>::C a, const typename Prec<L>::C b) {
-  return Prec<L>::add(a, b);
+  return Prec<L>::add_lazy(a, b);
 }
 template <int L>
 __device__ __noinline__ CPair<L> cadd2_ool(const typename Prec<L>::C a1, const typename Prec<L>::C b1,
                                            const typename Prec<L>::C a2, const typename Prec<L>::C b2) {
   CPair<L> r;
-  r.a = Prec<L>::add(a1, b1);
-  r.b = Prec<L>::add(a2, b2);
+  r.a = Prec<L>::add_lazy(a1, b1);
+  r.b = Prec<L>::add_lazy(a2, b2);
   return r;
 }
 template <int L, int G>
@@ -408,9 +411,9 @@ __global__ void __launch_bounds__(kSegMaxWarps * 32) poly_seg_kernel(const ScanA
     const C M = pre;
     r = cmul2l_ool<L>(Q0, suf, d1, suf);  // R0 = Q0 after, X1 = d1 after
     r = cmul2l_ool<L>(M, r.a, u0, r.b);   // g0 = M R0, R1 = u0 X1
-    const C g0 = P::norm(r.a);
+    const C g0 = r.a;
     r = cmul2l_ool<L>(M, r.b, M, T);      // g1 = M R1, y = M T (the term's value on the last lane)
-    const C g1 = P::norm(r.a), y = P::norm(r.b);
+    const C g1 = r.a, y = r.b;
     PHC_SEG_STAMP(2)
     // accumulate the gradients into the slot's rows (entry index relative to `rows`: the
     // swizzle depends on it)
@@ -445,9 +448,9 @@ __global__ void __launch_bounds__(kSegMaxWarps * 32) poly_seg_kernel(const ScanA
       acc = cadd_ool<L>(acc, col < nv ? row_ld<L>(rows, (size_t)q * nv + col) : sload<L>(fpart + (size_t)q * cd));
     if (direct) {
       if (col < nv)
-        cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)nv + col) * cd, acc);
+        cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)nv + col) * cd, P::norm(acc));
       else
-        cstore<L>(a.F + (p * a.n_eq + i) * cd, acc);
+        cstore<L>(a.F + (p * a.n_eq + i) * cd, P::norm(acc));
     } else {
       cstore<L>(a.part + (((p * a.n_eq + i) * a.S + s) * (int64_t)(nv + 1) + col) * cd, acc);
     }
@@ -470,9 +473,9 @@ __global__ void __launch_bounds__(kSegMaxWarps * 32) poly_seg_kernel(const ScanA
     C acc = cload_cg<L>(src + (size_t)col * cd);
     for (int q = 1; q < a.S; ++q) acc = cadd_ool<L>(acc, cload_cg<L>(src + ((size_t)q * (nv + 1) + col) * cd));
     if (col < nv)
-      cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)nv + col) * cd, acc);
+      cstore<L>(a.J + ((p * a.n_eq + i) * (int64_t)nv + col) * cd, P::norm(acc));
     else
-      cstore<L>(a.F + (p * a.n_eq + i) * cd, acc);
+      cstore<L>(a.F + (p * a.n_eq + i) * cd, P::norm(acc));
   }
   if (threadIdx.x == 0) a.count[p * a.n_eq + i] = 0;  // ready for the next call
   __syncthreads();

@@ -1137,22 +1137,22 @@ int phc_system_stats(const phc_system* s, int64_t out[PHC_STATS_LEN]) {
     const phc::OpFlops f = phc::op_flops(s->L);
     int64_t fl = 0;
     if (s->seg_ok && !s->common) {
-      // segmented path: per warp-task (32 / G terms) 8 + 2 ceil(log2 G) lazy products and three
-      // renormalisations on all 32 lanes, one addition per factor and per term; the global
-      // power table once per point (<= 2 log2(E) + 1 products and one integer scaling per
-      // entry); the epilogue's additions
+      // segmented path: per warp-task (32 / G terms) 8 + 2 ceil(log2 G) lazy products on all
+      // 32 lanes (the first task of a slot stores its partials, no addition); the global power
+      // table once per point (<= 2 log2(E) + 1 products and one integer scaling per entry); the
+      // epilogue's lazy additions and one renormalisation per stored entry
       int lg = 0, lgE = 0;
       while ((1 << lg) < s->seg_G) ++lg;
       while ((1 << lgE) < s->E) ++lgE;
       const int TPW = 32 / s->seg_G;
       for (int i = 0; i < s->n_eq; ++i) {
         const int64_t nt = s->poly_ptr[i + 1] - s->poly_ptr[i];
-        fl += (nt + TPW - 1) / TPW * 32 * ((8 + 2 * lg) * (int64_t)f.cm_lazy + 3 * (int64_t)f.norm);
+        fl += (nt + TPW - 1) / TPW * 32 * (8 + 2 * lg) * (int64_t)f.cm_lazy;
       }
-      fl += (s->n_factors + s->n_terms) * (int64_t)f.ca;
       fl += (int64_t)(s->n_var + 1) * s->E * ((2 * lgE + 1) * (int64_t)f.cm + f.ci);
-      fl += (int64_t)s->n_eq * s->seg_S * (s->n_var + 1) * (s->seg_W * TPW - 1) * (int64_t)f.ca;
-      fl += (int64_t)s->n_eq * (s->seg_S - 1) * (s->n_var + 1) * (int64_t)f.ca;
+      fl += (int64_t)s->n_eq * s->seg_S * (s->n_var + 1) * (s->seg_W * TPW - 1) * (int64_t)f.ca_lazy;
+      fl += (int64_t)s->n_eq * (s->seg_S - 1) * (s->n_var + 1) * (int64_t)f.ca_lazy;
+      fl += (int64_t)s->n_eq * (s->n_var + 1) * (int64_t)f.norm;
     } else if (s->scan_ok && !s->common) {
       for (int64_t t = 0; t < s->n_terms; ++t) {
         const int64_t k = s->term_ptr[t + 1] - s->term_ptr[t];
