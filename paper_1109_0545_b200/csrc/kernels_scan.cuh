@@ -243,7 +243,6 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
   if (threadIdx.x == 0) a.count[p * a.n_eq + i] = 0;  // ready for the next call
 }
 
-
 // ---------------------------------------------------------------------------
 // Segmented latency path (DESIGN.md §4 "segmented latency path"): the same evaluation as
 // poly_scan_kernel with G lanes per term instead of 32, so a warp carries TPW = 32 / G terms
@@ -254,8 +253,6 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
 //        (inclusive scans of the shifted T: ceil(log2 G) steps of 2 products)
 //   g_0 = M (Q_0 after),  g_1 = M (u_0 (d_1 after)),  y = M T   (6 products; y on the
 //   segment's last lane is the term's value)
-// Products and sums are lazy QD values (arith.cuh qd_dot2_parts / qd_add_levels), renormalised
-// when F and J are stored.
 // The prefix/suffix products are the paper's psi/phi (§6) over the segment's
 // lanes, the lane's own factors combined as in a two-factor Speelpenning product, the
 // coefficient folded into the prefix (reading C3): 8 + 2 ceil(log2 G) products per lane in
@@ -265,7 +262,8 @@ __global__ void __launch_bounds__(256) poly_scan_kernel(const ScanArgs a) {
 // of a programmatic dependent launch).  Accumulation: per (warp, term slot) shared-memory rows
 // (the variables of one term are distinct; different slots own different rows), summed in a
 // fixed order, then the S split partial rows as in poly_scan_kernel: bitwise reproducible for
-// a given system.
+// a given system.  Products and sums are lazy QD values (arith.cuh qd_dot2_parts /
+// qd_add_levels, reading R4), renormalised when F and J are stored.
 constexpr int kSegMaxWarps = 8;
 // PHC_SEG_TRACE (diagnostic builds only): per-CTA %globaltimer stamps of the kernel's phases
 // (start, table ready, products done, rows summed, end; then the SM id), read back with
@@ -275,7 +273,6 @@ constexpr int kSegMaxWarps = 8;
 #endif
 #if PHC_SEG_TRACE
 __device__ unsigned long long g_seg_trace[4096][8];
-__device__ unsigned long long g_tab_trace[64][2];
 #define PHC_SEG_STAMP(k)                                                   \
   if (threadIdx.x == 0 && blockIdx.x < 4096) {                             \
     unsigned long long t_;                                                 \
