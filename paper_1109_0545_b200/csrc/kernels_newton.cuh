@@ -35,10 +35,49 @@ __device__ __forceinline__ double nan_max(double a, double b) { return (b != b |
 // operations, so the value is bitwise P::recip(a) -- and every lane receives the result.  The
 // two long divisions then run side by side instead of interleaved in one thread.
 // Call with the full warp converged.
+// The eliminations' arithmetic, shared by every kernel below so that all of them form the
+// same operations in the same order.  PHC_NEWTON_LAZY: products and differences are lazy
+// values (arith.cuh: DD (hi, lo) unnormalised, QD level expansions), renormalised where a
+// value is divided by (the pivot) or leaves the elimination (dz); pivots are compared by the
+// leading part of the value (the sum of its limbs in binary64).
+#ifndef PHC_NEWTON_LAZY
+#define PHC_NEWTON_LAZY 0
+#endif
 template <int L>
-PHC_DEV typename Prec<L>::C recip_warp(const typename Prec<L>::C& a, int lane) {
+PHC_DEV typename Prec<L>::C emul(const typename Prec<L>::C& a, const typename Prec<L>::C& b) {
+  if constexpr (PHC_NEWTON_LAZY) return Prec<L>::mul_lazy(a, b);
+  else return Prec<L>::mul(a, b);
+}
+template <int L>
+PHC_DEV typename Prec<L>::C efms(const typename Prec<L>::C& c, const typename Prec<L>::C& a,
+                                 const typename Prec<L>::C& b) {
+  if constexpr (PHC_NEWTON_LAZY) return Prec<L>::add_lazy(c, Prec<L>::neg(Prec<L>::mul_lazy(a, b)));
+  else return Prec<L>::sub(c, Prec<L>::mul(a, b));
+}
+template <int L>
+PHC_DEV typename Prec<L>::C enorm(const typename Prec<L>::C& a) {
+  if constexpr (PHC_NEWTON_LAZY) return Prec<L>::norm(a);
+  else return a;
+}
+template <int L>
+PHC_DEV double ehi2(const typename Prec<L>::C& a) {
+  if constexpr (PHC_NEWTON_LAZY) {
+    double re = a.re.x[L - 1], im = a.im.x[L - 1];
+#pragma unroll
+    for (int i = L - 2; i >= 0; --i) {
+      re += a.re.x[i];
+      im += a.im.x[i];
+    }
+    return re * re + im * im;
+  } else {
+    return Prec<L>::abs2_hi(a);
+  }
+}
+template <int L>
+PHC_DEV typename Prec<L>::C recip_warp(const typename Prec<L>::C& a_in, int lane) {
   using P = Prec<L>;
   typename P::C r;
+  const typename P::C a = enorm<L>(a_in);
   const typename P::real d = P::abs2(a);
   const typename P::real q = P::rdiv((lane & 1) ? a.im : a.re, d);
 #pragma unroll
@@ -155,7 +194,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     double best = -1.0;
     int bi = n;
     for (int i = c + lane; i < n; i += 32) {
-      const double v = P::abs2_hi(ldE(src[i], c));
+      const double v = ehi2<L>(ldE(src[i], c));
       if (v > best) { best = v; bi = i; }
     }
     for (int o = 16; o; o >>= 1) {
@@ -168,7 +207,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     __syncwarp();
     const C inv = recip_warp<L>(ldE(dst[c], c), lane);
     if (lane == 0) sstore<L>(invd + (size_t)c * cd, inv);
-    for (int i = c + 1 + lane; i < n; i += 32) stE(dst[i], c, P::mul(ldE(dst[i], c), inv));
+    for (int i = c + 1 + lane; i < n; i += 32) stE(dst[i], c, emul<L>(ldE(dst[i], c), inv));
     return true;
   };
   int cur = 0;  // pbuf + cur * n: the permutation after the exchanges of columns < k + 1
@@ -182,7 +221,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       // look-ahead: column k+1 of the rows below k, then its pivot, exchange, multipliers
       const C pk = ldE(pc[k], k + 1);
       for (int i = k + 1 + lane; i < n; i += 32)
-        stE(pc[i], k + 1, P::sub(ldE(pc[i], k + 1), P::mul(ldE(pc[i], k), pk)));
+        stE(pc[i], k + 1, efms<L>(ldE(pc[i], k + 1), ldE(pc[i], k), pk));
       __syncwarp();
       if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad[(k + 1) & 1] = 1;
     } else if ((wid & 3) != 0 || nwarp <= 4) {
@@ -194,7 +233,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       for (int e = worker * 32 + lane; e < rows * ucols; e += nworker * 32) {
         const int i = k + 1 + e / ucols, j = k + 2 + e % ucols;
         const int r = pc[i];
-        stE(r, j, P::sub(ldE(r, j), P::mul(ldE(r, k), ldE(pr, j))));
+        stE(r, j, efms<L>(ldE(r, j), ldE(r, k), ldE(pr, j)));
       }
     }
     __syncthreads();
@@ -209,16 +248,16 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   // back substitution: x_i = M[i][n] / M[i][i], then M[r][n] -= M[r][i] x_i for r < i
   const int* pf = pbuf + cur * n;
   for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) stE(pf[i], n, P::mul(ldE(pf[i], n), sload<L>(invd + (size_t)i * cd)));
+    if (tid == 0) stE(pf[i], n, emul<L>(ldE(pf[i], n), sload<L>(invd + (size_t)i * cd)));
     __syncthreads();
     const C xi = ldE(pf[i], n);
-    for (int r = tid; r < i; r += T) stE(pf[r], n, P::sub(ldE(pf[r], n), P::mul(ldE(pf[r], i), xi)));
+    for (int r = tid; r < i; r += T) stE(pf[r], n, efms<L>(ldE(pf[r], n), ldE(pf[r], i), xi));
     __syncthreads();
   }
   // z := z + dz
   for (int e = tid; e < n; e += T) {
     const double* xp = a.X + ((size_t)p * n + e) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), ldE(pf[e], n)));
+    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(ldE(pf[e], n))));
   }
   if (tid == 0) a.status[p] = 0;
 }
@@ -311,7 +350,7 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     double best = -1.0;
     int bi = n;
     if (lane >= k && lane < n) {
-      best = P::abs2_hi(ldE(lane, k));
+      best = ehi2<L>(ldE(lane, k));
       bi = lane;
     }
     for (int o = 16; o; o >>= 1) {
@@ -334,7 +373,7 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     __syncwarp();
     const C inv = recip_warp<L>(ldE(k, k), lane);
     if (lane == k) inv_diag = inv;
-    if (lane > k && lane < n) stE(lane, k, P::mul(ldE(lane, k), inv));
+    if (lane > k && lane < n) stE(lane, k, emul<L>(ldE(lane, k), inv));
     __syncwarp();
     // trailing update spread over the lanes by (row, column) pairs: ceil((n-k-1)(n-k) / 32)
     // entries per lane instead of a whole row of n-k entries
@@ -342,21 +381,21 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     const int ne = (n - k - 1) * w;
     for (int e = lane; e < ne; e += 32) {
       const int i = k + 1 + e / w, j = k + 1 + e % w;
-      stE(i, j, P::sub(ldE(i, j), P::mul(ldE(i, k), ldE(k, j))));
+      stE(i, j, efms<L>(ldE(i, j), ldE(i, k), ldE(k, j)));
     }
     __syncwarp();
   }
   // back substitution, column oriented as in newton_solve_kernel
   for (int i = n - 1; i >= 0; --i) {
-    if (lane == i) stE(i, n, P::mul(ldE(i, n), inv_diag));
+    if (lane == i) stE(i, n, emul<L>(ldE(i, n), inv_diag));
     __syncwarp();
     const C xi = ldE(i, n);
-    if (lane < i) stE(lane, n, P::sub(ldE(lane, n), P::mul(ldE(lane, i), xi)));
+    if (lane < i) stE(lane, n, efms<L>(ldE(lane, n), ldE(lane, i), xi));
     __syncwarp();
   }
   if (lane < n) {
     const double* xp = a.X + ((size_t)p * n + lane) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), ldE(lane, n)));
+    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), enorm<L>(ldE(lane, n))));
   }
   if (lane == 0) a.status[p] = 0;
 }
@@ -425,7 +464,7 @@ __global__ void __launch_bounds__(256) newton_pivot_kernel(const NewtonArgs a, i
   double best = -1.0;
   int bi = n;
   for (int i = k + tid; i < n; i += T) {
-    const double v = P::abs2_hi(sload<L>(at(i, k)));
+    const double v = ehi2<L>(sload<L>(at(i, k)));
     if (v > best) { best = v; bi = i; }
   }
   for (int o = 16; o; o >>= 1) {
@@ -463,7 +502,7 @@ __global__ void __launch_bounds__(256) newton_pivot_kernel(const NewtonArgs a, i
   }
   __syncthreads();
   const C inv = sload<L>(s_inv);
-  for (int i = k + 1 + tid; i < n; i += T) sstore<L>(at(i, k), P::mul(sload<L>(at(i, k)), inv));
+  for (int i = k + 1 + tid; i < n; i += T) sstore<L>(at(i, k), emul<L>(sload<L>(at(i, k)), inv));
 }
 
 template <int L>
@@ -478,7 +517,7 @@ __global__ void __launch_bounds__(256) newton_update_kernel(const NewtonArgs a, 
   const int i = k + 1 + (int)(e / ucols), j = k + 1 + (int)(e % ucols);
   double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
   auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
-  sstore<L>(at(i, j), P::sub(sload<L>(at(i, j)), P::mul(sload<L>(at(i, k)), sload<L>(at(k, j)))));
+  sstore<L>(at(i, j), efms<L>(sload<L>(at(i, j)), sload<L>(at(i, k)), sload<L>(at(k, j))));
 }
 
 template <int L>
@@ -498,15 +537,15 @@ __global__ void __launch_bounds__(256) newton_backsub_kernel(const NewtonArgs a)
   double* invd = M + (size_t)n * cols * cd;
   auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
   for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) sstore<L>(at(i, n), P::mul(sload<L>(at(i, n)), sload<L>(invd + (size_t)i * cd)));
+    if (tid == 0) sstore<L>(at(i, n), emul<L>(sload<L>(at(i, n)), sload<L>(invd + (size_t)i * cd)));
     __syncthreads();
     const C xi = sload<L>(at(i, n));
-    for (int r = tid; r < i; r += T) sstore<L>(at(r, n), P::sub(sload<L>(at(r, n)), P::mul(sload<L>(at(r, i)), xi)));
+    for (int r = tid; r < i; r += T) sstore<L>(at(r, n), efms<L>(sload<L>(at(r, n)), sload<L>(at(r, i)), xi));
     __syncthreads();
   }
   for (int e = tid; e < n; e += T) {
     const double* xp = a.X + ((size_t)p * n + e) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), sload<L>(at(e, n))));
+    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(sload<L>(at(e, n)))));
   }
 }
 
@@ -561,12 +600,12 @@ PHC_DEV unsigned long long gtime() {
 // c - a b and a b, as every elimination forms them
 template <int L>
 PHC_DEV typename Prec<L>::C cmul_c(const typename Prec<L>::C& a, const typename Prec<L>::C& b) {
-  return Prec<L>::mul(a, b);
+  return emul<L>(a, b);
 }
 template <int L>
 PHC_DEV typename Prec<L>::C cfms_c(const typename Prec<L>::C& c, const typename Prec<L>::C& a,
                                    const typename Prec<L>::C& b) {
-  return Prec<L>::sub(c, Prec<L>::mul(a, b));
+  return efms<L>(c, a, b);
 }
 constexpr int kCoopThreads = 256;
 constexpr int kCoopRows = 4;  // chain rows per thread of CTA 0: n <= 1 + 4 * 256
@@ -689,7 +728,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
         perm[i] = i;
         const C v = ldl2<L>(at(i, 0));
         sstore<L>(colv + (size_t)i * cd, v);
-        const double m = P::abs2_hi(v);
+        const double m = ehi2<L>(v);
         if (m > best) { best = m; bi = i; }
       }
       warp_candidates(best, bi);
@@ -714,7 +753,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
             const int ph = perm[i];
             const C v = cfms_c<L>(ldl2<L>(at(ph, k + 1)), cval(lmul, ph), uk);
             sstore<L>(colv + (size_t)ph * cd, v);
-            const double m = P::abs2_hi(v);
+            const double m = ehi2<L>(v);
             if (m > best) { best = m; bi = i; }
           }
         }
@@ -769,7 +808,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
         }
         for (int e = tid; e < n; e += T) {
           const double* xp = a.X + ((size_t)p * n + e) * cd;
-          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), ldl2<L>(at(perm[e], n))));
+          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(ldl2<L>(at(perm[e], n)))));
         }
         if (tid == 0) a.status[p] = 0;
       }
