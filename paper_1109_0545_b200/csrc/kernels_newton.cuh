@@ -29,6 +29,38 @@ namespace phc {
 // NaN, so a non-finite F always reaches resid[] and the !isfinite(r) exits in phc.h fire.
 __device__ __forceinline__ double nan_max(double a, double b) { return (b != b || b > a) ? b : a; }
 
+// Phase timeline of the eliminations (diagnostic build -DPHC_NEWTON_TRACE=1, tools/newton_phase.cu):
+// %globaltimer stamps of point 0 / CTA 0, thread 0: [0] solve kernel, [1] cooperative kernel;
+// stamps 0 start, 1 matrix loaded, 2 elimination done, 3 back substitution done.
+#ifndef PHC_NEWTON_TRACE
+#define PHC_NEWTON_TRACE 0
+#endif
+#if PHC_NEWTON_TRACE
+__device__ unsigned long long g_newton_phase[2][4];
+// per column of the solve kernel: [0] start, [1] look-ahead update done, [2] pivot, reciprocal
+// and multipliers done, [3] last trailing-update warp done (atomicMax), [4] after the barrier
+__device__ unsigned long long g_newton_cols[128][5];
+PHC_DEV unsigned long long ntime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define NEWTON_C(k, s, cond) \
+  if ((cond) && (k) < 128) g_newton_cols[k][s] = ntime();
+#define NEWTON_CMAX(k, s, cond) \
+  if ((cond) && (k) < 128) atomicMax(&g_newton_cols[k][s], ntime());
+#define NEWTON_T(kind, s, cond)                                               \
+  if (cond) {                                                                 \
+    unsigned long long t_;                                                    \
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                    \
+    g_newton_phase[kind][s] = t_;                                             \
+  }
+#else
+#define NEWTON_T(kind, s, cond)
+#define NEWTON_C(k, s, cond)
+#define NEWTON_CMAX(k, s, cond)
+#endif
+
 
 // The pivot reciprocal (the serial step of every elimination column) computed by a whole
 // warp: lane 0 divides the real part by |a|^2, lane 1 the imaginary part -- P::recip's own
@@ -86,6 +118,41 @@ PHC_DEV typename Prec<L>::C recip_warp(const typename Prec<L>::C& a_in, int lane
     r.im.x[i] = -__shfl_sync(0xffffffffu, q.x[i], 1);
   }
   return r;
+}
+
+// Back substitution, row-scaled, the same in every elimination: with
+// d_r = 1 / U[r][r] (the stored pivot reciprocals), one parallel pass forms
+//   c_r = b_r d_r  and  N[r][j] = U[r][j] d_r  (r < j < n),
+// then the sweep c_r -= N[r][j] x_j for j = n-1, ..., r+1 in that order, x_j = c_j once row j
+// has received all its terms.  Its dependent chain is one efms per row (the column-oriented
+// form had a product, an efms and two block barriers per row).
+//
+// sweep_warp: one warp, lane l holding rows l, l + 32, ... (R per lane, n <= 32 R) in registers,
+// x_j broadcast by shuffles: no block barriers.  ldN(r, j) reads N[r][j], ldC(r) the scaled c_r.
+template <int L, int R, class LdN, class LdC>
+PHC_DEV void sweep_warp(int n, int lane, LdN ldN, LdC ldC, typename Prec<L>::C (&c)[R]) {
+  using C = typename Prec<L>::C;
+#pragma unroll
+  for (int q = 0; q < R; ++q)
+    if (lane + 32 * q < n) c[q] = ldC(lane + 32 * q);
+  for (int j = n - 1; j >= 1; --j) {
+    const int oq = j >> 5, ol = j & 31;
+    C src = c[0];
+#pragma unroll
+    for (int q = 1; q < R; ++q)
+      if (oq == q) src = c[q];
+    C xj;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      xj.re.x[i] = __shfl_sync(0xffffffffu, src.re.x[i], ol);
+      xj.im.x[i] = __shfl_sync(0xffffffffu, src.im.x[i], ol);
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int r = lane + 32 * q;
+      if (r < j) c[q] = efms<L>(c[q], ldN(r, j), xj);
+    }
+  }
 }
 
 struct NewtonArgs {
@@ -164,6 +231,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   int* pbuf = reinterpret_cast<int*>(invd + (size_t)n * cd);  // [2][n] row permutations
   auto ldE = [&](int r, int c) { return plane_ld<L>(Mre, Mim, ((size_t)r * cols + c) * L); };
   auto stE = [&](int r, int c, const C& v) { plane_st<L>(Mre, Mim, ((size_t)r * cols + c) * L, v); };
+  NEWTON_T(0, 0, p == 0 && tid == 0)
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
   // load [J | -F]; residual max_i |F_i|; identity permutation
@@ -210,6 +278,7 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     for (int i = c + 1 + lane; i < n; i += 32) stE(dst[i], c, emul<L>(ldE(dst[i], c), inv));
     return true;
   };
+  NEWTON_T(0, 1, p == 0 && tid == 0)
   int cur = 0;  // pbuf + cur * n: the permutation after the exchanges of columns < k + 1
   if (wid == 0 && !pivot_column(pbuf, pbuf + n, 0) && lane == 0) s_bad[0] = 1;
   __syncthreads();
@@ -217,13 +286,16 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   for (int k = 0; k < n - 1 && !s_bad[k & 1]; ++k) {
     const int* pc = pbuf + cur * n;
     int* pn = pbuf + (cur ^ 1) * n;
+    NEWTON_C(k, 0, p == 0 && tid == 0)
     if (wid == 0) {
       // look-ahead: column k+1 of the rows below k, then its pivot, exchange, multipliers
       const C pk = ldE(pc[k], k + 1);
       for (int i = k + 1 + lane; i < n; i += 32)
         stE(pc[i], k + 1, efms<L>(ldE(pc[i], k + 1), ldE(pc[i], k), pk));
       __syncwarp();
+      NEWTON_C(k, 1, p == 0 && lane == 0)
       if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad[(k + 1) & 1] = 1;
+      NEWTON_C(k, 2, p == 0 && lane == 0)
     } else if ((wid & 3) != 0 || nwarp <= 4) {
       // trailing update M[i][j] -= l_i M[k][j], i > k, j > k + 1, off warp 0's SMSP
       const int worker = (nwarp > 4) ? (wid >> 2) * 3 + (wid & 3) - 1 : wid - 1;
@@ -235,8 +307,10 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
         const int r = pc[i];
         stE(r, j, efms<L>(ldE(r, j), ldE(r, k), ldE(pr, j)));
       }
+      NEWTON_CMAX(k, 3, p == 0 && lane == 0)
     }
     __syncthreads();
+    NEWTON_C(k, 4, p == 0 && tid == 0)
     cur ^= 1;
   }
   if (s_bad[0] | s_bad[1]) {
@@ -245,19 +319,31 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
       cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
     return;
   }
-  // back substitution: x_i = M[i][n] / M[i][i], then M[r][n] -= M[r][i] x_i for r < i
+  NEWTON_T(0, 2, p == 0 && tid == 0)
+  // back substitution (row-scaled, sweep_warp above): c_r = b_r d_r, N[r][j] = U[r][j] d_r
+  // in place, then warp 0 sweeps with the rows in registers
   const int* pf = pbuf + cur * n;
-  for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) stE(pf[i], n, emul<L>(ldE(pf[i], n), sload<L>(invd + (size_t)i * cd)));
-    __syncthreads();
-    const C xi = ldE(pf[i], n);
-    for (int r = tid; r < i; r += T) stE(pf[r], n, efms<L>(ldE(pf[r], n), ldE(pf[r], i), xi));
-    __syncthreads();
+  for (int e = tid; e < n * cols; e += T) {
+    const int r = e / cols, j = e % cols;
+    if (j > r) stE(pf[r], j, emul<L>(ldE(pf[r], j), sload<L>(invd + (size_t)r * cd)));
   }
-  // z := z + dz
-  for (int e = tid; e < n; e += T) {
-    const double* xp = a.X + ((size_t)p * n + e) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(ldE(pf[e], n))));
+  __syncthreads();
+  // rows per lane: 200 KB of shared memory hold n <= 55 (QD) / 78 (DD)
+  constexpr int R = (L == 4) ? 2 : 3;
+  PHC_CHECK(n <= 32 * R);
+  if (wid == 0) {
+    C c[R];
+    sweep_warp<L, R>(n, lane, [&](int r, int j) { return ldE(pf[r], j); }, [&](int r) { return ldE(pf[r], n); }, c);
+    NEWTON_T(0, 3, p == 0 && tid == 0)
+    // z := z + dz
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      const int e = lane + 32 * q;
+      if (e < n) {
+        const double* xp = a.X + ((size_t)p * n + e) * cd;
+        cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(c[q])));
+      }
+    }
   }
   if (tid == 0) a.status[p] = 0;
 }
@@ -345,7 +431,6 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
   for (int o = 16; o; o >>= 1) rmax = nan_max(rmax, __shfl_xor_sync(0xffffffffu, rmax, o));
   if (lane == 0) a.resid[p] = rmax;
   __syncwarp();
-  C inv_diag = P::zero();  // lane i keeps 1 / U[i][i] for the back substitution
   for (int k = 0; k < n; ++k) {
     double best = -1.0;
     int bi = n;
@@ -372,9 +457,9 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
       }
     __syncwarp();
     const C inv = recip_warp<L>(ldE(k, k), lane);
-    if (lane == k) inv_diag = inv;
     if (lane > k && lane < n) stE(lane, k, emul<L>(ldE(lane, k), inv));
     __syncwarp();
+    if (lane == 0) stE(k, k, inv);  // U[k][k] is not read again: its slot keeps d_k = 1 / U[k][k]
     // trailing update spread over the lanes by (row, column) pairs: ceil((n-k-1)(n-k) / 32)
     // entries per lane instead of a whole row of n-k entries
     const int w = n - k;  // columns k+1 .. n
@@ -385,17 +470,17 @@ __global__ void __launch_bounds__(128) newton_warp_kernel(const NewtonArgs a) {
     }
     __syncwarp();
   }
-  // back substitution, column oriented as in newton_solve_kernel
-  for (int i = n - 1; i >= 0; --i) {
-    if (lane == i) stE(i, n, emul<L>(ldE(i, n), inv_diag));
-    __syncwarp();
-    const C xi = ldE(i, n);
-    if (lane < i) stE(lane, n, efms<L>(ldE(lane, n), ldE(lane, i), xi));
-    __syncwarp();
+  // back substitution, row-scaled as in newton_solve_kernel (d_r on the diagonal)
+  for (int e = lane; e < n * cols; e += 32) {
+    const int r = e / cols, j = e % cols;
+    if (j > r) stE(r, j, emul<L>(ldE(r, j), ldE(r, r)));
   }
+  __syncwarp();
+  C c[1];
+  sweep_warp<L, 1>(n, lane, [&](int r, int j) { return ldE(r, j); }, [&](int r) { return ldE(r, n); }, c);
   if (lane < n) {
     const double* xp = a.X + ((size_t)p * n + lane) * cd;
-    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), enorm<L>(ldE(lane, n))));
+    cstore<L>(a.Xnew + ((size_t)p * n + lane) * cd, P::add(cload_rw<L>(xp), enorm<L>(c[0])));
   }
   if (lane == 0) a.status[p] = 0;
 }
@@ -536,11 +621,16 @@ __global__ void __launch_bounds__(256) newton_backsub_kernel(const NewtonArgs a)
   double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
   double* invd = M + (size_t)n * cols * cd;
   auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
-  for (int i = n - 1; i >= 0; --i) {
-    if (tid == 0) sstore<L>(at(i, n), emul<L>(sload<L>(at(i, n)), sload<L>(invd + (size_t)i * cd)));
-    __syncthreads();
-    const C xi = sload<L>(at(i, n));
-    for (int r = tid; r < i; r += T) sstore<L>(at(r, n), efms<L>(sload<L>(at(r, n)), sload<L>(at(r, i)), xi));
+  // row-scaled back substitution (sweep_warp's operations and order): scale, then one block
+  // barrier per row with c in column n
+  for (int e = tid; e < n * cols; e += T) {
+    const int r = e / cols, j = e % cols;
+    if (j > r) sstore<L>(at(r, j), emul<L>(sload<L>(at(r, j)), sload<L>(invd + (size_t)r * cd)));
+  }
+  __syncthreads();
+  for (int j = n - 1; j >= 1; --j) {
+    const C xj = sload<L>(at(j, n));
+    for (int r = tid; r < j; r += T) sstore<L>(at(r, n), efms<L>(sload<L>(at(r, n)), sload<L>(at(r, j)), xj));
     __syncthreads();
   }
   for (int e = tid; e < n; e += T) {
@@ -688,6 +778,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
   };
   for (int64_t p = 0; p < a.n_points; ++p) {
     double* M = a.Mg + (size_t)p * ((size_t)n * cols + n) * cd;
+    NEWTON_T(1, 0, p == 0 && b == 0 && tid == 0)
     double* invd = M + (size_t)n * cols * cd;
     auto at = [&](int r, int c) { return M + ((size_t)r * cols + c) * cd; };
     const double* Fp = a.F + (size_t)p * n * cd;
@@ -738,6 +829,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
       if (!s_bad) multipliers(M, 0);
     }
     grid.sync();
+    NEWTON_T(1, 1, p == 0 && b == 0 && tid == 0)
     for (int k = 0; k < n - 1; ++k) {
       if (b == 0) {
         if (s_bad) break;
@@ -792,23 +884,45 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
       grid.sync();
       COOP_T(k, 5)
     }
-    if (b == 0) {
-      if (s_bad) {
+    NEWTON_T(1, 2, p == 0 && b == 0 && tid == 0)
+    // singular or not, grid-uniform: every column's flag was set before a grid barrier
+    __syncthreads();
+    if (tid == 0) s_bad = __ldcg(flag_g) | __ldcg(flag_g + 1);
+    __syncthreads();
+    if (s_bad) {
+      if (b == 0) {
         if (tid == 0) a.status[p] = 1;
         for (int e = tid; e < n; e += T)
           cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, cload_rw<L>(a.X + ((size_t)p * n + e) * cd));
-      } else {
-        for (int i = n - 1; i >= 0; --i) {
-          if (tid == 0) sstore<L>(at(perm[i], n), cmul_c<L>(ldl2<L>(at(perm[i], n)), ldl2<L>(invd + (size_t)i * cd)));
-          __syncthreads();
-          const C xi = ldl2<L>(at(perm[i], n));
-          for (int r = tid; r < i; r += T)
-            sstore<L>(at(perm[r], n), cfms_c<L>(ldl2<L>(at(perm[r], n)), ldl2<L>(at(perm[r], i)), xi));
+      }
+    } else {
+      // row-scaled back substitution (sweep_warp's operations and order): the scaling pass
+      // spread over the grid, then CTA 0 sweeps with c in shared memory, one barrier per row
+      if (b != 0)
+        for (int i = tid; i < n; i += T) perm[i] = __ldcg(perm_g + (size_t)((n - 1) & 1) * n + i);
+      __syncthreads();
+      for (int64_t e = (int64_t)b * T + tid; e < (int64_t)n * cols; e += (int64_t)G * T) {
+        const int r = (int)(e / cols), j = (int)(e % cols);
+        if (j > r) {
+          double* q = at(perm[r], j);
+          sstore<L>(q, cmul_c<L>(ldl2<L>(q), ldl2<L>(invd + (size_t)r * cd)));
+        }
+      }
+      grid.sync();
+      if (b == 0) {
+        double* cv = colv;  // c by logical row
+        for (int r = tid; r < n; r += T) sstore<L>(cv + (size_t)r * cd, ldl2<L>(at(perm[r], n)));
+        __syncthreads();
+        for (int j = n - 1; j >= 1; --j) {
+          const C xj = sload<L>(cv + (size_t)j * cd);
+          for (int r = tid; r < j; r += T)
+            sstore<L>(cv + (size_t)r * cd, cfms_c<L>(sload<L>(cv + (size_t)r * cd), ldl2<L>(at(perm[r], j)), xj));
           __syncthreads();
         }
+        NEWTON_T(1, 3, p == 0 && tid == 0)
         for (int e = tid; e < n; e += T) {
           const double* xp = a.X + ((size_t)p * n + e) * cd;
-          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(ldl2<L>(at(perm[e], n)))));
+          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(sload<L>(cv + (size_t)e * cd))));
         }
         if (tid == 0) a.status[p] = 0;
       }

@@ -18,6 +18,11 @@ __global__ void lat(double* out, long long* cyc, int reps) {
     if constexpr (OP == 1) x = P::mul(x, y);
     if constexpr (OP == 2) x = P::add(x, y);
     if constexpr (OP == 3) x = P::sub(x, P::mul(x, y));
+    if constexpr (OP == 4) x.re = P::rdiv(y.re, x.re);
+    if constexpr (OP == 5) x.re.x[0] = __ddiv_rn(y.re.x[0], x.re.x[0]);
+    if constexpr (OP == 6) x.re.x[0] = __drcp_rn(x.re.x[0]);
+    if constexpr (OP == 7) x.re = P::abs2(x);
+    if constexpr (OP == 8) x.re.x[0] = __dmul_rn(x.re.x[0], y.re.x[0]);
   }
   long long t1 = clock64();
   out[0] = x.re.x[0] + x.im.x[0];
@@ -29,13 +34,14 @@ int main() {
   long long* c;
   cudaMalloc(&o, 8);
   cudaMalloc(&c, 8);
-  const char* names[] = {"recip", "mul", "add", "x - x*y"};
+  const char* names[] = {"recip", "mul", "add", "x - x*y", "rdiv", "ddiv", "drcp", "abs2", "dmul"};
   long long h;
 #define RUN(L, OP)                                  \
   lat<L, OP><<<1, 1>>>(o, c, 64);                   \
   lat<L, OP><<<1, 1>>>(o, c, 256);                  \
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);     \
   printf("L=%d %-8s %lld cycles\n", L, names[OP], h);
-  RUN(2, 0) RUN(2, 1) RUN(2, 2) RUN(2, 3) RUN(4, 0) RUN(4, 1) RUN(4, 2) RUN(4, 3)
+  RUN(2, 0) RUN(2, 1) RUN(2, 2) RUN(2, 3) RUN(2, 4) RUN(2, 7) RUN(4, 0) RUN(4, 1) RUN(4, 2) RUN(4, 3) RUN(4, 4) RUN(4, 7)
+  RUN(2, 5) RUN(2, 6) RUN(2, 8)
   return 0;
 }
