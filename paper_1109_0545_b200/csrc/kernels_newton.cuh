@@ -155,6 +155,60 @@ PHC_DEV void sweep_warp(int n, int lane, LdN ldN, LdC ldC, typename Prec<L>::C (
   }
 }
 
+// Component h (0: real, 1: imaginary) of a complex product or update on its own lane.  With
+// -i z = (z.im, -z.re) (exact), im(c - a b) = re((-i c) - a (-i b)) and im(a b) = re(a (-i b)):
+// the real part of the same operation on rotated operands.  Every product in it pairs two
+// negated factors or none, and round-to-nearest is sign-symmetric, so the component is bitwise
+// the full operation's; the unused imaginary half is dead code after inlining.  Two lanes per
+// entry halve the instructions a lane issues on the elimination's serial chain.
+template <int L>
+PHC_DEV typename Prec<L>::C rot_if(const typename Prec<L>::C& z, bool h) {
+  typename Prec<L>::C r;
+#pragma unroll
+  for (int i = 0; i < L; ++i) {
+    r.re.x[i] = h ? z.im.x[i] : z.re.x[i];
+    r.im.x[i] = h ? -z.re.x[i] : z.im.x[i];
+  }
+  return r;
+}
+template <int L>
+PHC_DEV typename Prec<L>::C cpart(const typename Prec<L>::real& x) {
+  typename Prec<L>::C r;
+  r.re = x;
+  r.im = x;  // not read: only the real part of results built from it is used
+  return r;
+}
+// sweep_warp with two lanes per row (lane t: row t / 2, component t & 1; R2 slots per lane,
+// 2n <= 32 R2), bitwise sweep_warp's result.  ldC(r, h) reads component h of the scaled c_r.
+template <int L, int R2, class LdN, class LdC>
+PHC_DEV void sweep_warp2(int n, int lane, LdN ldN, LdC ldC, typename Prec<L>::real (&c)[R2]) {
+  using C = typename Prec<L>::C;
+  using real = typename Prec<L>::real;
+#pragma unroll
+  for (int q = 0; q < R2; ++q) {
+    const int t = lane + 32 * q;
+    if (t < 2 * n) c[q] = ldC(t >> 1, t & 1);
+  }
+  for (int j = n - 1; j >= 1; --j) {
+    const int oq = (2 * j) >> 5, ol = (2 * j) & 31;  // x_j.re on lane ol, x_j.im on ol + 1
+    real src = c[0];
+#pragma unroll
+    for (int q = 1; q < R2; ++q)
+      if (oq == q) src = c[q];
+    C xj;
+#pragma unroll
+    for (int i = 0; i < L; ++i) {
+      xj.re.x[i] = __shfl_sync(0xffffffffu, src.x[i], ol);
+      xj.im.x[i] = __shfl_sync(0xffffffffu, src.x[i], ol + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < R2; ++q) {
+      const int t = lane + 32 * q, r = t >> 1;
+      if (r < j) c[q] = efms<L>(cpart<L>(c[q]), ldN(r, j), rot_if<L>(xj, t & 1)).re;
+    }
+  }
+}
+
 struct NewtonArgs {
   const double* X;  // [P][n][2][L]
   const double* F;  // [P][n][2][L]
@@ -231,6 +285,22 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
   int* pbuf = reinterpret_cast<int*>(invd + (size_t)n * cd);  // [2][n] row permutations
   auto ldE = [&](int r, int c) { return plane_ld<L>(Mre, Mim, ((size_t)r * cols + c) * L); };
   auto stE = [&](int r, int c, const C& v) { plane_st<L>(Mre, Mim, ((size_t)r * cols + c) * L, v); };
+  auto st_part = [&](int r, int c, int h, const typename P::real& v) {
+    double* q = (h ? Mim : Mre) + ((size_t)r * cols + c) * L;
+#pragma unroll
+    for (int i = 0; i < L; i += 2) *reinterpret_cast<double2*>(q + i) = make_double2(v.x[i], v.x[i + 1]);
+  };
+  auto ld_part = [&](int r, int c, int h) {
+    const double* q = (h ? Mim : Mre) + ((size_t)r * cols + c) * L;
+    typename P::real v;
+#pragma unroll
+    for (int i = 0; i < L; i += 2) {
+      const double2 x = *reinterpret_cast<const double2*>(q + i);
+      v.x[i] = x.x;
+      v.x[i + 1] = x.y;
+    }
+    return v;
+  };
   NEWTON_T(0, 0, p == 0 && tid == 0)
   const double* Fp = a.F + (size_t)p * n * cd;
   const double* Jp = a.J + (size_t)p * n * n * cd;
@@ -289,9 +359,22 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     NEWTON_C(k, 0, p == 0 && tid == 0)
     if (wid == 0) {
       // look-ahead: column k+1 of the rows below k, then its pivot, exchange, multipliers
-      const C pk = ldE(pc[k], k + 1);
-      for (int i = k + 1 + lane; i < n; i += 32)
-        stE(pc[i], k + 1, efms<L>(ldE(pc[i], k + 1), ldE(pc[i], k), pk));
+      if constexpr (L == 4) {
+        // QD: one component per lane (rot_if; measured 1.14 -> 1.00 us per column for c3;
+        // DD lost 0.07 us per column this way and keeps one entry per lane)
+        const C pkh = rot_if<L>(ldE(pc[k], k + 1), lane & 1);
+        for (int t0 = 0; t0 < 2 * (n - k - 1); t0 += 32) {
+          const int t = t0 + lane, i = k + 1 + (t >> 1), h = t & 1;
+          typename P::real v;
+          if (i < n) v = efms<L>(cpart<L>(ld_part(pc[i], k + 1, h)), ldE(pc[i], k), pkh).re;
+          __syncwarp();  // the pair's loads of the entry precede its stores
+          if (i < n) st_part(pc[i], k + 1, h, v);
+        }
+      } else {
+        const C pk = ldE(pc[k], k + 1);
+        for (int i = k + 1 + lane; i < n; i += 32)
+          stE(pc[i], k + 1, efms<L>(ldE(pc[i], k + 1), ldE(pc[i], k), pk));
+      }
       __syncwarp();
       NEWTON_C(k, 1, p == 0 && lane == 0)
       if (!pivot_column(pc, pn, k + 1) && lane == 0) s_bad[(k + 1) & 1] = 1;
@@ -328,20 +411,44 @@ __global__ void __launch_bounds__(512) newton_solve_kernel(const NewtonArgs a) {
     if (j > r) stE(pf[r], j, emul<L>(ldE(pf[r], j), sload<L>(invd + (size_t)r * cd)));
   }
   __syncthreads();
-  // rows per lane: 200 KB of shared memory hold n <= 55 (QD) / 78 (DD)
-  constexpr int R = (L == 4) ? 2 : 3;
-  PHC_CHECK(n <= 32 * R);
-  if (wid == 0) {
-    C c[R];
-    sweep_warp<L, R>(n, lane, [&](int r, int j) { return ldE(pf[r], j); }, [&](int r) { return ldE(pf[r], n); }, c);
-    NEWTON_T(0, 3, p == 0 && tid == 0)
-    // z := z + dz
+  // QD: half-rows per lane (n <= 55 fits 200 KB of shared memory; c3 sweep 51 -> 45 us);
+  // DD: whole rows (n <= 78)
+  if constexpr (L == 2) {
+    constexpr int R = 3;
+    PHC_CHECK(n <= 32 * R);
+    if (wid == 0) {
+      C c[R];
+      sweep_warp<L, R>(n, lane, [&](int r, int j) { return ldE(pf[r], j); }, [&](int r) { return ldE(pf[r], n); }, c);
+      NEWTON_T(0, 3, p == 0 && tid == 0)
 #pragma unroll
-    for (int q = 0; q < R; ++q) {
-      const int e = lane + 32 * q;
+      for (int q = 0; q < R; ++q) {
+        const int e = lane + 32 * q;
+        if (e < n) {
+          const double* xp = a.X + ((size_t)p * n + e) * cd;
+          cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(c[q])));
+        }
+      }
+    }
+  } else if (wid == 0) {
+    constexpr int R2 = 4;
+    PHC_CHECK(2 * n <= 32 * R2);
+    typename P::real c[R2];
+    sweep_warp2<L, R2>(n, lane, [&](int r, int j) { return ldE(pf[r], j); },
+                       [&](int r, int h) { return ld_part(pf[r], n, h); }, c);
+    NEWTON_T(0, 3, p == 0 && tid == 0)
+    // z := z + dz, one component per lane
+#pragma unroll
+    for (int q = 0; q < R2; ++q) {
+      const int t = lane + 32 * q, e = t >> 1, h = t & 1;
       if (e < n) {
-        const double* xp = a.X + ((size_t)p * n + e) * cd;
-        cstore<L>(a.Xnew + ((size_t)p * n + e) * cd, P::add(cload_rw<L>(xp), enorm<L>(c[q])));
+        double* xo = a.Xnew + ((size_t)p * n + e) * cd + h * L;
+        const double* xp = a.X + ((size_t)p * n + e) * cd + h * L;
+        typename P::real xv;
+#pragma unroll
+        for (int i = 0; i < L; ++i) xv.x[i] = xp[i];
+        const typename P::real v = P::add(cpart<L>(xv), enorm<L>(cpart<L>(c[q]))).re;
+#pragma unroll
+        for (int i = 0; i < L; ++i) xo[i] = v.x[i];
       }
     }
   }
