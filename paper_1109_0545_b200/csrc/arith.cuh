@@ -376,6 +376,32 @@ PHC_DEV qd qd_mul_d(const qd& a, double s) {
   const double s3 = add_(add_(p3, e2), add_(e1, t1));
   return renorm5(p0, s1, p2, s3, 0.0);
 }
+// The same long divisions with each quotient digit formed as r_0 * (1 / b_0) -- one
+// correctly rounded reciprocal (__drcp_rn) and a DMUL per digit instead of a DDIV per digit.
+// A digit may be off by an ulp more; the remainders stay exact as before, so the next digit
+// absorbs it and the last digit's error is ~2^-52 of a remainder already ~2^-104 (DD) /
+// ~2^-208 (QD) of the quotient.
+PHC_DEV dd dd_div_rc(const dd& a, const dd& b) {
+  const double rc = __drcp_rn(b.x[0]);
+  const double q1 = mul_(a.x[0], rc);
+  dd r = dd_sub(a, dd_mul_d(b, q1));
+  const double q2 = mul_(r.x[0], rc);
+  r = dd_sub(r, dd_mul_d(b, q2));
+  const double q3 = mul_(r.x[0], rc);
+  dd q;
+  quick_two_sum(q1, q2, q.x[0], q.x[1]);
+  return dd_add(q, dd_make(q3, 0.0));
+}
+PHC_DEV qd qd_div_rc(const qd& a, const qd& b) {
+  const double rc = __drcp_rn(b.x[0]);
+  double q[5];
+  qd r = a;
+  for (int j = 0; j < 5; ++j) {
+    q[j] = mul_(r.x[0], rc);
+    if (j < 4) r = qd_sub(r, qd_mul_d(b, q[j]));
+  }
+  return renorm5(q[0], q[1], q[2], q[3], q[4]);
+}
 PHC_DEV qd qd_div(const qd& a, const qd& b) {
   double q[5];
   qd r = a;
@@ -443,7 +469,7 @@ template <> struct Prec<2> {
   PHC_DEV static real radd(const real& a, const real& b) { return dd_add(a, b); }
   PHC_DEV static real rsub(const real& a, const real& b) { return dd_sub(a, b); }
   PHC_DEV static real rmul(const real& a, const real& b) { return dd_mul(a, b); }
-  PHC_DEV static real rdiv(const real& a, const real& b) { return dd_div(a, b); }
+  PHC_DEV static real rdiv(const real& a, const real& b) { return dd_div_rc(a, b); }
   PHC_DEV static void rstore(double* p, const real& a) { p[0] = a.x[0]; p[1] = a.x[1]; }
   // fused complex DD product: each real part is a 2-term dot product accumulated
   // in one error term, with one renormalisation (normwise error ~ u^2 |a||b|).
@@ -507,8 +533,8 @@ template <> struct Prec<2> {
   PHC_DEV static C recip(const C& a) {
     const dd d = abs2(a);
     C r;
-    r.re = dd_div(a.re, d);
-    r.im = dd_neg(dd_div(a.im, d));
+    r.re = dd_div_rc(a.re, d);
+    r.im = dd_neg(dd_div_rc(a.im, d));
     return r;
   }
   // |a|^2 from the leading limbs (pivot selection only)
@@ -530,7 +556,7 @@ template <> struct Prec<4> {
   PHC_DEV static real radd(const real& a, const real& b) { return qd_add(a, b); }
   PHC_DEV static real rsub(const real& a, const real& b) { return qd_sub(a, b); }
   PHC_DEV static real rmul(const real& a, const real& b) { return qd_mul(a, b); }
-  PHC_DEV static real rdiv(const real& a, const real& b) { return qd_div(a, b); }
+  PHC_DEV static real rdiv(const real& a, const real& b) { return qd_div_rc(a, b); }
   PHC_DEV static void rstore(double* p, const real& a) { for (int i = 0; i < 4; ++i) p[i] = a.x[i]; }
   // fused complex QD product: each real part is a QD dot product x*y + z*w evaluated in
   // one pass (qd_dot2), instead of two qd_mul and a qd_add (~440 vs ~680 FP64 instructions).
@@ -600,8 +626,8 @@ template <> struct Prec<4> {
   PHC_DEV static C recip(const C& a) {
     const qd d = abs2(a);
     C r;
-    r.re = qd_div(a.re, d);
-    r.im = qd_neg(qd_div(a.im, d));
+    r.re = qd_div_rc(a.re, d);
+    r.im = qd_neg(qd_div_rc(a.im, d));
     return r;
   }
   PHC_DEV static double abs2_hi(const C& a) { return a.re.x[0] * a.re.x[0] + a.im.x[0] * a.im.x[0]; }

@@ -1019,10 +1019,16 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
       if (b == 0) {
         double* cv = colv;  // c by logical row
         for (int r = tid; r < n; r += T) sstore<L>(cv + (size_t)r * cd, ldl2<L>(at(perm[r], n)));
+        // N[tid][j] of the next step is fetched one step ahead (its L2 latency off the chain)
+        const int ph0 = tid < n ? perm[tid] : 0;
+        C nx = tid < n - 1 ? ldl2<L>(at(ph0, n - 1)) : P::zero();
         __syncthreads();
         for (int j = n - 1; j >= 1; --j) {
           const C xj = sload<L>(cv + (size_t)j * cd);
-          for (int r = tid; r < j; r += T)
+          const C nj = nx;
+          if (tid < j - 1) nx = ldl2<L>(at(ph0, j - 1));
+          if (tid < j) sstore<L>(cv + (size_t)tid * cd, cfms_c<L>(sload<L>(cv + (size_t)tid * cd), nj, xj));
+          for (int r = tid + T; r < j; r += T)
             sstore<L>(cv + (size_t)r * cd, cfms_c<L>(sload<L>(cv + (size_t)r * cd), ldl2<L>(at(perm[r], j)), xj));
           __syncthreads();
         }

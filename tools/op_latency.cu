@@ -23,6 +23,11 @@ __global__ void lat(double* out, long long* cyc, int reps) {
     if constexpr (OP == 6) x.re.x[0] = __drcp_rn(x.re.x[0]);
     if constexpr (OP == 7) x.re = P::abs2(x);
     if constexpr (OP == 8) x.re.x[0] = __dmul_rn(x.re.x[0], y.re.x[0]);
+    if constexpr (OP == 9) {
+      if constexpr (L == 2) x.re = dd_div_rc(y.re, x.re);
+      else x.re = qd_div_rc(y.re, x.re);
+    }
+    if constexpr (OP == 10) x.re.x[0] = __ddiv_rn(y.re.x[0], x.re.x[0] + 1e-300 * i);
   }
   long long t1 = clock64();
   out[0] = x.re.x[0] + x.im.x[0];
@@ -34,7 +39,7 @@ int main() {
   long long* c;
   cudaMalloc(&o, 8);
   cudaMalloc(&c, 8);
-  const char* names[] = {"recip", "mul", "add", "x - x*y", "rdiv", "ddiv", "drcp", "abs2", "dmul"};
+  const char* names[] = {"recip", "mul", "add", "x - x*y", "rdiv", "ddiv", "drcp", "abs2", "dmul", "rdiv_rc", "ddiv2"};
   long long h;
 #define RUN(L, OP)                                  \
   lat<L, OP><<<1, 1>>>(o, c, 64);                   \
@@ -42,6 +47,6 @@ int main() {
   cudaMemcpy(&h, c, 8, cudaMemcpyDeviceToHost);     \
   printf("L=%d %-8s %lld cycles\n", L, names[OP], h);
   RUN(2, 0) RUN(2, 1) RUN(2, 2) RUN(2, 3) RUN(2, 4) RUN(2, 7) RUN(4, 0) RUN(4, 1) RUN(4, 2) RUN(4, 3) RUN(4, 4) RUN(4, 7)
-  RUN(2, 5) RUN(2, 6) RUN(2, 8)
+  RUN(2, 5) RUN(2, 6) RUN(2, 8) RUN(2, 9) RUN(4, 9) RUN(2, 10)
   return 0;
 }
