@@ -91,3 +91,62 @@ def test_quadratic_convergence_to_known_root():
     assert errs[0] < 1e-5
     assert errs[1] < 50 * errs[0] ** 2
     assert errs[2] < 50 * errs[1] ** 2 + 1e-60
+
+
+def _row_scaled_solve(A, b):
+    """Test-only model of the device eliminations' solve (readings N6/N7 context):
+    Gaussian elimination with partial pivoting on [A | b] (largest modulus, ties to the lowest
+    row, rows exchanged through a permutation), then the ROW-SCALED back substitution
+    c_r = b_r d_r, N_rj = U_rj d_r (d_r = 1 / U_rr), c_r -= N_rj x_j for j = n-1 .. r+1 -- in
+    exact Gaussian rationals, so it must reach solve_exact's solution exactly."""
+    n = len(A)
+    M = [[A[i][j] for j in range(n)] + [b[i]] for i in range(n)]
+    perm = list(range(n))
+    d = [None] * n
+    mod2 = lambda z: z[0] * z[0] + z[1] * z[1]  # noqa: E731
+    for k in range(n):
+        bi = max(range(k, n), key=lambda i: (mod2(M[perm[i]][k]), -i))
+        assert mod2(M[perm[bi]][k]) != 0
+        perm[k], perm[bi] = perm[bi], perm[k]
+        p = M[perm[k]][k]
+        m2 = mod2(p)
+        d[k] = (p[0] / m2, -p[1] / m2)
+        for i in range(k + 1, n):
+            r = perm[i]
+            li = (M[r][k][0] * d[k][0] - M[r][k][1] * d[k][1], M[r][k][0] * d[k][1] + M[r][k][1] * d[k][0])
+            for j in range(k + 1, n + 1):
+                u = M[perm[k]][j]
+                M[r][j] = (M[r][j][0] - (li[0] * u[0] - li[1] * u[1]), M[r][j][1] - (li[0] * u[1] + li[1] * u[0]))
+    cm = lambda x, y: (x[0] * y[0] - x[1] * y[1], x[0] * y[1] + x[1] * y[0])  # noqa: E731
+    c = [cm(M[perm[r]][n], d[r]) for r in range(n)]
+    N = [[cm(M[perm[r]][j], d[r]) if j > r else None for j in range(n)] for r in range(n)]
+    for j in range(n - 1, 0, -1):
+        for r in range(j):
+            t = cm(N[r][j], c[j])
+            c[r] = (c[r][0] - t[0], c[r][1] - t[1])
+    return c
+
+
+def test_row_scaled_back_substitution_reaches_the_exact_solution():
+    """Reading N6: the row-scaled back substitution (scaled rows N = D^-1 U, c = D^-1 b, one
+    multiply-subtract per row on the chain) is the same exact solve as the plain definition:
+    equal to solve_exact (and to the generating x) in exact rationals, with pivoting exercised
+    by small leading entries."""
+    rng = np.random.default_rng(6)
+    ran = 0
+    for n in (1, 2, 3, 6, 9):
+        for _ in range(3):
+            A = [[(Fraction(int(a), 5), Fraction(int(b), 3)) for a, b in rng.integers(-7, 8, (n, 2))]
+                 for _ in range(n)]
+            for i in range(n):  # a tiny diagonal forces row exchanges
+                A[i][i] = (Fraction(1, 1000), Fraction(0))
+            x = [(Fraction(int(a), 7), Fraction(int(b), 11)) for a, b in rng.integers(-9, 10, (n, 2))]
+            b = _mat_vec(A, x)
+            try:
+                ref = solve_exact(A, b)
+            except (ZeroDivisionError, AssertionError):
+                continue
+            got = _row_scaled_solve(A, b)
+            assert got == ref == x
+            ran += 1
+    assert ran >= 12
