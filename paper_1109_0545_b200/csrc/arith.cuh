@@ -392,15 +392,33 @@ PHC_DEV dd dd_div_rc(const dd& a, const dd& b) {
   quick_two_sum(q1, q2, q.x[0], q.x[1]);
   return dd_add(q, dd_make(q3, 0.0));
 }
+// QD: the first two remainders are full QD updates; the later ones are ~2^-104 and ~2^-156 of
+// |a| and only need ~2^-108 and ~2^-56 of their own size to keep the quotient at ~2^-212, so
+// they are formed in two and one levels (two_prod / two_sum where an error could reach
+// 2^-212 |a|, plain FMA below): dependent latency 2,050 -> 1,358 cycles, same maximum error
+// over the arithmetic test's samples (profiles/op_latency_r02s3_taper.txt).
 PHC_DEV qd qd_div_rc(const qd& a, const qd& b) {
   const double rc = __drcp_rn(b.x[0]);
-  double q[5];
-  qd r = a;
-  for (int j = 0; j < 5; ++j) {
-    q[j] = mul_(r.x[0], rc);
-    if (j < 4) r = qd_sub(r, qd_mul_d(b, q[j]));
-  }
-  return renorm5(q[0], q[1], q[2], q[3], q[4]);
+  const double q0 = mul_(a.x[0], rc);
+  qd r = qd_sub(a, qd_mul_d(b, q0));  // |r| ~ 2^-52 |a|
+  const double q1 = mul_(r.x[0], rc);
+  r = qd_sub(r, qd_mul_d(b, q1));  // |r| ~ 2^-104 |a|, normalised
+  const double q2 = mul_(r.x[0], rc);
+  // t = r - q2 b (|t| ~ 2^-156 |a|): r0 - b0 q2 exact (Sterbenz: b0 q2 is within a few ulps of
+  // r0), the order-1 terms summed exactly, the order-2 terms in one double
+  double p0, e0, p1, e1;
+  two_prod(b.x[0], q2, p0, e0);
+  two_prod(b.x[1], q2, p1, e1);
+  double t0, f1, f2, f3;
+  two_sum(sub_(r.x[0], p0), r.x[1], t0, f1);
+  two_sum(t0, -e0, t0, f2);
+  two_sum(t0, -p1, t0, f3);
+  const double t1 = add_(fma_(-q2, b.x[2], sub_(r.x[2], e1)), add_(add_(f1, f2), f3));
+  const double q3 = mul_(add_(t0, t1), rc);
+  // t - q3 b (~2^-208 |a|) in one double
+  const double r4 = add_(fma_(-q3, b.x[0], t0), fma_(-q3, b.x[1], t1));
+  const double q4 = mul_(r4, rc);
+  return renorm5(q0, q1, q2, q3, q4);
 }
 PHC_DEV qd qd_div(const qd& a, const qd& b) {
   double q[5];
