@@ -829,6 +829,7 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
   __shared__ double red_v[32];
   __shared__ int red_i[32];
   __shared__ int s_bad;
+  __shared__ int s_front;  // back substitution: lowest logical row whose x is published
   __shared__ __align__(16) double s_inv[2 * L];
   const int tid = threadIdx.x, T = blockDim.x, lane = tid & 31, wid = tid >> 5, nwarp = T >> 5;
   const int G = gridDim.x, b = blockIdx.x;
@@ -1018,19 +1019,70 @@ __global__ void __launch_bounds__(kCoopThreads) newton_coop_kernel(const NewtonA
       grid.sync();
       if (b == 0) {
         double* cv = colv;  // c by logical row
-        for (int r = tid; r < n; r += T) sstore<L>(cv + (size_t)r * cd, ldl2<L>(at(perm[r], n)));
-        // N[tid][j] of the next step is fetched one step ahead (its L2 latency off the chain)
-        const int ph0 = tid < n ? perm[tid] : 0;
-        C nx = tid < n - 1 ? ldl2<L>(at(ph0, n - 1)) : P::zero();
-        __syncthreads();
-        for (int j = n - 1; j >= 1; --j) {
-          const C xj = sload<L>(cv + (size_t)j * cd);
-          const C nj = nx;
-          if (tid < j - 1) nx = ldl2<L>(at(ph0, j - 1));
-          if (tid < j) sstore<L>(cv + (size_t)tid * cd, cfms_c<L>(sload<L>(cv + (size_t)tid * cd), nj, xj));
-          for (int r = tid + T; r < j; r += T)
-            sstore<L>(cv + (size_t)r * cd, cfms_c<L>(sload<L>(cv + (size_t)r * cd), ldl2<L>(at(perm[r], j)), xj));
+        if (n <= T) {
+          // One row per thread, no block barrier per row: warp w holds rows [32w, 32w+32) in
+          // registers, applies x_j of the rows above it as they are published (phase 1, j
+          // descending), then sweeps its own rows with shuffles and publishes each x_j when it
+          // is final (phase 2).  Only the critical row waits: the chain is one efms per row
+          // plus one publication per warp.  Per row the same operations in the same order.
+          volatile int* vfront = &s_front;  // x_j published <=> front <= j (decreasing)
+          if (tid == 0) *vfront = n;
+          const int r = tid, lo = wid * 32, hi = min(lo + 32, n) - 1;
+          const int ph = r < n ? perm[r] : 0;
+          C c = r < n ? ldl2<L>(at(ph, n)) : P::zero();
           __syncthreads();
+          if (lo < n) {
+            // N[r][j] is fetched one step ahead through both phases (L2 latency off the chain)
+            C nx = (r < n - 1) ? ldl2<L>(at(ph, n - 1)) : P::zero();
+            for (int j = n - 1; j > hi; --j) {  // phase 1: rows of the warps above
+              if (lane == 0)
+                while (*vfront > j) {
+                }
+              __syncwarp();
+              __threadfence_block();
+              const C xj = sload<L>(cv + (size_t)j * cd);
+              const C nj = nx;
+              if (r < j - 1) nx = ldl2<L>(at(ph, j - 1));
+              if (r < n) c = cfms_c<L>(c, nj, xj);
+            }
+            for (int j = hi; j >= lo && j >= 1; --j) {  // phase 2: this warp's rows
+              const C nj = nx;
+              if (r < j - 1) nx = ldl2<L>(at(ph, j - 1));
+              C xj;
+#pragma unroll
+              for (int i = 0; i < L; ++i) {
+                xj.re.x[i] = __shfl_sync(0xffffffffu, c.re.x[i], j - lo);
+                xj.im.x[i] = __shfl_sync(0xffffffffu, c.im.x[i], j - lo);
+              }
+              if (lane == j - lo) {
+                sstore<L>(cv + (size_t)j * cd, c);
+                __threadfence_block();
+                *vfront = j;
+              }
+              if (r < j) c = cfms_c<L>(c, nj, xj);
+            }
+            if (lane == 0) {  // row lo is final
+              sstore<L>(cv + (size_t)lo * cd, c);
+              __threadfence_block();
+              *vfront = lo;
+            }
+          }
+          __syncthreads();
+        } else {
+          for (int r = tid; r < n; r += T) sstore<L>(cv + (size_t)r * cd, ldl2<L>(at(perm[r], n)));
+          // N[tid][j] of the next step is fetched one step ahead (its L2 latency off the chain)
+          const int ph0 = tid < n ? perm[tid] : 0;
+          C nx = tid < n - 1 ? ldl2<L>(at(ph0, n - 1)) : P::zero();
+          __syncthreads();
+          for (int j = n - 1; j >= 1; --j) {
+            const C xj = sload<L>(cv + (size_t)j * cd);
+            const C nj = nx;
+            if (tid < j - 1) nx = ldl2<L>(at(ph0, j - 1));
+            if (tid < j) sstore<L>(cv + (size_t)tid * cd, cfms_c<L>(sload<L>(cv + (size_t)tid * cd), nj, xj));
+            for (int r = tid + T; r < j; r += T)
+              sstore<L>(cv + (size_t)r * cd, cfms_c<L>(sload<L>(cv + (size_t)r * cd), ldl2<L>(at(perm[r], j)), xj));
+            __syncthreads();
+          }
         }
         NEWTON_T(1, 3, p == 0 && tid == 0)
         for (int e = tid; e < n; e += T) {
