@@ -392,6 +392,9 @@ PHC_DEV dd dd_div_rc(const dd& a, const dd& b) {
   quick_two_sum(q1, q2, q.x[0], q.x[1]);
   return dd_add(q, dd_make(q3, 0.0));
 }
+#ifndef PHC_QD_DIV_TAPER2
+#define PHC_QD_DIV_TAPER2 1
+#endif
 // QD: the first two remainders are full QD updates; the later ones are ~2^-104 and ~2^-156 of
 // |a| and only need ~2^-108 and ~2^-56 of their own size to keep the quotient at ~2^-212, so
 // they are formed in two and one levels (two_prod / two_sum where an error could reach
@@ -402,7 +405,35 @@ PHC_DEV qd qd_div_rc(const qd& a, const qd& b) {
   const double q0 = mul_(a.x[0], rc);
   qd r = qd_sub(a, qd_mul_d(b, q0));  // |r| ~ 2^-52 |a|
   const double q1 = mul_(r.x[0], rc);
+#if PHC_QD_DIV_TAPER2
+  {
+    // r - q1 b (~2^-104 |a|, needed to ~2^-212 |a|): r0 - b0 q1 exact (Sterbenz), order-1 and
+    // order-2 terms summed exactly, order-3 terms in one FMA-rounded double; then made
+    // (nearly) normalised for the next digit's Sterbenz step
+    double p0, e0, p1, e1, p2, e2;
+    two_prod(b.x[0], q1, p0, e0);
+    two_prod(b.x[1], q1, p1, e1);
+    two_prod(b.x[2], q1, p2, e2);
+    double u0, f1, f2, f3, u1, g1, g2, g3, g4, g5;
+    two_sum(sub_(r.x[0], p0), r.x[1], u0, f1);
+    two_sum(u0, -e0, u0, f2);
+    two_sum(u0, -p1, u0, f3);
+    two_sum(r.x[2], -e1, u1, g1);
+    two_sum(u1, -p2, u1, g2);
+    two_sum(u1, f1, u1, g3);
+    two_sum(u1, f2, u1, g4);
+    two_sum(u1, f3, u1, g5);
+    const double u2 = add_(fma_(-q1, b.x[3], sub_(r.x[3], e2)), add_(add_(g1, g2), add_(add_(g3, g4), g5)));
+    double v0, v1, v2, v3;
+    two_sum(u0, u1, v0, v1);
+    two_sum(v1, u2, v1, v2);
+    two_sum(v0, v1, r.x[0], v3);
+    two_sum(v3, v2, r.x[1], r.x[2]);
+    r.x[3] = 0.0;
+  }
+#else
   r = qd_sub(r, qd_mul_d(b, q1));  // |r| ~ 2^-104 |a|, normalised
+#endif
   const double q2 = mul_(r.x[0], rc);
   // t = r - q2 b (|t| ~ 2^-156 |a|): r0 - b0 q2 exact (Sterbenz: b0 q2 is within a few ulps of
   // r0), the order-1 terms summed exactly, the order-2 terms in one double
